@@ -1,0 +1,471 @@
+"""Python mirror of the reference C++ API (proj/include/grasp/*.hpp).
+
+Names and argument meaning follow the reference: HandModel (hand.hpp:20-47),
+ObjectModel (object.hpp:19-25), RunConfig (config.hpp:77-88),
+init_poses / squeeze_pose / synthesize (pipeline.hpp:55-71), GraspRecord
+(records.hpp:29-44). All compute goes through the native library
+(include/grasp_b200.h); synthesize runs on a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import json
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _native as N
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+
+
+def dptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp) if a is not None else None
+
+
+def iptr(a: np.ndarray):
+    return a.ctypes.data_as(_ip) if a is not None else None
+
+
+# --------------------------------------------------------------------- config
+@dataclass
+class QpParams:
+    rho: float = 0.1
+    sigma: float = 1e-6
+    alpha: float = 1.6
+    max_iters: int = 500
+    eps_primal: float = 1e-5
+    eps_dual: float = 1e-5
+    check_interval: int = 10
+
+
+@dataclass
+class ContactParams:
+    mu: float = 0.6
+    n_edges: int = 8
+
+
+@dataclass
+class EnergyParams:
+    beta: float = 10.0
+    gamma_per_contact: float = 0.1
+
+
+@dataclass
+class ObjectiveWeights:
+    grasp: float = 1.0
+    distance: float = 100.0
+    joint_limit: float = 10.0
+    self_penetration: float = 10.0
+    object_penetration: float = 10.0
+
+
+@dataclass
+class StageSchedule:
+    iters: int = 300
+    step_rotation: float = 0.010
+    step_translation: float = 0.0025
+    step_joints: float = 0.010
+    step_floor: float = 0.1
+
+
+@dataclass
+class PipelineParams:
+    coarse: StageSchedule = field(default_factory=lambda: StageSchedule(300, 0.010, 0.0025, 0.010, 0.1))
+    fine: StageSchedule = field(default_factory=lambda: StageSchedule(100, 0.004, 0.0010, 0.004, 0.1))
+    final_stage: StageSchedule = field(default_factory=lambda: StageSchedule(100, 0.004, 0.0010, 0.004, 0.1))
+    contact_offset: float = 0.01
+    fd_step: float = 1e-6
+    skip_fine_stages: bool = False
+
+
+@dataclass
+class InitParams:
+    standoff: float = 0.10
+    joint_span_fraction: float = 0.25
+
+
+@dataclass
+class EvalParams:
+    mass: float = 0.03
+    gravity: float = 9.8
+    residual_rel_tol: float = 1e-3
+    force_budget_factor: float = 20.0
+    contact_tol: float = 0.002
+    penetration_tol: float = 0.003
+    qp_eps: float = 1e-8
+
+
+@dataclass
+class RunConfig:
+    qp: QpParams = field(default_factory=QpParams)
+    contact: ContactParams = field(default_factory=ContactParams)
+    energy: EnergyParams = field(default_factory=EnergyParams)
+    weights: ObjectiveWeights = field(default_factory=ObjectiveWeights)
+    pipeline: PipelineParams = field(default_factory=PipelineParams)
+    init: InitParams = field(default_factory=InitParams)
+    eval: EvalParams = field(default_factory=EvalParams)
+    seed: int = 0
+    batch: int = 64
+    workers: int = 1
+
+    def to_params(self) -> N.RunParams:
+        p = N.RunParams()
+        p.qp_rho, p.qp_sigma, p.qp_alpha = self.qp.rho, self.qp.sigma, self.qp.alpha
+        p.qp_max_iters, p.qp_eps_primal, p.qp_eps_dual = self.qp.max_iters, self.qp.eps_primal, self.qp.eps_dual
+        p.qp_check_interval = self.qp.check_interval
+        p.mu, p.n_edges = self.contact.mu, self.contact.n_edges
+        p.beta, p.gamma_per_contact = self.energy.beta, self.energy.gamma_per_contact
+        w = self.weights
+        p.w_grasp, p.w_distance, p.w_joint_limit = w.grasp, w.distance, w.joint_limit
+        p.w_self_penetration, p.w_object_penetration = w.self_penetration, w.object_penetration
+        for name in ("coarse", "fine", "final_stage"):
+            s = getattr(self.pipeline, name)
+            setattr(p, name, N.StageParams(s.iters, s.step_rotation, s.step_translation, s.step_joints,
+                                           s.step_floor))
+        p.contact_offset, p.fd_step = self.pipeline.contact_offset, self.pipeline.fd_step
+        p.skip_fine_stages = int(bool(self.pipeline.skip_fine_stages))
+        p.standoff, p.joint_span_fraction = self.init.standoff, self.init.joint_span_fraction
+        p.seed, p.batch, p.workers = int(self.seed), int(self.batch), int(self.workers)
+        return p
+
+    @staticmethod
+    def from_params(p: N.RunParams, eval_params: Optional[EvalParams] = None) -> "RunConfig":
+        st = lambda s: StageSchedule(s.iters, s.step_rotation, s.step_translation, s.step_joints, s.step_floor)
+        return RunConfig(
+            qp=QpParams(p.qp_rho, p.qp_sigma, p.qp_alpha, p.qp_max_iters, p.qp_eps_primal, p.qp_eps_dual,
+                        p.qp_check_interval),
+            contact=ContactParams(p.mu, p.n_edges),
+            energy=EnergyParams(p.beta, p.gamma_per_contact),
+            weights=ObjectiveWeights(p.w_grasp, p.w_distance, p.w_joint_limit, p.w_self_penetration,
+                                     p.w_object_penetration),
+            pipeline=PipelineParams(st(p.coarse), st(p.fine), st(p.final_stage), p.contact_offset, p.fd_step,
+                                    bool(p.skip_fine_stages)),
+            init=InitParams(p.standoff, p.joint_span_fraction),
+            eval=eval_params or EvalParams(), seed=p.seed, batch=p.batch, workers=p.workers)
+
+
+def parse_run_config(json_text: str) -> RunConfig:
+    """config.cpp:139-156: strict parse + validate (eval block checked natively too)."""
+    p = N.RunParams()
+    N.check(N.lib().grasp_run_params_parse(json_text.encode(), C.byref(p)))
+    ev = EvalParams()
+    doc = json.loads(json_text)
+    for k, v in doc.get("eval", {}).items():
+        setattr(ev, k, v)
+    return RunConfig.from_params(p, ev)
+
+
+def validate(cfg: RunConfig) -> None:
+    """config.cpp:196-229 (eval ranges checked here, the rest natively)."""
+    N.check(N.lib().grasp_run_params_validate(C.byref(cfg.to_params())))
+    e = cfg.eval
+    for ok, what in ((e.mass > 0, "eval.mass must be positive"), (e.gravity > 0, "eval.gravity must be positive"),
+                     (e.residual_rel_tol > 0, "eval.residual_rel_tol must be positive"),
+                     (e.force_budget_factor > 0, "eval.force_budget_factor must be positive"),
+                     (e.contact_tol >= 0, "eval.contact_tol must be nonnegative"),
+                     (e.penetration_tol >= 0, "eval.penetration_tol must be nonnegative"),
+                     (e.qp_eps > 0, "eval.qp_eps must be positive")):
+        if not ok:
+            from .errors import InvalidArgument
+            raise InvalidArgument("config: " + what)
+
+
+# --------------------------------------------------------------------- models
+def _arr(ptr, n, dtype):
+    if n == 0:
+        return np.zeros(0, dtype=dtype)
+    return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dtype, copy=True)
+
+
+class HandModel:
+    """Owns a native grasp_hand; exposes the packed arrays (hand.hpp:20-47)."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        self.desc = N.HandDesc()
+        N.check(N.lib().grasp_hand_describe(self._h, C.byref(self.desc)))
+        d = self.desc
+        self.n_links, self.n_tips, self.n_pairs = d.n_links, d.n_tips, d.n_pairs
+        self.fingertip_links = _arr(d.tip_links, d.n_tips, np.int32)
+        self.lower = _arr(d.joint_lower, d.dof, np.float64)
+        self.upper = _arr(d.joint_upper, d.dof, np.float64)
+        self.link_vert_begin = _arr(d.link_vert_begin, d.n_links + 1, np.int32)
+        self.link_face_begin = _arr(d.link_face_begin, d.n_links + 1, np.int32)
+        self.link_proxy_begin = _arr(d.link_proxy_begin, d.n_links + 1, np.int32)
+        self.proxies = _arr(d.proxies, 4 * d.n_proxies, np.float64).reshape(-1, 4)
+        self.collision_pairs = _arr(d.collision_pairs, 2 * d.n_pairs, np.int32).reshape(-1, 2)
+        self.link_parent_joint = _arr(d.link_parent_joint, d.n_links, np.int32)
+        self.link_tip_proxy = _arr(d.link_tip_proxy, d.n_links, np.int32)
+
+    @staticmethod
+    def builtin() -> "HandModel":
+        h = C.c_void_p()
+        N.check(N.lib().grasp_hand_builtin(C.byref(h)))
+        return HandModel(h)
+
+    @staticmethod
+    def from_json(text: str) -> "HandModel":
+        h = C.c_void_p()
+        N.check(N.lib().grasp_hand_parse(text.encode(), C.byref(h)))
+        return HandModel(h)
+
+    @staticmethod
+    def from_file(path) -> "HandModel":
+        with open(path) as f:
+            return HandModel.from_json(f.read())
+
+    def dof(self) -> int:
+        return self.desc.dof
+
+    def dims(self) -> int:
+        return 12 + self.desc.dof
+
+    def lower_limits(self):
+        return self.lower.copy()
+
+    def upper_limits(self):
+        return self.upper.copy()
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib().grasp_hand_free(self._h)
+        except Exception:
+            pass
+
+
+def builtin_hand_json() -> str:
+    n = N.lib().grasp_hand_builtin_json(None, 0)
+    buf = C.create_string_buffer(int(n))
+    N.lib().grasp_hand_builtin_json(buf, n)
+    return buf.value.decode()
+
+
+class ObjectModel:
+    """Owns a native grasp_object (object.hpp:19-25)."""
+
+    def __init__(self, handle):
+        self._o = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        self.desc = N.ObjectDesc()
+        N.check(N.lib().grasp_object_describe(self._o, C.byref(self.desc)))
+        d = self.desc
+        self.scale = d.scale
+        self.bbox_diagonal = d.bbox_diagonal
+        self.mass_center = np.array(list(d.mass_center))
+        self.source = d.source.decode() if d.source else ""
+        self.part_vert_begin = _arr(d.part_vert_begin, d.n_parts + 1, np.int32)
+        self.part_face_begin = _arr(d.part_face_begin, d.n_parts + 1, np.int32)
+        self.verts = _arr(d.verts, 3 * d.n_verts, np.float64).reshape(-1, 3)
+        self.faces = _arr(d.faces, 3 * d.n_faces, np.int32).reshape(-1, 3)
+        self.part_obb = _arr(d.part_obb, 15 * d.n_parts, np.float64).reshape(-1, 15)
+        self.part_volume = _arr(d.part_volume, d.n_parts, np.float64)
+        self.part_centroid = _arr(d.part_centroid, 3 * d.n_parts, np.float64).reshape(-1, 3)
+
+    @property
+    def n_parts(self) -> int:
+        return self.desc.n_parts
+
+    def part_vertices(self, i):
+        return self.verts[self.part_vert_begin[i]:self.part_vert_begin[i + 1]]
+
+    def part_faces(self, i):
+        return self.faces[self.part_face_begin[i]:self.part_face_begin[i + 1]]
+
+    @staticmethod
+    def primitive(name: str, scale: float) -> "ObjectModel":
+        o = C.c_void_p()
+        N.check(N.lib().grasp_object_primitive(name.encode(), float(scale), C.byref(o)))
+        return ObjectModel(o)
+
+    @staticmethod
+    def from_obj_text(text: str, scale: float, source: str = "mesh") -> "ObjectModel":
+        o = C.c_void_p()
+        N.check(N.lib().grasp_object_parse(text.encode(), float(scale), source.encode(), C.byref(o)))
+        return ObjectModel(o)
+
+    @staticmethod
+    def load(path, scale: float) -> "ObjectModel":
+        with open(path) as f:
+            return ObjectModel.from_obj_text(f.read(), scale, str(path))
+
+    @staticmethod
+    def from_points(parts) -> "ObjectModel":
+        """Raw convex parts (make_convex_part), no normalization."""
+        counts = np.array([len(p) for p in parts], dtype=np.int32)
+        pts = np.ascontiguousarray(np.concatenate([np.asarray(p, dtype=np.float64) for p in parts]))
+        o = C.c_void_p()
+        N.check(N.lib().grasp_object_from_points(len(parts), iptr(counts), dptr(pts), C.byref(o)))
+        return ObjectModel(o)
+
+    def bounding_radius(self) -> float:
+        return N.lib().grasp_object_bounding_radius(self._o)
+
+    def bounding_box(self):
+        return self.verts.min(axis=0), self.verts.max(axis=0)
+
+    def __del__(self):
+        try:
+            if self._o:
+                N.lib().grasp_object_free(self._o)
+        except Exception:
+            pass
+
+
+make_primitive = ObjectModel.primitive
+parse_object_text = ObjectModel.from_obj_text
+load_object = ObjectModel.load
+PRIMITIVE_NAMES = ("sphere", "box", "cylinder", "capsule", "flat_box")
+
+
+def init_poses(model: HandModel, obj: ObjectModel, n: int, seed: int, params: InitParams = None) -> np.ndarray:
+    """pipeline.cpp:388-424 -> (n, D) array."""
+    params = params or InitParams()
+    out = np.zeros((n, model.dims()), dtype=np.float64)
+    N.check(N.lib().grasp_init_poses(model._h, obj._o, int(n), int(seed), params.standoff,
+                                     params.joint_span_fraction, dptr(out)))
+    return out
+
+
+def squeeze_pose(model: HandModel, x, x_p) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    x_p = np.ascontiguousarray(x_p, dtype=np.float64)
+    out = np.zeros(model.dims())
+    N.check(N.lib().grasp_squeeze_pose(model._h, dptr(x), dptr(x_p), dptr(out)))
+    return out
+
+
+# -------------------------------------------------------------------- records
+@dataclass
+class ContactFrame:
+    p: np.ndarray
+    n: np.ndarray
+    d: np.ndarray
+    e: np.ndarray
+
+
+@dataclass
+class StageTrace:
+    stage: str
+    iterations: int
+    energy_start: float
+    energy_end: float
+
+
+@dataclass
+class GraspRecord:
+    x_p: np.ndarray
+    x: np.ndarray
+    x_s: np.ndarray
+    energy_total: float
+    per_direction: np.ndarray
+    contact_forces: np.ndarray
+    contacts: List[ContactFrame]
+    object_id: str
+    object_scale: float
+    seed: int
+    index: int
+    failed: bool
+    note: str
+    stages: List[StageTrace]
+
+
+_NOTES = {0: "", 1: "non-finite energy", 2: "diverged"}
+
+
+class SynthesisOutput:
+    """SoA result buffers laid out like grasp_out (host numpy arrays)."""
+
+    def __init__(self, batch: int, dims: int, m: int, n_edges: int):
+        n = m * n_edges
+        self.x_p = np.zeros((batch, dims))
+        self.x = np.zeros((batch, dims))
+        self.x_s = np.zeros((batch, dims))
+        self.energy_total = np.zeros(batch)
+        self.per_direction = np.zeros((batch, 6))
+        self.contact_forces = np.zeros((batch, 6, n))  # per grasp column-major (n x 6) == row-major (6, n)
+        self.contacts = np.zeros((batch, m, 12))
+        self.stage_energy = np.zeros((batch, 3, 2))
+        self.failed = np.zeros(batch, dtype=np.int32)
+        self.qp_converged = np.zeros((batch, 6), dtype=np.int32)
+
+    def as_struct(self) -> N.Out:
+        return N.Out(dptr(self.x_p), dptr(self.x), dptr(self.x_s), dptr(self.energy_total),
+                     dptr(self.per_direction), dptr(self.contact_forces), dptr(self.contacts),
+                     dptr(self.stage_energy), iptr(self.failed), iptr(self.qp_converged))
+
+    def records(self, cfg: RunConfig, obj: ObjectModel, index_offset: int = 0) -> List[GraspRecord]:
+        names = ("coarse", "fine", "final")
+        iters = (cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters)
+        n_stages = 1 if cfg.pipeline.skip_fine_stages else 3
+        out = []
+        for g in range(self.x.shape[0]):
+            failed = int(self.failed[g])
+            contacts = [] if failed else [ContactFrame(c[0:3].copy(), c[3:6].copy(), c[6:9].copy(), c[9:12].copy())
+                                          for c in self.contacts[g]]
+            out.append(GraspRecord(
+                x_p=self.x_p[g].copy(), x=self.x[g].copy(), x_s=self.x_s[g].copy(),
+                energy_total=float(self.energy_total[g]),
+                per_direction=np.zeros(0) if failed else self.per_direction[g].copy(),
+                contact_forces=np.zeros((0, 0)) if failed else self.contact_forces[g].T.copy(),
+                contacts=contacts, object_id=obj.source, object_scale=obj.scale, seed=int(cfg.seed),
+                index=index_offset + g, failed=bool(failed), note=_NOTES.get(failed, "failed"),
+                stages=[StageTrace(names[s], iters[s], float(self.stage_energy[g, s, 0]),
+                                   float(self.stage_energy[g, s, 1])) for s in range(n_stages)]))
+        return out
+
+
+# --------------------------------------------------------------------- engine
+class Engine:
+    """One CUDA device, one stream (grasp_ctx). Hand/object uploaded once."""
+
+    def __init__(self, device: int = 0):
+        self._ctx = C.c_void_p()
+        N.check(N.lib().grasp_ctx_create(int(device), C.byref(self._ctx)))
+        self.hand: Optional[HandModel] = None
+        self.obj: Optional[ObjectModel] = None
+
+    def set_hand(self, hand: HandModel):
+        N.check(N.lib().grasp_ctx_set_hand(self._ctx, C.byref(hand.desc)))
+        self.hand = hand
+
+    def set_object(self, obj: ObjectModel):
+        N.check(N.lib().grasp_ctx_set_object(self._ctx, C.byref(obj.desc)))
+        self.obj = obj
+
+    def synthesize(self, cfg: RunConfig, x0: np.ndarray) -> SynthesisOutput:
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        batch = x0.shape[0]
+        out = SynthesisOutput(batch, self.hand.dims(), self.hand.n_tips, cfg.contact.n_edges)
+        s = out.as_struct()
+        N.check(N.lib().grasp_synthesize(self._ctx, C.byref(cfg.to_params()), batch, dptr(x0), C.byref(s)))
+        return out
+
+    def close(self):
+        if self._ctx:
+            N.lib().grasp_ctx_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def synthesize(model: HandModel, obj: ObjectModel, cfg: RunConfig, device: int = 0,
+               engine: Optional[Engine] = None) -> List[GraspRecord]:
+    """pipeline.cpp:436-457 on a B200: validate, init_poses (host, one RNG
+    stream), the three-stage loop on the GPU, records in input order."""
+    validate(cfg)
+    x0 = init_poses(model, obj, cfg.batch, cfg.seed, cfg.init)
+    eng = engine or Engine(device)
+    if eng.hand is not model:
+        eng.set_hand(model)
+    if eng.obj is not obj:
+        eng.set_object(obj)
+    return eng.synthesize(cfg, x0).records(cfg, obj)
