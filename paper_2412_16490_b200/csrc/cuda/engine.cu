@@ -1,0 +1,741 @@
+// Host orchestration of the B200 grasp-synthesis engine and the device half
+// of the C ABI (include/grasp_b200.h). One grasp_ctx = one device + one
+// stream; the hand/object are uploaded once and stay resident in HBM, and
+// the per-grasp state is sized for the largest batch seen.
+//
+// Stage loop (reference run_grasp, proj/src/pipeline.cpp:233-316), all
+// grasps in lockstep on the device:
+//   for stage s: k_fk; for it: [queries, qp|pairs, step+fk]; stage-end eval
+//   after coarse: anchors; after fine: x_p; final record: witnesses, cold QP,
+//   squeeze.
+#include "../../../include/grasp_b200.h"
+#include "../host/capi_common.hpp"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <numbers>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using namespace gdev;
+
+namespace {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    n = count;
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    ensure(v.size());
+    if (!v.empty()) ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "upload");
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+struct grasp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool has_hand = false, has_object = false;
+
+  // hand
+  DevHand H{};
+  DevBuf<int> h_lpj, h_depth, h_path, h_jpl, h_proxy_link, h_tip_link, h_tip_proxy, h_spa, h_spb, h_lvbeg,
+      h_tip_slots, h_tip_links_sorted;
+  DevBuf<unsigned> h_subtree;
+  DevBuf<double> h_jorigin, h_jaxis, h_jlo, h_jhi, h_proxy, h_envelope, h_lverts, h_lcentroid, h_lhalf;
+  // object
+  DevObject O{};
+  DevBuf<int> o_fbeg, o_vbeg;
+  DevBuf<double> o_faces, o_verts, o_centroid, o_half, o_obb;
+
+  // per-grasp state
+  DevState st{};
+  DevBuf<double> x, pose, world, joints, qpts, qres, pairs, warm_x, warm_y, out_z, qp_force, qp_energy, qp_perdir,
+      frames, anchors, energy, grad, stage_energy, x_p, x_s, witness;
+  DevBuf<int> qp_iters, qp_conv, qp_ready, failed, have_pregrasp, err;
+
+  ~grasp_ctx() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void set_device() { ck(cudaSetDevice(device), "cudaSetDevice"); }
+
+  void set_hand(const grasp_hand_desc* d) {
+    set_device();
+    if (d->n_links > kMaxLinks) throw std::invalid_argument("hand has more than 32 links");
+    if (d->dof > kMaxDof) throw std::invalid_argument("hand has more than 32 joints");
+    if (d->n_tips < 1 || d->n_tips > kMaxTips) throw std::invalid_argument("hand needs 1..5 fingertips");
+    if (d->n_proxies > kMaxProxies) throw std::invalid_argument("hand has more than 128 sphere proxies");
+    const int L = d->n_links, dof = d->dof, m = d->n_tips, S = d->n_proxies;
+    std::vector<int> depth(L), path(static_cast<size_t>(L) * kMaxDepth, 0);
+    for (int l = 0; l < L; ++l) {
+      std::vector<int> chain;
+      int cur = l;
+      while (cur >= 0) {
+        chain.push_back(cur);
+        const int j = d->link_parent_joint[cur];
+        cur = j < 0 ? -1 : d->joint_parent_link[j];
+        if (static_cast<int>(chain.size()) > kMaxDepth) throw std::invalid_argument("kinematic chain deeper than 12");
+      }
+      std::reverse(chain.begin(), chain.end());
+      depth[l] = static_cast<int>(chain.size());
+      for (size_t i = 0; i < chain.size(); ++i) path[l * kMaxDepth + i] = chain[i];
+    }
+    std::vector<unsigned> subtree(dof, 0u);
+    for (int j = 0; j < dof; ++j) {
+      const int child = d->joint_child_link[j];
+      for (int l = 0; l < L; ++l)
+        for (int i = 0; i < depth[l]; ++i)
+          if (path[l * kMaxDepth + i] == child) subtree[j] |= 1u << l;
+    }
+    std::vector<int> proxy_link(S);
+    for (int l = 0; l < L; ++l)
+      for (int p = d->link_proxy_begin[l]; p < d->link_proxy_begin[l + 1]; ++p) proxy_link[p] = l;
+    std::vector<int> tip_link(d->tip_links, d->tip_links + m), tip_proxy(m);
+    std::vector<double> envelope(m);
+    for (int f = 0; f < m; ++f) {
+      const int l = tip_link[f];
+      tip_proxy[f] = d->link_proxy_begin[l] + d->link_tip_proxy[l];
+      const double* c = d->proxies + 4 * tip_proxy[f];
+      double r = 0.0;
+      for (int v = d->link_vert_begin[l]; v < d->link_vert_begin[l + 1]; ++v) {
+        const double dx = d->verts[3 * v] - c[0], dy = d->verts[3 * v + 1] - c[1], dz = d->verts[3 * v + 2] - c[2];
+        r = std::max(r, std::sqrt(dx * dx + dy * dy + dz * dz));
+      }
+      envelope[f] = r;
+    }
+    // Sphere pairs in the reference order (hand.cpp:225-231).
+    std::vector<int> spa, spb;
+    for (int i = 0; i < d->n_pairs; ++i) {
+      const int la = d->collision_pairs[2 * i], lb = d->collision_pairs[2 * i + 1];
+      for (int a = d->link_proxy_begin[la]; a < d->link_proxy_begin[la + 1]; ++a)
+        for (int b = d->link_proxy_begin[lb]; b < d->link_proxy_begin[lb + 1]; ++b) {
+          spa.push_back(a);
+          spb.push_back(b);
+        }
+    }
+    std::vector<double> half(L), centroid(d->link_centroid, d->link_centroid + 3 * L);
+    for (int l = 0; l < L; ++l) {
+      const double* o = d->link_obb + 15 * l;
+      half[l] = std::sqrt(o[3] * o[3] + o[4] * o[4] + o[5] * o[5]);
+    }
+    cudaStream_t s = stream;
+    h_lpj.upload(std::vector<int>(d->link_parent_joint, d->link_parent_joint + L), s);
+    h_depth.upload(depth, s);
+    h_path.upload(path, s);
+    h_jpl.upload(std::vector<int>(d->joint_parent_link, d->joint_parent_link + dof), s);
+    h_jorigin.upload(std::vector<double>(d->joint_origin, d->joint_origin + 3 * dof), s);
+    h_jaxis.upload(std::vector<double>(d->joint_axis, d->joint_axis + 3 * dof), s);
+    h_jlo.upload(std::vector<double>(d->joint_lower, d->joint_lower + dof), s);
+    h_jhi.upload(std::vector<double>(d->joint_upper, d->joint_upper + dof), s);
+    h_subtree.upload(subtree, s);
+    h_proxy.upload(std::vector<double>(d->proxies, d->proxies + 4 * S), s);
+    h_proxy_link.upload(proxy_link, s);
+    h_tip_link.upload(tip_link, s);
+    h_tip_proxy.upload(tip_proxy, s);
+    h_tip_slots.upload(tip_proxy, s);
+    h_envelope.upload(envelope, s);
+    h_spa.upload(spa, s);
+    h_spb.upload(spb, s);
+    h_lvbeg.upload(std::vector<int>(d->link_vert_begin, d->link_vert_begin + L + 1), s);
+    h_lverts.upload(std::vector<double>(d->verts, d->verts + 3 * d->n_verts), s);
+    h_lcentroid.upload(centroid, s);
+    h_lhalf.upload(half, s);
+    h_tip_links_sorted.upload(tip_link, s);
+    ck(cudaStreamSynchronize(s), "hand upload");
+    H.L = L;
+    H.dof = dof;
+    H.m = m;
+    H.S = S;
+    H.nsp = static_cast<int>(spa.size());
+    H.D = 12 + dof;
+    H.link_parent_joint = h_lpj.p;
+    H.link_depth = h_depth.p;
+    H.link_path = h_path.p;
+    H.joint_parent_link = h_jpl.p;
+    H.joint_origin = h_jorigin.p;
+    H.joint_axis = h_jaxis.p;
+    H.joint_lower = h_jlo.p;
+    H.joint_upper = h_jhi.p;
+    H.joint_subtree = h_subtree.p;
+    H.proxy = h_proxy.p;
+    H.proxy_link = h_proxy_link.p;
+    H.tip_link = h_tip_link.p;
+    H.tip_proxy = h_tip_proxy.p;
+    H.tip_envelope = h_envelope.p;
+    H.sp_a = h_spa.p;
+    H.sp_b = h_spb.p;
+    H.link_vbeg = h_lvbeg.p;
+    H.link_verts = h_lverts.p;
+    H.link_centroid = h_lcentroid.p;
+    H.link_halfnorm = h_lhalf.p;
+    has_hand = true;
+  }
+
+  void set_object(const grasp_object_desc* d) {
+    set_device();
+    if (d->n_parts < 1) throw std::invalid_argument("point query against an empty part list");
+    if (d->n_parts > kMaxParts) throw std::invalid_argument("object has more than 64 parts");
+    const int P = d->n_parts;
+    std::vector<double> faces(static_cast<size_t>(d->n_faces) * kFaceStride, 0.0);
+    for (int p = 0; p < P; ++p) {
+      const int v0 = d->part_vert_begin[p];
+      for (int f = d->part_face_begin[p]; f < d->part_face_begin[p + 1]; ++f) {
+        double* F = faces.data() + static_cast<size_t>(f) * kFaceStride;
+        const double* a = d->verts + 3 * (v0 + d->faces[3 * f]);
+        const double* b = d->verts + 3 * (v0 + d->faces[3 * f + 1]);
+        const double* c = d->verts + 3 * (v0 + d->faces[3 * f + 2]);
+        for (int k = 0; k < 3; ++k) {
+          F[k] = a[k];
+          F[3 + k] = b[k];
+          F[6 + k] = c[k];
+        }
+        // n = (b - a) x (c - a), |n|, n /= |n|, nd = n . a  (query_part, geometry.cpp:363-368)
+        const double e1[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+        const double e2[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+        double n[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+        const double len = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+        if (len < 1e-30) {
+          F[13] = 0.0;
+          continue;
+        }
+        for (double& v : n) v /= len;
+        F[9] = n[0];
+        F[10] = n[1];
+        F[11] = n[2];
+        F[12] = n[0] * a[0] + n[1] * a[1] + n[2] * a[2];
+        F[13] = 1.0;
+      }
+    }
+    std::vector<int> fbeg(d->part_face_begin, d->part_face_begin + P + 1);
+    std::vector<int> vbeg(d->part_vert_begin, d->part_vert_begin + P + 1);
+    std::vector<double> half(P);
+    for (int p = 0; p < P; ++p) {
+      const double* o = d->part_obb + 15 * p;
+      half[p] = std::sqrt(o[3] * o[3] + o[4] * o[4] + o[5] * o[5]);
+    }
+    cudaStream_t s = stream;
+    o_fbeg.upload(fbeg, s);
+    o_vbeg.upload(vbeg, s);
+    o_faces.upload(faces, s);
+    o_verts.upload(std::vector<double>(d->verts, d->verts + 3 * d->n_verts), s);
+    o_centroid.upload(std::vector<double>(d->part_centroid, d->part_centroid + 3 * P), s);
+    o_half.upload(half, s);
+    o_obb.upload(std::vector<double>(d->part_obb, d->part_obb + 15 * P), s);
+    ck(cudaStreamSynchronize(s), "object upload");
+    O.P = P;
+    O.F = d->n_faces;
+    O.part_fbeg = o_fbeg.p;
+    O.part_vbeg = o_vbeg.p;
+    O.faces = o_faces.p;
+    O.verts = o_verts.p;
+    O.part_centroid = o_centroid.p;
+    O.part_halfnorm = o_half.p;
+    O.part_obb = o_obb.p;
+    has_object = true;
+  }
+
+  // Sizes every per-grasp buffer for G grasps (m contacts for the QP).
+  void ensure_state(int G, int m_qp, int k) {
+    const int L = has_hand ? H.L : 1, dof = has_hand ? H.dof : 0, m = has_hand ? H.m : m_qp;
+    const int mq = std::max(m, m_qp);
+    const int D = 12 + dof;
+    const int NQ = has_hand ? H.S + 6 * H.m : 1;
+    const int NP = L * (has_object ? O.P : 1);
+    const int n = mq * k, M = mq + 1 + n;
+    const size_t g = static_cast<size_t>(G);
+    x.ensure(g * D);
+    pose.ensure(g * 24);
+    world.ensure(g * L * 12);
+    joints.ensure(g * std::max(dof, 1) * 6);
+    qpts.ensure(g * NQ * 3);
+    qres.ensure(g * NQ * 8);
+    pairs.ensure(g * NP * 12);
+    warm_x.ensure(g * n * 6);
+    warm_y.ensure(g * M * 6);
+    out_z.ensure(g * M * 6);
+    qp_force.ensure(g * mq * 3);
+    qp_energy.ensure(g);
+    qp_perdir.ensure(g * 6);
+    frames.ensure(g * mq * 12);
+    anchors.ensure(g * mq * 3);
+    energy.ensure(g);
+    grad.ensure(g * D);
+    stage_energy.ensure(g * 6);
+    x_p.ensure(g * D);
+    x_s.ensure(g * D);
+    witness.ensure(g * mq * 11);
+    qp_iters.ensure(g * 6);
+    qp_conv.ensure(g * 6);
+    qp_ready.ensure(g);
+    failed.ensure(g);
+    have_pregrasp.ensure(g);
+    err.ensure(4);
+    st.G = G;
+    st.NQ = NQ;
+    st.NP = NP;
+    st.x = x.p;
+    st.pose = pose.p;
+    st.world = world.p;
+    st.joints = joints.p;
+    st.qpts = qpts.p;
+    st.qres = qres.p;
+    st.pairs = pairs.p;
+    st.warm_x = warm_x.p;
+    st.warm_y = warm_y.p;
+    st.out_z = out_z.p;
+    st.qp_iters = qp_iters.p;
+    st.qp_conv = qp_conv.p;
+    st.qp_ready = qp_ready.p;
+    st.qp_force = qp_force.p;
+    st.qp_energy = qp_energy.p;
+    st.qp_perdir = qp_perdir.p;
+    st.frames = frames.p;
+    st.anchors = anchors.p;
+    st.energy = energy.p;
+    st.grad = grad.p;
+    st.failed = failed.p;
+    st.stage_energy = stage_energy.p;
+    st.x_p = x_p.p;
+    st.have_pregrasp = have_pregrasp.p;
+    st.err = err.p;
+  }
+
+  DevParams make_params(const grasp_run_params* p, int m) const {
+    DevParams P{};
+    P.rho = p->qp_rho;
+    P.sigma = p->qp_sigma;
+    P.alpha = p->qp_alpha;
+    P.max_iters = p->qp_max_iters;
+    P.eps_primal = p->qp_eps_primal;
+    P.eps_dual = p->qp_eps_dual;
+    P.check_interval = p->qp_check_interval;
+    P.mu = p->mu;
+    P.k = p->n_edges;
+    P.beta = p->beta;
+    P.gamma_total = p->gamma_per_contact * m;
+    P.w_grasp = p->w_grasp;
+    P.w_distance = p->w_distance;
+    P.w_limit = p->w_joint_limit;
+    P.w_self = p->w_self_penetration;
+    P.w_pen = p->w_object_penetration;
+    P.fd_step = p->fd_step;
+    for (int j = 0; j < p->n_edges && j < kMaxEdges; ++j) {
+      const double th = 2.0 * std::numbers::pi * j / p->n_edges;  // contact.cpp:35
+      P.cos_t[j] = std::cos(th);
+      P.sin_t[j] = std::sin(th);
+    }
+    return P;
+  }
+
+  static StageArgs stage_args(int stage, const grasp_stage_params& sp, double offset, int it, int mode) {
+    StageArgs A{};
+    A.stage = stage;
+    A.iters = sp.iters;
+    A.it = it;
+    A.step_rot = sp.step_rotation;
+    A.step_trans = sp.step_translation;
+    A.step_joints = sp.step_joints;
+    A.step_floor = sp.step_floor;
+    A.offset = offset;
+    A.mode = mode;
+    const double t = sp.iters > 1 ? static_cast<double>(it) / sp.iters : 0.0;  // pipeline.cpp:216-218
+    A.decay = sp.step_floor + (1.0 - sp.step_floor) * 0.5 * (1.0 + std::cos(std::numbers::pi * t));
+    return A;
+  }
+
+  static unsigned blocks(long long threads, int per) { return static_cast<unsigned>((threads + per - 1) / per); }
+
+  void launch_queries(bool tips_only) {
+    const int per = tips_only ? H.m : st.NQ;
+    const long long n = static_cast<long long>(st.G) * per;
+    k_point_query<<<blocks(n, 128), 128, 0, stream>>>(O, st, tips_only ? h_tip_slots.p : nullptr, per);
+  }
+  void launch_pairs(bool tips_only) {
+    const int nl = tips_only ? H.m : H.L;
+    const long long n = static_cast<long long>(st.G) * nl * O.P;
+    k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, tips_only ? h_tip_links_sorted.p : nullptr, nl);
+  }
+  void launch_qp(const DevParams& P, int m, int mode, int with_grad) {
+    k_qp<<<blocks(st.G, 4), 128, 0, stream>>>(H, P, st, m, mode, with_grad);
+  }
+  void launch_fk(const DevParams& P) { k_fk<<<blocks(st.G, 2), 64, 0, stream>>>(H, P, st); }
+  void launch_step(const DevParams& P, const StageArgs& A, bool coarse) {
+    if (coarse)
+      k_step_coarse<<<blocks(st.G, 2), 64, 0, stream>>>(H, P, A, st);
+    else
+      k_step_mesh<<<blocks(st.G, 2), 64, 0, stream>>>(H, O, P, A, st);
+  }
+
+  void check_errors() {
+    int e[4];
+    ck(cudaMemcpyAsync(e, err.p, sizeof(e), cudaMemcpyDeviceToHost, stream), "err copy");
+    ck(cudaStreamSynchronize(stream), "sync");
+    if (e[0]) throw grasp::geom::GeometryError("penetration query on a degenerate shape pair");
+    if (e[1]) throw grasp::geom::GeometryError("EPA polytope exceeded the device capacity");
+  }
+
+  void reset_run_state(int G) {
+    ck(cudaMemsetAsync(failed.p, 0, sizeof(int) * G, stream), "memset");
+    ck(cudaMemsetAsync(qp_ready.p, 0, sizeof(int) * G, stream), "memset");
+    ck(cudaMemsetAsync(have_pregrasp.p, 0, sizeof(int) * G, stream), "memset");
+    ck(cudaMemsetAsync(err.p, 0, sizeof(int) * 4, stream), "memset");
+    std::vector<double> nan(static_cast<size_t>(G) * 6, std::numeric_limits<double>::quiet_NaN());
+    ck(cudaMemcpyAsync(stage_energy.p, nan.data(), nan.size() * sizeof(double), cudaMemcpyHostToDevice, stream),
+       "nan fill");
+    ck(cudaStreamSynchronize(stream), "sync");
+  }
+
+  // The whole synthesis for G grasps whose start states are in x (device).
+  void run(const grasp_run_params* p) {
+    const DevParams P = make_params(p, H.m);
+    const grasp_stage_params* scheds[3] = {&p->coarse, &p->fine, &p->final_stage};
+    const double offsets[3] = {p->contact_offset, p->contact_offset, 0.0};
+    const int n_stages = p->skip_fine_stages ? 1 : 3;
+    for (int s = 0; s < n_stages; ++s) {
+      const bool coarse = s == 0;
+      launch_fk(P);
+      for (int it = 0; it < scheds[s]->iters; ++it) {
+        const StageArgs A = stage_args(s, *scheds[s], offsets[s], it, 0);
+        if (coarse) {
+          launch_queries(false);
+          launch_qp(P, H.m, 0, 1);
+        } else {
+          launch_queries(true);
+          launch_pairs(false);
+        }
+        launch_step(P, A, coarse);
+      }
+      // Stage-end energy (pipeline.cpp:279-280); in the coarse stage this
+      // also solves the QP and refreshes the warm start.
+      const StageArgs A = stage_args(s, *scheds[s], offsets[s], 0, 1);
+      if (coarse) {
+        launch_queries(false);
+        launch_qp(P, H.m, 0, 0);
+      } else {
+        launch_queries(true);
+        launch_pairs(false);
+      }
+      launch_step(P, A, coarse);
+      if (s == 0) k_anchors<<<blocks(st.G, 128), 128, 0, stream>>>(H, st, p->skip_fine_stages ? 1 : 0);
+      if (s == 1) k_set_pregrasp<<<blocks(st.G, 128), 128, 0, stream>>>(H, st);
+    }
+    // Final record: witnesses at x, cold QP on their frames, squeeze.
+    launch_fk(P);
+    launch_queries(true);
+    launch_pairs(true);
+    k_final_frames<<<blocks(static_cast<long long>(st.G) * H.m, 128), 128, 0, stream>>>(H, O, st, nullptr);
+    launch_qp(P, H.m, 1, 0);
+    k_squeeze<<<blocks(st.G, 128), 128, 0, stream>>>(H, st, x_s.p);
+    ck(cudaGetLastError(), "kernel launch");
+  }
+};
+
+namespace {
+
+using grasp::capi::fail;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return GRASP_OK;
+  } catch (const CudaError& e) {
+    return fail(GRASP_ECUDA, e.what());
+  } catch (const grasp::geom::GeometryError& e) {
+    return fail(GRASP_EGEOM, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(GRASP_EINVAL, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(GRASP_ENOMEM, "out of host memory");
+  } catch (const std::exception& e) {
+    return fail(GRASP_EINVAL, e.what());
+  }
+}
+
+void require_models(const grasp_ctx* ctx) {
+  if (!ctx) throw std::invalid_argument("null context");
+  if (!ctx->has_hand) throw std::invalid_argument("no hand uploaded (grasp_ctx_set_hand)");
+  if (!ctx->has_object) throw std::invalid_argument("no object uploaded (grasp_ctx_set_object)");
+}
+
+void copy_out(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+  if (dst && bytes) ck(cudaMemcpyAsync(dst, src, bytes, kind, s), "output copy");
+}
+
+// Collects the record fields into caller buffers (host or device).
+void emit_outputs(grasp_ctx* ctx, const grasp_run_params* p, int G, grasp_out* out, cudaMemcpyKind kind) {
+  const int D = ctx->H.D, m = ctx->H.m, n = m * p->n_edges;
+  cudaStream_t s = ctx->stream;
+  copy_out(out->x_p, ctx->x_p.p, sizeof(double) * G * D, kind, s);
+  copy_out(out->x, ctx->x.p, sizeof(double) * G * D, kind, s);
+  copy_out(out->x_s, ctx->x_s.p, sizeof(double) * G * D, kind, s);
+  copy_out(out->energy_total, ctx->qp_energy.p, sizeof(double) * G, kind, s);
+  copy_out(out->per_direction, ctx->qp_perdir.p, sizeof(double) * G * 6, kind, s);
+  copy_out(out->contact_forces, ctx->warm_x.p, sizeof(double) * G * n * 6, kind, s);
+  copy_out(out->contacts, ctx->frames.p, sizeof(double) * G * m * 12, kind, s);
+  copy_out(out->stage_energy, ctx->stage_energy.p, sizeof(double) * G * 6, kind, s);
+  copy_out(out->failed, ctx->failed.p, sizeof(int) * G, kind, s);
+  copy_out(out->qp_converged, ctx->qp_conv.p, sizeof(int) * G * 6, kind, s);
+  ck(cudaStreamSynchronize(s), "output sync");
+}
+
+// Failed grasps report NaN energy and no QP fields (pipeline.cpp:312-314).
+void mask_failed_host(const grasp_ctx* ctx, const grasp_run_params* p, int G, grasp_out* out) {
+  if (!out->failed) return;
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  const int m = ctx->H.m, n = m * p->n_edges;
+  for (int g = 0; g < G; ++g) {
+    if (!out->failed[g]) continue;
+    if (out->energy_total) out->energy_total[g] = nan;
+    if (out->per_direction)
+      for (int j = 0; j < 6; ++j) out->per_direction[6 * g + j] = nan;
+    if (out->contact_forces)
+      for (int i = 0; i < n * 6; ++i) out->contact_forces[static_cast<size_t>(g) * n * 6 + i] = nan;
+    if (out->contacts)
+      for (int i = 0; i < m * 12; ++i) out->contacts[static_cast<size_t>(g) * m * 12 + i] = nan;
+    if (out->qp_converged)
+      for (int j = 0; j < 6; ++j) out->qp_converged[6 * g + j] = 0;
+  }
+}
+
+int synthesize_impl(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0, grasp_out* out,
+                    bool device_ptrs) {
+  return guard([&] {
+    require_models(ctx);
+    if (!p || !out) throw std::invalid_argument("null argument");
+    grasp::validate(grasp::capi::to_config(p));
+    if (batch <= 0) throw std::invalid_argument("config: batch must be positive");
+    if (p->n_edges > kMaxEdges) throw std::invalid_argument("contact.n_edges above 8 is not supported on device");
+    ctx->set_device();
+    ctx->ensure_state(batch, ctx->H.m, p->n_edges);
+    ctx->reset_run_state(batch);
+    ck(cudaMemcpyAsync(ctx->x.p, x0, sizeof(double) * batch * ctx->H.D,
+                       device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream),
+       "x0 copy");
+    ctx->run(p);
+    ctx->check_errors();
+    emit_outputs(ctx, p, batch, out, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+    if (!device_ptrs) mask_failed_host(ctx, p, batch, out);
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int grasp_ctx_create(int device, grasp_ctx** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null output");
+    int count = 0;
+    ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count) throw CudaError("device index out of range");
+    auto* ctx = new grasp_ctx();
+    ctx->device = device;
+    try {
+      ctx->set_device();
+      ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      // Large per-thread stacks for the EPA scratch of k_pairs.
+      ck(cudaDeviceSetLimit(cudaLimitStackSize, 32 * 1024), "stack limit");
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+void grasp_ctx_destroy(grasp_ctx* ctx) { delete ctx; }
+
+int grasp_ctx_set_hand(grasp_ctx* ctx, const grasp_hand_desc* hand) {
+  return guard([&] {
+    if (!ctx || !hand) throw std::invalid_argument("null argument");
+    ctx->set_hand(hand);
+  });
+}
+
+int grasp_ctx_set_object(grasp_ctx* ctx, const grasp_object_desc* object) {
+  return guard([&] {
+    if (!ctx || !object) throw std::invalid_argument("null argument");
+    ctx->set_object(object);
+  });
+}
+
+int grasp_synthesize(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0, grasp_out* out) {
+  return synthesize_impl(ctx, p, batch, x0, out, false);
+}
+
+int grasp_synthesize_device(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0_dev,
+                            grasp_out* out_dev) {
+  return synthesize_impl(ctx, p, batch, x0_dev, out_dev, true);
+}
+
+int grasp_qp_batch(grasp_ctx* ctx, const grasp_run_params* p, int n_grasps, int m, const double* frames,
+                   const double* warm_x, const double* warm_y, double* X, double* Y, double* Z, int* iters,
+                   int* converged, double* per_direction, int device_ptrs) {
+  return guard([&] {
+    if (!ctx || !p || !frames) throw std::invalid_argument("null argument");
+    if (m < 1 || m > kMaxTips) throw std::invalid_argument("grasp energy needs 1..5 contacts on device");
+    if (p->n_edges < 3 || p->n_edges > kMaxEdges) throw std::invalid_argument("n_edges must lie in [3, 8]");
+    if (p->gamma_per_contact * m > m + 1e-12 || p->gamma_per_contact < 0)
+      throw std::invalid_argument("total-weight floor exceeds the per-contact caps; lower QP infeasible");
+    ctx->set_device();
+    const bool had_hand = ctx->has_hand;
+    DevHand saved = ctx->H;
+    ctx->ensure_state(n_grasps, m, p->n_edges);
+    const int n = m * p->n_edges, M = m + 1 + n;
+    const cudaMemcpyKind in = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const cudaMemcpyKind outk = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    cudaStream_t s = ctx->stream;
+    ck(cudaMemsetAsync(ctx->failed.p, 0, sizeof(int) * n_grasps, s), "memset");
+    ck(cudaMemcpyAsync(ctx->frames.p, frames, sizeof(double) * n_grasps * m * 12, in, s), "frames");
+    const bool warm = warm_x && warm_y;
+    if (warm) {
+      ck(cudaMemcpyAsync(ctx->warm_x.p, warm_x, sizeof(double) * n_grasps * n * 6, in, s), "warm x");
+      ck(cudaMemcpyAsync(ctx->warm_y.p, warm_y, sizeof(double) * n_grasps * M * 6, in, s), "warm y");
+    }
+    std::vector<int> ready(n_grasps, warm ? 1 : 0);
+    ck(cudaMemcpyAsync(ctx->qp_ready.p, ready.data(), sizeof(int) * n_grasps, cudaMemcpyHostToDevice, s), "ready");
+    const DevParams P = ctx->make_params(p, m);
+    ctx->launch_qp(P, m, 2, 0);
+    ck(cudaGetLastError(), "k_qp launch");
+    copy_out(X, ctx->warm_x.p, sizeof(double) * n_grasps * n * 6, outk, s);
+    copy_out(Y, ctx->warm_y.p, sizeof(double) * n_grasps * M * 6, outk, s);
+    copy_out(Z, ctx->out_z.p, sizeof(double) * n_grasps * M * 6, outk, s);
+    copy_out(iters, ctx->qp_iters.p, sizeof(int) * n_grasps * 6, outk, s);
+    copy_out(converged, ctx->qp_conv.p, sizeof(int) * n_grasps * 6, outk, s);
+    copy_out(per_direction, ctx->qp_perdir.p, sizeof(double) * n_grasps * 6, outk, s);
+    ck(cudaStreamSynchronize(s), "qp sync");
+    ctx->H = saved;
+    ctx->has_hand = had_hand;
+  });
+}
+
+int grasp_point_to_mesh(grasp_ctx* ctx, int n, const double* points, double* out) {
+  return guard([&] {
+    if (!ctx || !ctx->has_object) throw std::invalid_argument("no object uploaded");
+    ctx->set_device();
+    DevBuf<double> dp, dout;
+    dp.ensure(static_cast<size_t>(n) * 3);
+    dout.ensure(static_cast<size_t>(n) * 8);
+    ck(cudaMemcpyAsync(dp.p, points, sizeof(double) * n * 3, cudaMemcpyHostToDevice, ctx->stream), "pts");
+    k_points_raw<<<grasp_ctx::blocks(n, 128), 128, 0, ctx->stream>>>(ctx->O, n, dp.p, dout.p);
+    ck(cudaGetLastError(), "launch");
+    ck(cudaMemcpyAsync(out, dout.p, sizeof(double) * n * 8, cudaMemcpyDeviceToHost, ctx->stream), "out");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int grasp_signed_distance(grasp_ctx* ctx, int n, const int* link_ids, const int* part_ids, const double* poses,
+                          double* out) {
+  return guard([&] {
+    require_models(ctx);
+    ctx->set_device();
+    DevBuf<int> dl, dpi;
+    DevBuf<double> dpose, dout;
+    dl.upload(std::vector<int>(link_ids, link_ids + n), ctx->stream);
+    dpi.upload(std::vector<int>(part_ids, part_ids + n), ctx->stream);
+    dpose.upload(std::vector<double>(poses, poses + 12 * static_cast<size_t>(n)), ctx->stream);
+    dout.ensure(static_cast<size_t>(n) * 11);
+    k_pairs_raw<<<grasp_ctx::blocks(n, 128), 128, 0, ctx->stream>>>(ctx->H, ctx->O, n, dl.p, dpi.p, dpose.p, dout.p);
+    ck(cudaGetLastError(), "launch");
+    ck(cudaMemcpyAsync(out, dout.p, sizeof(double) * n * 11, cudaMemcpyDeviceToHost, ctx->stream), "out");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int grasp_total_energy(grasp_ctx* ctx, const grasp_run_params* p, int stage, int n, const double* x,
+                       const double* anchors, double* warm_x, double* warm_y, double* energy, double* grad) {
+  return guard([&] {
+    require_models(ctx);
+    if (stage < 0 || stage > 2) throw std::invalid_argument("stage must be 0, 1 or 2");
+    ctx->set_device();
+    ctx->ensure_state(n, ctx->H.m, p->n_edges);
+    ctx->reset_run_state(n);
+    cudaStream_t s = ctx->stream;
+    const int D = ctx->H.D, m = ctx->H.m, nv = m * p->n_edges, M = m + 1 + nv;
+    ck(cudaMemcpyAsync(ctx->x.p, x, sizeof(double) * n * D, cudaMemcpyHostToDevice, s), "x");
+    const DevParams P = ctx->make_params(p, m);
+    ctx->launch_fk(P);
+    const grasp_stage_params* sp = stage == 0 ? &p->coarse : (stage == 1 ? &p->fine : &p->final_stage);
+    const StageArgs A = grasp_ctx::stage_args(stage, *sp, stage == 2 ? 0.0 : p->contact_offset, 0, 2);
+    if (stage == 0) {
+      const bool warm = warm_x && warm_y;
+      if (warm) {
+        ck(cudaMemcpyAsync(ctx->warm_x.p, warm_x, sizeof(double) * n * nv * 6, cudaMemcpyHostToDevice, s), "wx");
+        ck(cudaMemcpyAsync(ctx->warm_y.p, warm_y, sizeof(double) * n * M * 6, cudaMemcpyHostToDevice, s), "wy");
+        std::vector<int> ready(n, 1);
+        ck(cudaMemcpyAsync(ctx->qp_ready.p, ready.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s), "ready");
+      }
+      ctx->launch_queries(false);
+      ctx->launch_qp(P, m, 0, 1);
+      ctx->launch_step(P, A, true);
+      if (warm) {
+        copy_out(warm_x, ctx->warm_x.p, sizeof(double) * n * nv * 6, cudaMemcpyDeviceToHost, s);
+        copy_out(warm_y, ctx->warm_y.p, sizeof(double) * n * M * 6, cudaMemcpyDeviceToHost, s);
+      }
+    } else {
+      if (!anchors) throw std::invalid_argument("mesh stages need anchors");
+      ck(cudaMemcpyAsync(ctx->anchors.p, anchors, sizeof(double) * n * m * 3, cudaMemcpyHostToDevice, s), "anchors");
+      ctx->launch_queries(true);
+      ctx->launch_pairs(false);
+      ctx->launch_step(P, A, false);
+    }
+    ck(cudaGetLastError(), "launch");
+    ctx->check_errors();
+    copy_out(energy, ctx->energy.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+    copy_out(grad, ctx->grad.p, sizeof(double) * n * D, cudaMemcpyDeviceToHost, s);
+    ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+int grasp_fine_contact_query(grasp_ctx* ctx, int n, const double* x, double* out) {
+  return guard([&] {
+    require_models(ctx);
+    ctx->set_device();
+    ctx->ensure_state(n, ctx->H.m, 8);
+    ctx->reset_run_state(n);
+    cudaStream_t s = ctx->stream;
+    ck(cudaMemcpyAsync(ctx->x.p, x, sizeof(double) * n * ctx->H.D, cudaMemcpyHostToDevice, s), "x");
+    grasp_run_params def;
+    grasp_run_params_default(&def);
+    const DevParams P = ctx->make_params(&def, ctx->H.m);
+    ctx->launch_fk(P);
+    ctx->launch_queries(true);
+    ctx->launch_pairs(true);
+    k_final_frames<<<grasp_ctx::blocks(static_cast<long long>(n) * ctx->H.m, 128), 128, 0, s>>>(ctx->H, ctx->O, ctx->st,
+                                                                                              ctx->witness.p);
+    ck(cudaGetLastError(), "launch");
+    ctx->check_errors();
+    copy_out(out, ctx->witness.p, sizeof(double) * n * ctx->H.m * 11, cudaMemcpyDeviceToHost, s);
+    ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+}  // extern "C"

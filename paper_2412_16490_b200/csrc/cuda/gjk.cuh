@@ -1,0 +1,452 @@
+// Device GJK / EPA signed distance between a posed hand-link hull and an
+// object part (reference proj/src/geometry.cpp:17-324, 399-412, 500-525).
+// One thread owns one pair; warps are laid out so their 32 threads share the
+// same (link, part) and differ in grasp, so vertex loads in the support scans
+// are warp-uniform (broadcast) loads. The EPA polytope lives in a fixed
+// per-thread buffer; dead faces are compacted in order, which keeps the
+// reference's face iteration order (and thus its tie-breaks) unchanged.
+#pragma once
+
+#include "dmath.cuh"
+
+namespace gdev {
+
+constexpr double kTouchTol = 1e-10;   // geometry.cpp:12
+constexpr double kGjkRelTol = 1e-14;  // geometry.cpp:13
+constexpr int kGjkMaxIters = 128;     // geometry.cpp:14
+constexpr int kEpaMaxIters = 512;     // geometry.cpp:15
+constexpr int kEpaMaxVerts = 72;
+constexpr int kEpaMaxFaces = 160;
+constexpr int kEpaMaxHorizon = 120;
+
+// Pair status bits written next to each result.
+constexpr int kPairEpa = 1;
+constexpr int kPairOverflow = 2;
+constexpr int kPairDegenerate = 4;
+
+struct Hull {
+  const double* __restrict__ verts;  // nv*3
+  int nv;
+  bool posed;  // false: identity pose (object frame)
+  M33 R;       // row-major
+  D3 t;
+};
+
+struct SP {
+  D3 w, a, b;
+};
+
+__device__ __forceinline__ D3 support(const Hull& h, D3 dir) {
+  const D3 dl = h.posed ? mulT(h.R, dir) : dir;
+  double best = -INFINITY;
+  int arg = 0;
+  for (int i = 0; i < h.nv; ++i) {
+    const double s = dl.x * __ldg(h.verts + 3 * i) + dl.y * __ldg(h.verts + 3 * i + 1) + dl.z * __ldg(h.verts + 3 * i + 2);
+    if (s > best) {
+      best = s;
+      arg = i;
+    }
+  }
+  const D3 v = ldg3(h.verts + 3 * arg);
+  return h.posed ? mul(h.R, v) + h.t : v;
+}
+
+__device__ __forceinline__ SP support_pair(const Hull& A, const Hull& B, D3 dir) {
+  SP s;
+  s.a = support(A, dir);
+  s.b = support(B, -dir);
+  s.w = s.a - s.b;
+  return s;
+}
+
+// Eigen::FullPivLU::solve restated (complete pivoting, first max in
+// column-major order, rank threshold max_pivot * n * eps, free unknowns 0).
+__device__ inline void fullpiv_solve(int n, double* m, const double* rhs, double* sol) {
+  int rowt[5], colt[5];
+  int nonzero = n;
+  double maxpivot = 0.0;
+  for (int k = 0; k < n; ++k) {
+    double biggest = -1.0;
+    int br = k, bc = k;
+    for (int c = k; c < n; ++c)
+      for (int r = k; r < n; ++r) {
+        const double v = fabs(m[c * n + r]);
+        if (v > biggest) {
+          biggest = v;
+          br = r;
+          bc = c;
+        }
+      }
+    if (biggest == 0.0) {
+      nonzero = k;
+      for (int i = k; i < n; ++i) rowt[i] = colt[i] = i;
+      break;
+    }
+    maxpivot = fmax(maxpivot, biggest);
+    rowt[k] = br;
+    colt[k] = bc;
+    if (br != k)
+      for (int c = 0; c < n; ++c) {
+        const double t = m[c * n + k];
+        m[c * n + k] = m[c * n + br];
+        m[c * n + br] = t;
+      }
+    if (bc != k)
+      for (int r = 0; r < n; ++r) {
+        const double t = m[k * n + r];
+        m[k * n + r] = m[bc * n + r];
+        m[bc * n + r] = t;
+      }
+    if (k < n - 1) {
+      const double piv = m[k * n + k];
+      for (int r = k + 1; r < n; ++r) m[k * n + r] /= piv;
+      for (int c = k + 1; c < n; ++c) {
+        const double mkc = m[c * n + k];
+        for (int r = k + 1; r < n; ++r) m[c * n + r] -= m[k * n + r] * mkc;
+      }
+    }
+  }
+  const double thresh = maxpivot * (n * 2.220446049250313e-16);
+  int rank = 0;
+  for (int i = 0; i < nonzero; ++i) rank += fabs(m[i * n + i]) > thresh;
+  if (rank == 0) {
+    for (int i = 0; i < n; ++i) sol[i] = 0.0;
+    return;
+  }
+  double c[5];
+  for (int i = 0; i < n; ++i) c[i] = rhs[i];
+  for (int k = 0; k < n; ++k) {
+    const double t = c[k];
+    c[k] = c[rowt[k]];
+    c[rowt[k]] = t;
+  }
+  for (int i = 0; i < n; ++i)
+    if (c[i] != 0.0)
+      for (int r = i + 1; r < n; ++r) c[r] -= c[i] * m[i * n + r];
+  for (int i = rank - 1; i >= 0; --i)
+    if (c[i] != 0.0) {
+      c[i] /= m[i * n + i];
+      for (int r = 0; r < i; ++r) c[r] -= c[i] * m[i * n + r];
+    }
+  int perm[5] = {0, 1, 2, 3, 4};
+  for (int k = 0; k < n; ++k) {
+    const int t = perm[k];
+    perm[k] = perm[colt[k]];
+    perm[colt[k]] = t;
+  }
+  for (int i = 0; i < n; ++i) sol[perm[i]] = i < rank ? c[i] : 0.0;
+}
+
+struct Simplex {
+  double dist2;
+  D3 v;
+  int keep[4];
+  double wts[4];
+  int nkeep;
+  bool contains;
+};
+
+// Closest point of conv(simp) to the origin by subset enumeration
+// (geometry.cpp:58-95), same acceptance and tie rules.
+__device__ inline Simplex closest_on_simplex(const SP* simp, int n) {
+  Simplex best;
+  best.dist2 = INFINITY;
+  best.v = mk(0, 0, 0);
+  best.nkeep = 0;
+  best.contains = false;
+  for (int mask = 1; mask < (1 << n); ++mask) {
+    int idx[4];
+    int k = 0;
+    for (int i = 0; i < n; ++i)
+      if (mask & (1 << i)) idx[k++] = i;
+    const int s = k + 1;
+    double M[25];
+    double rhs[5] = {0, 0, 0, 0, 0};
+    for (int i = 0; i < k; ++i) {
+      for (int j = 0; j < k; ++j) M[j * s + i] = dot(simp[idx[i]].w, simp[idx[j]].w);
+      M[k * s + i] = 1.0;
+      M[i * s + k] = 1.0;
+    }
+    M[k * s + k] = 0.0;
+    rhs[k] = 1.0;
+    double sol[5];
+    fullpiv_solve(s, M, rhs, sol);
+    bool ok = true;
+    for (int i = 0; i < s; ++i) ok = ok && isfinite(sol[i]);
+    for (int i = 0; ok && i < k; ++i)
+      if (sol[i] < -1e-12) ok = false;
+    if (!ok) continue;
+    D3 v = mk(0, 0, 0);
+    for (int i = 0; i < k; ++i) v += sol[i] * simp[idx[i]].w;
+    const double d2 = sqn(v);
+    if (d2 < best.dist2 - 1e-300 || (k < best.nkeep && d2 <= best.dist2 * (1.0 + 1e-12))) {
+      best.dist2 = d2;
+      best.v = v;
+      best.nkeep = k;
+      for (int i = 0; i < k; ++i) {
+        best.keep[i] = idx[i];
+        best.wts[i] = sol[i];
+      }
+      if (k == 4) best.contains = true;
+    }
+  }
+  return best;
+}
+
+struct PairResult {
+  double d;
+  D3 pa, pb, n;
+  int flags;
+};
+
+struct EpaFace {
+  int v0, v1, v2;
+  D3 n;
+  double d;
+};
+
+__device__ __forceinline__ bool lex_less(D3 a, D3 b) {
+  if (a.x != b.x) return a.x < b.x;
+  if (a.y != b.y) return a.y < b.y;
+  return a.z < b.z;
+}
+
+struct EpaScratch {
+  SP verts[kEpaMaxVerts];
+  EpaFace faces[kEpaMaxFaces];
+  int hu[kEpaMaxHorizon], hv[kEpaMaxHorizon];
+};
+
+__device__ inline EpaFace epa_make_face(const SP* verts, D3 interior, int i0, int i1, int i2) {
+  EpaFace f;
+  f.v0 = i0;
+  f.v1 = i1;
+  f.v2 = i2;
+  const D3 c = cross(verts[i1].w - verts[i0].w, verts[i2].w - verts[i0].w);
+  const double len = nrm(c);
+  f.n = len > 0 ? c / len : mk(0, 0, 1);
+  f.d = dot(f.n, verts[i0].w);
+  if (dot(f.n, interior) > f.d) {
+    const int t = f.v1;
+    f.v1 = f.v2;
+    f.v2 = t;
+    f.n = -f.n;
+    f.d = -f.d;
+  }
+  return f;
+}
+
+// geometry.cpp:168-205 + 227-324.
+__device__ inline bool epa(SP* simp, int ns, const Hull& A, const Hull& B, double scale, EpaScratch& s,
+                           PairResult& out) {
+  // pad_to_tetrahedron
+  const double tol = 1e-12 * scale;
+  D3 dirs[10];
+  int nd = 0;
+  if (ns == 2) {
+    const D3 d = normalized(simp[1].w - simp[0].w);
+    const D3 t = fabs(d.x) < 0.9 ? mk(1, 0, 0) : mk(0, 1, 0);
+    const D3 e1 = normalized(cross(d, t));
+    const D3 e2 = cross(d, e1);
+    dirs[nd++] = e1;
+    dirs[nd++] = -e1;
+    dirs[nd++] = e2;
+    dirs[nd++] = -e2;
+  }
+  if (ns == 3) {
+    const D3 n = normalized(cross(simp[1].w - simp[0].w, simp[2].w - simp[0].w));
+    dirs[nd++] = n;
+    dirs[nd++] = -n;
+  }
+  dirs[nd++] = mk(1, 0, 0);
+  dirs[nd++] = mk(-1, 0, 0);
+  dirs[nd++] = mk(0, 1, 0);
+  dirs[nd++] = mk(0, -1, 0);
+  dirs[nd++] = mk(0, 0, 1);
+  dirs[nd++] = mk(0, 0, -1);
+  for (int i = 0; i < ns; ++i) s.verts[i] = simp[i];
+  int nv = ns;
+  for (int k = 0; k < nd && nv < 4; ++k) {
+    const SP cand = support_pair(A, B, dirs[k]);
+    bool indep;
+    if (nv == 0) {
+      indep = true;
+    } else if (nv == 1) {
+      indep = nrm(cand.w - s.verts[0].w) > tol;
+    } else if (nv == 2) {
+      const D3 d = normalized(s.verts[1].w - s.verts[0].w);
+      const D3 r = cand.w - s.verts[0].w;
+      indep = nrm(r - d * dot(d, r)) > tol;
+    } else {
+      const D3 n = normalized(cross(s.verts[1].w - s.verts[0].w, s.verts[2].w - s.verts[0].w));
+      indep = fabs(dot(n, cand.w - s.verts[0].w)) > tol;
+    }
+    if (indep) s.verts[nv++] = cand;
+  }
+  if (nv != 4) {
+    out.flags |= kPairDegenerate;
+    return false;
+  }
+  const D3 interior = (s.verts[0].w + s.verts[1].w + s.verts[2].w + s.verts[3].w) / 4.0;
+  int nf = 0;
+  s.faces[nf++] = epa_make_face(s.verts, interior, 0, 1, 2);
+  s.faces[nf++] = epa_make_face(s.verts, interior, 0, 2, 3);
+  s.faces[nf++] = epa_make_face(s.verts, interior, 0, 3, 1);
+  s.faces[nf++] = epa_make_face(s.verts, interior, 1, 3, 2);
+
+  const double grow_tol = 1e-10 * scale;
+  EpaFace best_copy = s.faces[0];
+  for (int iter = 0; iter < kEpaMaxIters; ++iter) {
+    int best = -1;
+    double best_d = INFINITY;
+    for (int i = 0; i < nf; ++i) {
+      const double di = s.faces[i].d;
+      if (di < best_d - 1e-12 * scale ||
+          (di < best_d + 1e-12 * scale && best >= 0 && lex_less(-s.faces[i].n, -s.faces[best].n))) {
+        best_d = fmin(best_d, di);
+        best = i;
+      }
+    }
+    if (best < 0) {
+      out.flags |= kPairDegenerate;
+      return false;
+    }
+    best_copy = s.faces[best];
+    const SP w = support_pair(A, B, best_copy.n);
+    if (dot(best_copy.n, w.w) - best_copy.d <= grow_tol) break;
+    if (nv >= kEpaMaxVerts) {
+      out.flags |= kPairOverflow;
+      break;
+    }
+    const int wi = nv;
+    s.verts[nv++] = w;
+    // Kill visible faces in order, collecting their directed edges.
+    int nh = 0;
+    int kept = 0;
+    bool overflow = false;
+    for (int i = 0; i < nf; ++i) {
+      const EpaFace f = s.faces[i];
+      if (dot(f.n, w.w) - f.d > 1e-12 * scale) {
+        if (nh + 3 > kEpaMaxHorizon) {
+          overflow = true;
+        } else {
+          s.hu[nh] = f.v0; s.hv[nh++] = f.v1;
+          s.hu[nh] = f.v1; s.hv[nh++] = f.v2;
+          s.hu[nh] = f.v2; s.hv[nh++] = f.v0;
+        }
+      } else {
+        s.faces[kept++] = f;
+      }
+    }
+    nf = kept;
+    if (overflow) {
+      out.flags |= kPairOverflow;
+      break;
+    }
+    int n_boundary = 0;
+    for (int e = 0; e < nh; ++e) {
+      bool paired = false;
+      for (int o = 0; o < nh; ++o)
+        if (s.hu[o] == s.hv[e] && s.hv[o] == s.hu[e]) paired = true;
+      if (!paired) {
+        if (nf >= kEpaMaxFaces) {
+          overflow = true;
+          break;
+        }
+        s.faces[nf++] = epa_make_face(s.verts, interior, s.hu[e], s.hv[e], wi);
+        ++n_boundary;
+      }
+    }
+    if (overflow) {
+      out.flags |= kPairOverflow;
+      break;
+    }
+    if (n_boundary == 0) break;
+  }
+  out.d = -fmax(best_copy.d, 0.0);
+  out.n = -best_copy.n;
+  const SP tri[3] = {s.verts[best_copy.v0], s.verts[best_copy.v1], s.verts[best_copy.v2]};
+  const Simplex sx = closest_on_simplex(tri, 3);
+  D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
+  double wsum = 0.0;
+  for (int i = 0; i < sx.nkeep; ++i) {
+    wa += sx.wts[i] * tri[sx.keep[i]].a;
+    wb += sx.wts[i] * tri[sx.keep[i]].b;
+    wsum += sx.wts[i];
+  }
+  if (wsum > 0.5) {
+    out.pa = wa;
+    out.pb = wb;
+  } else {
+    out.pa = tri[0].a;
+    out.pb = tri[0].b;
+  }
+  out.flags |= kPairEpa;
+  return true;
+}
+
+// signed_distance(a, pose_a, b, identity) (geometry.cpp:500-525).
+__device__ inline PairResult signed_distance(const Hull& A, const Hull& B, double scale, EpaScratch& scratch) {
+  PairResult out;
+  out.flags = 0;
+  SP simp[4];
+  int ns = 1;
+  simp[0] = support_pair(A, B, mk(1, 0, 0));
+  bool done = false;
+  bool overlap = false;
+  Simplex sx;
+  for (int iter = 0; iter < kGjkMaxIters && !done; ++iter) {
+    sx = closest_on_simplex(simp, ns);
+    SP red[4];
+    for (int i = 0; i < sx.nkeep; ++i) red[i] = simp[sx.keep[i]];
+    ns = sx.nkeep;
+    for (int i = 0; i < ns; ++i) simp[i] = red[i];
+    if (sx.contains || sqrt(sx.dist2) < kTouchTol * scale) {
+      overlap = true;
+      done = true;
+      break;
+    }
+    const SP w = support_pair(A, B, -sx.v);
+    const double gap = sx.dist2 - dot(sx.v, w.w);
+    bool repeat = false;
+    for (int i = 0; i < ns; ++i)
+      if (nrm(simp[i].w - w.w) < 1e-14 * scale) repeat = true;
+    if (gap <= kGjkRelTol * sx.dist2 + 1e-300 || repeat || ns == 4) {
+      done = true;
+      break;
+    }
+    simp[ns++] = w;
+  }
+  if (!done) {
+    // Iteration cap: current estimate from the unreduced simplex.
+    sx = closest_on_simplex(simp, ns);
+    D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
+    for (int i = 0; i < sx.nkeep; ++i) {
+      wa += sx.wts[i] * simp[sx.keep[i]].a;
+      wb += sx.wts[i] * simp[sx.keep[i]].b;
+    }
+    const double d = sqrt(sx.dist2);
+    out.d = d;
+    out.pa = wa;
+    out.pb = wb;
+    out.n = d > 1e-14 ? (wa - wb) / d : mk(0, 0, 1);
+    return out;
+  }
+  if (!overlap) {
+    D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
+    for (int i = 0; i < ns; ++i) {
+      wa += sx.wts[i] * simp[i].a;
+      wb += sx.wts[i] * simp[i].b;
+    }
+    const double d = sqrt(sx.dist2);
+    out.d = d;
+    out.pa = wa;
+    out.pb = wb;
+    out.n = d > 1e-14 ? (wa - wb) / d : mk(0, 0, 1);
+    return out;
+  }
+  epa(simp, ns, A, B, scale, scratch, out);
+  return out;
+}
+
+}  // namespace gdev

@@ -1,0 +1,1204 @@
+// sm_100a kernels of the bilevel grasp-synthesis loop.
+//
+// Per upper-level iteration (reference total_energy + apply_step,
+// proj/src/pipeline.cpp:96-231):
+//   coarse stage: k_point_query -> k_qp -> k_step<coarse>
+//   mesh stages:  k_point_query(tips) -> k_pairs -> k_step<mesh>
+// k_step ends with the forward kinematics of the new state and writes the
+// next iteration's query points, so there is no separate FK launch inside a
+// stage. All arithmetic is fp64 like the reference; every reduction runs in
+// a fixed order so results do not depend on batch size or scheduling.
+#pragma once
+
+#include "dmath.cuh"
+#include "gjk.cuh"
+#include "model.cuh"
+
+namespace gdev {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ----------------------------------------------------------------- helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;  // butterfly: identical on every lane
+}
+
+// Fixed-order sum of `v` over lanes base..base+cnt-1, identical on all lanes.
+__device__ __forceinline__ double group_sum(double v, int base, int cnt) {
+  double s = 0.0;
+  for (int b = 0; b < cnt; ++b) s += __shfl_sync(kFull, v, base + b);
+  return s;
+}
+__device__ __forceinline__ double group_max(double v, int base, int cnt) {
+  double s = 0.0;
+  for (int b = 0; b < cnt; ++b) s = fmax(s, __shfl_sync(kFull, v, base + b));
+  return s;
+}
+
+struct Pose {
+  M33 R;
+  D3 t;
+  M33 a_inv;
+  bool degenerate;
+};
+
+__device__ __forceinline__ void store_pose(double* p, const Pose& ps) {
+  for (int i = 0; i < 9; ++i) p[i] = ps.R.m[i];
+  st3(p + 9, ps.t);
+  for (int i = 0; i < 9; ++i) p[12 + i] = ps.a_inv.m[i];
+  p[21] = ps.degenerate ? 1.0 : 0.0;
+}
+__device__ __forceinline__ Pose load_pose(const double* p) {
+  Pose ps;
+  for (int i = 0; i < 9; ++i) ps.R.m[i] = p[i];
+  ps.t = ld3(p + 9);
+  for (int i = 0; i < 9; ++i) ps.a_inv.m[i] = p[12 + i];
+  ps.degenerate = p[21] != 0.0;
+  return ps;
+}
+
+// make_pose_state + pose_from_state (hand.cpp:75-116): raw block is
+// column-major in x.
+__device__ inline Pose compute_pose(const double* x) {
+  M33 raw;
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < 3; ++i) raw.m[i * 3 + c] = x[3 * c + i];
+  Pose ps;
+  bool fallback = false;
+  ps.R = project_rotation(raw, &fallback);
+  ps.t = mk(x[9], x[10], x[11]);
+  ps.a_inv = eye();
+  ps.degenerate = fallback;
+  if (!fallback) ps.degenerate = !pose_a_inv(ps.R, raw, ps.a_inv);
+  return ps;
+}
+
+// Per-warp scratch of the warp-per-grasp kernels.
+struct WarpScratch {
+  double x[kMaxDims];
+  double xn[kMaxDims];
+  double grad[kMaxDims];
+  double pose[24];
+  double world[kMaxLinks * 12];
+  double jo[kMaxDof * 6];
+  double pc[kMaxProxies * 3];
+  double itF[32 * 3];
+  double itT[32 * 3];
+  int itL[32];
+  double red[32];
+  int flag[4];
+};
+
+// Forward kinematics for one grasp (hand.cpp:126-153): lane 0 projects the
+// rotation, lane l < L walks its root-to-l path (same op sequence as the
+// sequential reference), then proxy centers and the coarse FD stencil points
+// are written as the next iteration's point queries.
+__device__ inline void warp_fk(const DevHand& H, const DevState& st, int g, int lane, WarpScratch& s, double fd_step,
+                               bool write_state) {
+  if (lane == 0) {
+    const Pose ps = compute_pose(s.x);
+    store_pose(s.pose, ps);
+  }
+  __syncwarp();
+  const Pose base = load_pose(s.pose);
+  if (lane < H.L) {
+    const int l = lane;
+    M33 Rc = eye();
+    D3 tc = mk(0, 0, 0);
+    const int depth = H.link_depth[l];
+    for (int d = 0; d < depth; ++d) {
+      const int p = H.link_path[l * kMaxDepth + d];
+      const int j = H.link_parent_joint[p];
+      if (j < 0) continue;  // base link: identity chain
+      const D3 origin = ld3(H.joint_origin + 3 * j);
+      const D3 axis = ld3(H.joint_axis + 3 * j);
+      const M33 Rs = angle_axis(s.x[12 + j], axis);
+      const D3 jo = mul(Rc, origin) + tc;  // parent.apply(origin)
+      const M33 Rn = mul(Rc, Rs);
+      if (p == l) {
+        st3(s.jo + 6 * j, jo);
+        st3(s.jo + 6 * j + 3, mul(Rn, axis));
+      }
+      Rc = Rn;
+      tc = jo;
+    }
+    const M33 Rw = mul(base.R, Rc);
+    const D3 tw = mul(base.R, tc) + base.t;
+    for (int i = 0; i < 9; ++i) s.world[l * 12 + i] = Rw.m[i];
+    st3(s.world + l * 12 + 9, tw);
+  }
+  __syncwarp();
+  for (int p = lane; p < H.S; p += 32) {
+    const int l = H.proxy_link[p];
+    M33 Rw;
+    for (int i = 0; i < 9; ++i) Rw.m[i] = s.world[l * 12 + i];
+    const D3 c = mul(Rw, ld3(H.proxy + 4 * p)) + ld3(s.world + l * 12 + 9);
+    st3(s.pc + 3 * p, c);
+  }
+  __syncwarp();
+  if (!write_state) return;
+  double* gp = st.pose + (size_t)g * 24;
+  for (int i = lane; i < 24; i += 32) gp[i] = s.pose[i];
+  double* gw = st.world + (size_t)g * H.L * 12;
+  for (int i = lane; i < H.L * 12; i += 32) gw[i] = s.world[i];
+  double* gj = st.joints + (size_t)g * H.dof * 6;
+  for (int i = lane; i < H.dof * 6; i += 32) gj[i] = s.jo[i];
+  double* q = st.qpts + (size_t)g * st.NQ * 3;
+  for (int p = lane; p < H.S; p += 32) st3(q + 3 * p, ld3(s.pc + 3 * p));
+  for (int t = lane; t < 6 * H.m; t += 32) {
+    const int f = t / 6, k = (t % 6) / 2;
+    const double sign = (t & 1) ? -1.0 : 1.0;
+    D3 c = ld3(s.pc + 3 * H.tip_proxy[f]);
+    // c +/- h e_k touches only component k (pipeline.cpp:150-152).
+    if (k == 0) c.x = c.x + sign * fd_step;
+    if (k == 1) c.y = c.y + sign * fd_step;
+    if (k == 2) c.z = c.z + sign * fd_step;
+    st3(q + 3 * (H.S + t), c);
+  }
+}
+
+__device__ inline void load_fk(const DevHand& H, const DevState& st, int g, int lane, WarpScratch& s) {
+  const double* gp = st.pose + (size_t)g * 24;
+  for (int i = lane; i < 24; i += 32) s.pose[i] = gp[i];
+  const double* gw = st.world + (size_t)g * H.L * 12;
+  for (int i = lane; i < H.L * 12; i += 32) s.world[i] = gw[i];
+  const double* gj = st.joints + (size_t)g * H.dof * 6;
+  for (int i = lane; i < H.dof * 6; i += 32) s.jo[i] = gj[i];
+  __syncwarp();
+  for (int p = lane; p < H.S; p += 32) {
+    const int l = H.proxy_link[p];
+    M33 Rw;
+    for (int i = 0; i < 9; ++i) Rw.m[i] = s.world[l * 12 + i];
+    st3(s.pc + 3 * p, mul(Rw, ld3(H.proxy + 4 * p)) + ld3(s.world + l * 12 + 9));
+  }
+  __syncwarp();
+}
+
+// --------------------------------------------------------- point queries
+// Ericson closest point on a triangle (geometry.cpp:327-347).
+__device__ __forceinline__ D3 closest_on_triangle(D3 p, D3 a, D3 b, D3 c) {
+  const D3 ab = b - a, ac = c - a, ap = p - a;
+  const double d1 = dot(ab, ap), d2 = dot(ac, ap);
+  if (d1 <= 0 && d2 <= 0) return a;
+  const D3 bp = p - b;
+  const double d3 = dot(ab, bp), d4 = dot(ac, bp);
+  if (d3 >= 0 && d4 <= d3) return b;
+  const double vc = d1 * d4 - d3 * d2;
+  if (vc <= 0 && d1 >= 0 && d3 <= 0) return a + ab * (d1 / (d1 - d3));
+  const D3 cp = p - c;
+  const double d5 = dot(ab, cp), d6 = dot(ac, cp);
+  if (d6 >= 0 && d5 <= d6) return c;
+  const double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0 && d2 >= 0 && d6 <= 0) return a + ac * (d2 / (d2 - d6));
+  const double va = d3 * d6 - d5 * d4;
+  if (va <= 0 && d4 - d3 >= 0 && d5 - d6 >= 0) return b + (c - b) * ((d4 - d3) / ((d4 - d3) + (d5 - d6)));
+  const double denom = 1.0 / (va + vb + vc);
+  return a + ab * (vb * denom) + ac * (vc * denom);
+}
+
+struct PointHit {
+  double d;
+  D3 pb, n;
+  int part;
+};
+
+// point_to_mesh (geometry.cpp:527-542) with query_part (:355-395): inside
+// test breaking at the first plane with depth < -1e-12, else the brute-force
+// closest point with strict '<' over faces and parts.
+__device__ inline PointHit point_to_mesh(const DevObject& O, D3 p) {
+  PointHit best;
+  best.d = INFINITY;
+  best.pb = mk(0, 0, 0);
+  best.n = mk(0, 0, 1);
+  best.part = -1;
+  for (int part = 0; part < O.P; ++part) {
+    const int f0 = __ldg(O.part_fbeg + part), f1 = __ldg(O.part_fbeg + part + 1);
+    bool inside = true;
+    double min_depth = INFINITY;
+    D3 best_n = mk(0, 0, 1);
+    for (int f = f0; f < f1; ++f) {
+      const double* F = O.faces + (size_t)f * kFaceStride;
+      if (__ldg(F + 13) == 0.0) continue;  // degenerate face (len < 1e-30)
+      const D3 n = ldg3(F + 9);
+      const double depth = __ldg(F + 12) - dot(n, p);
+      if (depth < -1e-12) {
+        inside = false;
+        break;
+      }
+      if (depth < min_depth) {
+        min_depth = depth;
+        best_n = n;
+      }
+    }
+    double sd;
+    D3 pt, nn;
+    if (inside && isfinite(min_depth)) {
+      sd = -min_depth;
+      nn = best_n;
+      pt = p + best_n * min_depth;
+    } else {
+      sd = INFINITY;
+      pt = mk(0, 0, 0);
+      for (int f = f0; f < f1; ++f) {
+        const double* F = O.faces + (size_t)f * kFaceStride;
+        const D3 c = closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6));
+        const double d = nrm(p - c);
+        if (d < sd) {
+          sd = d;
+          pt = c;
+        }
+      }
+      nn = sd > 1e-14 ? (p - pt) / sd : mk(0, 0, 1);
+    }
+    if (sd < best.d) {
+      best.d = sd;
+      best.pb = pt;
+      best.n = nn;
+      best.part = part;
+    }
+  }
+  return best;
+}
+
+// One thread per (grasp, query slot). slots == nullptr: all NQ slots.
+__global__ void k_point_query(DevObject O, DevState st, const int* __restrict__ slots, int n_slots) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = slots ? n_slots : st.NQ;
+  if (t >= (long long)st.G * per) return;
+  const int g = (int)(t / per);
+  const int slot = slots ? slots[t % per] : (int)(t % per);
+  if (st.failed[g]) return;
+  const D3 p = ld3(st.qpts + ((size_t)g * st.NQ + slot) * 3);
+  const PointHit h = point_to_mesh(O, p);
+  double* o = st.qres + ((size_t)g * st.NQ + slot) * 8;
+  o[0] = h.d;
+  st3(o + 1, h.pb);
+  st3(o + 4, h.n);
+  o[7] = h.part;
+}
+
+// Standalone query surface (teacher-forced tests).
+__global__ void k_points_raw(DevObject O, int n, const double* __restrict__ pts, double* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const PointHit h = point_to_mesh(O, ld3(pts + 3 * t));
+  double* o = out + 8 * t;
+  o[0] = h.d;
+  st3(o + 1, h.pb);
+  st3(o + 4, h.n);
+  o[7] = h.part;
+}
+
+// ------------------------------------------------------------ GJK pairs
+__device__ __forceinline__ double scale_of(D3 centroid_world, double halfnorm) {
+  return nrm(centroid_world) + 2.0 * halfnorm;
+}
+
+__device__ inline PairResult link_part_distance(const DevHand& H, const DevObject& O, int link, int part,
+                                                const M33& Rw, D3 tw, EpaScratch& scratch) {
+  Hull A;
+  A.verts = H.link_verts + 3 * (size_t)H.link_vbeg[link];
+  A.nv = H.link_vbeg[link + 1] - H.link_vbeg[link];
+  A.posed = true;
+  A.R = Rw;
+  A.t = tw;
+  Hull B;
+  B.verts = O.verts + 3 * (size_t)O.part_vbeg[part];
+  B.nv = O.part_vbeg[part + 1] - O.part_vbeg[part];
+  B.posed = false;
+  B.R = eye();
+  B.t = mk(0, 0, 0);
+  // cloud_scale (geometry.cpp:17-23).
+  double scale = 1.0;
+  scale = fmax(scale, scale_of(mul(Rw, ld3(H.link_centroid + 3 * link)) + tw, H.link_halfnorm[link]));
+  scale = fmax(scale, scale_of(ld3(O.part_centroid + 3 * part), O.part_halfnorm[part]));
+  return signed_distance(A, B, scale, scratch);
+}
+
+__device__ __forceinline__ void store_pair(double* o, const PairResult& r) {
+  o[0] = r.d;
+  st3(o + 1, r.pa);
+  st3(o + 4, r.pb);
+  st3(o + 7, r.n);
+  o[10] = r.flags;
+}
+
+// One thread per (grasp, link, part); consecutive threads share (link, part)
+// so the support scans read the same vertices across the warp.
+__global__ void __launch_bounds__(128) k_pairs(DevHand H, DevObject O, DevState st, const int* __restrict__ links,
+                                               int n_links) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)st.G * n_links * O.P) return;
+  const int g = (int)(t % st.G);
+  const int lp = (int)(t / st.G);
+  const int link = links ? links[lp / O.P] : lp / O.P;
+  const int part = lp % O.P;
+  if (st.failed[g]) return;
+  const double* w = st.world + ((size_t)g * H.L + link) * 12;
+  M33 Rw;
+  for (int i = 0; i < 9; ++i) Rw.m[i] = w[i];
+  EpaScratch scratch;
+  const PairResult r = link_part_distance(H, O, link, part, Rw, ld3(w + 9), scratch);
+  store_pair(st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12, r);
+  if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
+  if (r.flags & kPairOverflow) atomicAdd(st.err + 1, 1);
+}
+
+// Standalone pair surface (teacher-forced tests): poses[n*12] column-major R + t.
+__global__ void k_pairs_raw(DevHand H, DevObject O, int n, const int* __restrict__ links, const int* __restrict__ parts,
+                            const double* __restrict__ poses, double* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  M33 Rw;
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < 3; ++i) Rw.m[i * 3 + c] = poses[12 * t + 3 * c + i];
+  EpaScratch scratch;
+  const PairResult r = link_part_distance(H, O, links[t], parts[t], Rw, ld3(poses + 12 * t + 9), scratch);
+  store_pair(out + 11 * t, r);
+  out[11 * t + 10] = r.flags;
+}
+
+// --------------------------------------------------------------- the QP
+// Lower-level QP batch of one grasp (energy.cpp:60-92, qpsolve.cpp:45-120,
+// 193-235). Lane (j, c) = (closure direction j, contact block c) owns the
+// k edge weights of contact c in column j, the identity rows of those
+// weights and the contact-cap row c; the total-weight row is replicated in
+// the m lanes of a column. The K = P + sigma I + rho A'A solve uses the
+// structure K = B + U U^T (B block-diagonal, U = [sqrt2 W^T | sqrt(rho) 1],
+// rank 7) through Woodbury with a 7x7 capacitance inverse, so a sweep costs
+// O(k) per lane plus 8 fixed-order column reductions.
+struct QpSmem {
+  double frame[kMaxTips * 12];
+  double W[6 * kMaxTips * kMaxEdges];   // row-major 6 x n
+  double Gm[kMaxTips * kMaxEdges * 7];  // B^-1 U, n x 7
+  double Hm[49];                        // (I + U^T B^-1 U)^-1
+  double C[49];
+};
+
+__device__ __forceinline__ void build_frame(D3 p, D3 n, double* f) {
+  // contact.cpp:9-21; n is the inward normal.
+  const D3 seed = fabs(n.x) > 0.99 ? mk(0, 1, 0) : mk(1, 0, 0);
+  const D3 d = normalized(cross(n, seed));
+  const D3 e = cross(n, d);
+  st3(f, p);
+  st3(f + 3, n);
+  st3(f + 6, d);
+  st3(f + 9, e);
+}
+
+// mode 0: coarse (frames from the tip point queries, warm start from the
+// per-grasp scratch, envelope-gradient forces written when with_grad).
+// mode 1: final record (frames from st.frames, cold start).
+// mode 2: standalone batch (frames from st.frames, warm if qp_ready).
+__global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st, int m, int mode, int with_grad) {
+  __shared__ QpSmem smem_all[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * 4 + warp;
+  if (g >= st.G) return;
+  if (st.failed[g]) return;
+  QpSmem& s = smem_all[warp];
+  const int k = P.k, n = m * k, M = m + 1 + n;
+
+  // Frames.
+  if (lane < m) {
+    if (mode == 0) {
+      const double* q = st.qres + ((size_t)g * st.NQ + H.tip_proxy[lane]) * 8;
+      build_frame(ld3(q + 1), -ld3(q + 4), s.frame + 12 * lane);
+    } else {
+      const double* f = st.frames + ((size_t)g * m + lane) * 12;
+      for (int i = 0; i < 12; ++i) s.frame[12 * lane + i] = f[i];
+    }
+  }
+  __syncwarp();
+  const double a_diag = P.sigma + P.rho;
+  const double betap = P.rho / (a_diag + k * P.rho);
+  const double sqrt2 = 1.4142135623730951, sqrt_rho = sqrt(P.rho);
+  // Wrench basis block c (contact.cpp:47-53) and B^-1 U rows.
+  if (lane < m) {
+    const int c = lane;
+    const D3 p = ld3(s.frame + 12 * c), nn = ld3(s.frame + 12 * c + 3);
+    const D3 d = ld3(s.frame + 12 * c + 6), e = ld3(s.frame + 12 * c + 9);
+    for (int j = 0; j < k; ++j) {
+      const D3 edge = nn + P.mu * (P.cos_t[j] * d + P.sin_t[j] * e);
+      const D3 tq = cross(p, edge);
+      const int col = c * k + j;
+      s.W[0 * n + col] = edge.x;
+      s.W[1 * n + col] = edge.y;
+      s.W[2 * n + col] = edge.z;
+      s.W[3 * n + col] = tq.x;
+      s.W[4 * n + col] = tq.y;
+      s.W[5 * n + col] = tq.z;
+    }
+    for (int q = 0; q < 7; ++q) {
+      double bs = 0.0;
+      for (int j = 0; j < k; ++j) bs += q < 6 ? sqrt2 * s.W[q * n + c * k + j] : sqrt_rho;
+      for (int j = 0; j < k; ++j) {
+        const double u = q < 6 ? sqrt2 * s.W[q * n + c * k + j] : sqrt_rho;
+        s.Gm[(c * k + j) * 7 + q] = (u - betap * bs) / a_diag;
+      }
+    }
+  }
+  __syncwarp();
+  // Capacitance C = I + U^T G (symmetric, 28 unique entries).
+  if (lane < 28) {
+    int p = 0, q = lane;
+    while (q >= 7 - p) {
+      q -= 7 - p;
+      ++p;
+    }
+    q += p;
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double u = p < 6 ? sqrt2 * s.W[p * n + i] : sqrt_rho;
+      acc += u * s.Gm[i * 7 + q];
+    }
+    const double v = acc + (p == q ? 1.0 : 0.0);
+    s.C[p * 7 + q] = v;
+    s.C[q * 7 + p] = v;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    // Cholesky of C, then H = C^-1 column by column.
+    double L[49];
+    for (int i = 0; i < 49; ++i) L[i] = 0.0;
+    for (int j = 0; j < 7; ++j) {
+      double dsum = s.C[j * 7 + j];
+      for (int q = 0; q < j; ++q) dsum -= L[j * 7 + q] * L[j * 7 + q];
+      const double ljj = sqrt(dsum);
+      L[j * 7 + j] = ljj;
+      for (int i = j + 1; i < 7; ++i) {
+        double v = s.C[i * 7 + j];
+        for (int q = 0; q < j; ++q) v -= L[i * 7 + q] * L[j * 7 + q];
+        L[i * 7 + j] = v / ljj;
+      }
+    }
+    for (int cidx = 0; cidx < 7; ++cidx) {
+      double y[7];
+      for (int i = 0; i < 7; ++i) {
+        double v = i == cidx ? 1.0 : 0.0;
+        for (int q = 0; q < i; ++q) v -= L[i * 7 + q] * y[q];
+        y[i] = v / L[i * 7 + i];
+      }
+      for (int i = 6; i >= 0; --i) {
+        double v = y[i];
+        for (int q = i + 1; q < 7; ++q) v -= L[q * 7 + i] * y[q];
+        y[i] = v / L[i * 7 + i];
+      }
+      for (int i = 0; i < 7; ++i) s.Hm[i * 7 + cidx] = y[i];
+    }
+  }
+  __syncwarp();
+
+  const bool active = lane < 6 * m;
+  const int j = active ? lane / m : 0;
+  const int c = active ? lane % m : 0;
+  const int base = j * m;
+  const int axis = j >> 1;
+  const double tsign = (j & 1) ? -1.0 : 1.0;
+  const double rho = P.rho, sigma = P.sigma, alpha = P.alpha;
+  const double inv_a = 1.0 / a_diag;
+  const double inv_rho = 1.0 / rho;
+
+  double x[kMaxEdges], zid[kMaxEdges], yid[kMaxEdges], q[kMaxEdges], xs[kMaxEdges];
+  double zc, yc, ztot, ytot;
+  const bool warm = (mode == 0 || mode == 2) && st.qp_ready[g];
+  const double* wx = st.warm_x + (size_t)g * n * 6;
+  const double* wy = st.warm_y + (size_t)g * M * 6;
+#pragma unroll
+  for (int e = 0; e < kMaxEdges; ++e) {
+    if (e < k) {
+      const int i = c * k + e;
+      x[e] = warm ? wx[j * n + i] : 0.0;
+      yid[e] = warm ? wy[j * M + m + 1 + i] : 0.0;
+      q[e] = (-2.0 * P.beta) * (tsign * s.W[axis * n + i]);
+    } else {
+      x[e] = yid[e] = q[e] = 0.0;
+    }
+    zid[e] = x[e];
+    xs[e] = x[e];
+  }
+  yc = warm ? wy[j * M + c] : 0.0;
+  ytot = warm ? wy[j * M + m] : 0.0;
+  {
+    double bs = 0.0;
+    for (int e = 0; e < k; ++e) bs += x[e];
+    zc = bs;
+    ztot = group_sum(bs, base, m);
+  }
+  const double gamma = P.gamma_total;
+  bool frozen = !active;
+  double* ox = st.warm_x + (size_t)g * n * 6;
+  double* oy = st.warm_y + (size_t)g * M * 6;
+  double* oz = st.out_z + (size_t)g * M * 6;
+
+  for (int iter = 1; iter <= P.max_iters; ++iter) {
+    // rhs = A'(rho z - y) + sigma x - q
+    const double vc = rho * zc - yc, vt = rho * ztot - ytot;
+    double rhs[kMaxEdges];
+    double bsum = 0.0;
+#pragma unroll
+    for (int e = 0; e < kMaxEdges; ++e) {
+      if (e < k) {
+        const double vi = rho * zid[e] - yid[e];
+        rhs[e] = ((vc + vt) + vi) + (sigma * x[e] - q[e]);
+        bsum += rhs[e];
+      } else {
+        rhs[e] = 0.0;
+      }
+    }
+    // t = G^T rhs over the column, s = H t
+    double tv[7];
+#pragma unroll
+    for (int p = 0; p < 7; ++p) {
+      double acc = 0.0;
+      for (int e = 0; e < k; ++e) acc += s.Gm[(c * k + e) * 7 + p] * rhs[e];
+      tv[p] = group_sum(acc, base, m);
+    }
+    double sv[7];
+#pragma unroll
+    for (int p = 0; p < 7; ++p) {
+      double acc = 0.0;
+#pragma unroll
+      for (int r = 0; r < 7; ++r) acc += s.Hm[p * 7 + r] * tv[r];
+      sv[p] = acc;
+    }
+    // xt = B^-1 rhs - G s ; zt = A xt
+    double xt[kMaxEdges];
+    double ztc = 0.0;
+#pragma unroll
+    for (int e = 0; e < kMaxEdges; ++e) {
+      if (e < k) {
+        double gs = 0.0;
+#pragma unroll
+        for (int p = 0; p < 7; ++p) gs += s.Gm[(c * k + e) * 7 + p] * sv[p];
+        xt[e] = (rhs[e] - betap * bsum) * inv_a - gs;
+        ztc += xt[e];
+      } else {
+        xt[e] = 0.0;
+      }
+    }
+    const double ztt = group_sum(ztc, base, m);
+    // Relaxed updates and projection.
+#pragma unroll
+    for (int e = 0; e < kMaxEdges; ++e) {
+      if (e < k) {
+        x[e] = alpha * xt[e] + (1.0 - alpha) * x[e];
+        const double zbar = alpha * xt[e] + (1.0 - alpha) * zid[e];
+        const double zn = fmax(zbar + yid[e] * inv_rho, 0.0);
+        yid[e] += rho * (zbar - zn);
+        zid[e] = zn;
+      }
+    }
+    {
+      const double zbar = alpha * ztc + (1.0 - alpha) * zc;
+      const double zn = fmin(fmax(zbar + yc * inv_rho, 0.0), 1.0);
+      yc += rho * (zbar - zn);
+      zc = zn;
+    }
+    {
+      const double zbar = alpha * ztt + (1.0 - alpha) * ztot;
+      const double zn = fmax(zbar + ytot * inv_rho, gamma);
+      ytot += rho * (zbar - zn);
+      ztot = zn;
+    }
+    if (iter % P.check_interval == 0 || iter == P.max_iters) {
+      double axc = 0.0;
+      for (int e = 0; e < k; ++e) axc += x[e];
+      const double axt = group_sum(axc, base, m);
+      double rp = fmax(fabs(axc - zc), fabs(axt - ztot));
+      for (int e = 0; e < k; ++e) rp = fmax(rp, fabs(x[e] - zid[e]));
+      rp = group_max(rp, base, m);
+      double wx6[6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        double acc = 0.0;
+        for (int e = 0; e < k; ++e) acc += s.W[r * n + c * k + e] * x[e];
+        wx6[r] = group_sum(acc, base, m);
+      }
+      double rd = 0.0;
+      for (int e = 0; e < k; ++e) {
+        double px = 0.0;
+#pragma unroll
+        for (int r = 0; r < 6; ++r) px += s.W[r * n + c * k + e] * wx6[r];
+        const double dual = (2.0 * px + ((yc + ytot) + yid[e])) + q[e];
+        rd = fmax(rd, fabs(dual));
+      }
+      rd = group_max(rd, base, m);
+      if (!frozen) {
+        const bool ok = rp <= P.eps_primal && rd <= P.eps_dual;
+        if (ok || iter == P.max_iters) {
+          frozen = true;
+          for (int e = 0; e < k; ++e) {
+            const int i = c * k + e;
+            xs[e] = x[e];
+            ox[j * n + i] = x[e];
+            oy[j * M + m + 1 + i] = yid[e];
+            oz[j * M + m + 1 + i] = zid[e];
+          }
+          oy[j * M + c] = yc;
+          oz[j * M + c] = zc;
+          if (c == 0) {
+            oy[j * M + m] = ytot;
+            oz[j * M + m] = ztot;
+            st.qp_iters[(size_t)g * 6 + j] = iter;
+            st.qp_conv[(size_t)g * 6 + j] = ok ? 1 : 0;
+          }
+        }
+      }
+      if (__all_sync(kFull, frozen)) break;
+    }
+  }
+  if (lane == 0) st.qp_ready[g] = 1;
+
+  // Energy report from the snapshot (energy.cpp:78-90).
+  double res[6];
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+    double acc = 0.0;
+    for (int e = 0; e < k; ++e) acc += s.W[r * n + c * k + e] * xs[e];
+    const double wl = group_sum(acc, base, m);
+    res[r] = P.beta * (r == axis ? tsign : 0.0) - wl;
+  }
+  double pd = 0.0;
+#pragma unroll
+  for (int r = 0; r < 6; ++r) pd += res[r] * res[r];
+  if (active && c == 0) st.qp_perdir[(size_t)g * 6 + j] = pd;
+  double total = 0.0;
+  for (int jj = 0; jj < 6; ++jj) total += __shfl_sync(kFull, pd, jj * m);
+  if (lane == 0) st.qp_energy[g] = total;
+  if (!with_grad) return;
+
+  // Envelope gradient (energy.cpp:94-145) reduced to one force per tip.
+  const D3 p = ld3(s.frame + 12 * c), nn = ld3(s.frame + 12 * c + 3);
+  const D3 dd = ld3(s.frame + 12 * c + 6), ee = ld3(s.frame + 12 * c + 9);
+  const D3 seed = fabs(nn.x) > 0.99 ? mk(0, 1, 0) : mk(1, 0, 0);
+  const double cnorm = nrm(cross(nn, seed));
+  const D3 rf = mk(res[0], res[1], res[2]), rt = mk(res[3], res[4], res[5]);
+  double sum = 0.0, sum_cos = 0.0, sum_sin = 0.0;
+  D3 fsum = mk(0, 0, 0);
+  for (int e = 0; e < k; ++e) {
+    sum += xs[e];
+    sum_cos += xs[e] * P.cos_t[e];
+    sum_sin += xs[e] * P.sin_t[e];
+    fsum += xs[e] * (nn + P.mu * (P.cos_t[e] * dd + P.sin_t[e] * ee));
+  }
+  const D3 gv = rf + cross(rt, p);
+  // md^T g with md = -(I - d d^T)[seed]x / cnorm  ->  md^T g = (seed x ((I - d d^T) g)) / cnorm
+  const D3 proj = gv - dd * dot(dd, gv);
+  const D3 mdTg = cross(seed, proj) / cnorm;
+  // me = [n]x md - [d]x  ->  me^T g = md^T([n]x^T g) - [d]x^T g = md^T(g x n) + d x g ... expanded:
+  const D3 gxn = cross(gv, nn);
+  const D3 proj2 = gxn - dd * dot(dd, gxn);
+  const D3 meTg = cross(seed, proj2) / cnorm + cross(dd, gv);
+  const D3 an = sum * gv + (P.mu * sum_cos) * mdTg + (P.mu * sum_sin) * meTg;
+  const D3 ap = cross(fsum, rt);
+  // Sum over the 6 directions of contact c, fixed order.
+  D3 AN = mk(0, 0, 0), AP;
+  AP = mk(0, 0, 0);
+  for (int jj = 0; jj < 6; ++jj) {
+    const int src = jj * m + c;
+    AN.x += __shfl_sync(kFull, an.x, src);
+    AN.y += __shfl_sync(kFull, an.y, src);
+    AN.z += __shfl_sync(kFull, an.z, src);
+    AP.x += __shfl_sync(kFull, ap.x, src);
+    AP.y += __shfl_sync(kFull, ap.y, src);
+    AP.z += __shfl_sync(kFull, ap.z, src);
+  }
+  if (active && j == 0) {
+    const double* qb = st.qres + (size_t)g * st.NQ * 8;
+    const double h2 = 2.0 * P.fd_step;
+    D3 dpT_AP, dnT_AN;  // (dp^T AP)_k = dp.col(k) . AP
+    double vals_p[3], vals_n[3];
+    for (int kk = 0; kk < 3; ++kk) {
+      const double* qp = qb + (size_t)(H.S + c * 6 + 2 * kk) * 8;
+      const double* qm = qb + (size_t)(H.S + c * 6 + 2 * kk + 1) * 8;
+      const D3 dpc = (ld3(qp + 1) - ld3(qm + 1)) / h2;
+      const D3 dnc = (ld3(qp + 4) - ld3(qm + 4)) / h2;
+      vals_p[kk] = dot(dpc, AP);
+      vals_n[kk] = dot(dnc, AN);
+    }
+    dpT_AP = mk(vals_p[0], vals_p[1], vals_p[2]);
+    dnT_AN = mk(vals_n[0], vals_n[1], vals_n[2]);
+    const D3 F = (-2.0 * P.w_grasp) * (dpT_AP - dnT_AN);
+    st3(st.qp_force + ((size_t)g * m + c) * 3, F);
+  }
+}
+
+// ------------------------------------------------------ gradient assembly
+// A force f (world) at world point p on link l contributes J(l,p)^T f to
+// the state gradient (hand.cpp:155-169). With v = R^T (p - t) and
+// f' = R^T f this is: rotation block J_tan^T (v x f'), translation f, joint j
+// (ancestor of l) a_j . ((v - o_j) x f'). Forces are therefore accumulated
+// per link as F_l = sum f', T_l = sum v x f' and expanded once per iteration.
+struct LinkAcc {
+  D3 F, T;
+};
+
+// Adds one chunk of up to 32 items (item lane t owns itL/itF/itT[t]) to the
+// per-link accumulator held by lane == link. Fixed item order.
+__device__ __forceinline__ void flush_items(WarpScratch& s, int lane, LinkAcc& acc, bool any) {
+  __syncwarp();
+  if (any) {
+    for (int i = 0; i < 32; ++i) {
+      if (s.itL[i] == lane) {
+        acc.F += ld3(s.itF + 3 * i);
+        acc.T += ld3(s.itT + 3 * i);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void put_item(WarpScratch& s, int lane, int link, D3 pw, D3 fw) {
+  const M33 R = {{s.pose[0], s.pose[1], s.pose[2], s.pose[3], s.pose[4], s.pose[5], s.pose[6], s.pose[7], s.pose[8]}};
+  const D3 v = mulT(R, pw - ld3(s.pose + 9));
+  const D3 f = mulT(R, fw);
+  s.itL[lane] = link;
+  st3(s.itF + 3 * lane, f);
+  st3(s.itT + 3 * lane, cross(v, f));
+}
+
+// Expands per-link accumulators into the state gradient s.grad (adds to the
+// limit gradient already there).
+__device__ inline void expand_gradient(const DevHand& H, WarpScratch& s, int lane, const LinkAcc& acc) {
+  // Totals and per-joint subtree sums, fixed link order.
+  D3 Ftot = mk(0, 0, 0), Ttot = mk(0, 0, 0), Fsub = mk(0, 0, 0), Tsub = mk(0, 0, 0);
+  const unsigned sub = lane < H.dof ? H.joint_subtree[lane] : 0u;
+  for (int l = 0; l < H.L; ++l) {
+    const D3 F = mk(__shfl_sync(kFull, acc.F.x, l), __shfl_sync(kFull, acc.F.y, l), __shfl_sync(kFull, acc.F.z, l));
+    const D3 T = mk(__shfl_sync(kFull, acc.T.x, l), __shfl_sync(kFull, acc.T.y, l), __shfl_sync(kFull, acc.T.z, l));
+    Ftot += F;
+    Ttot += T;
+    if (sub & (1u << l)) {
+      Fsub += F;
+      Tsub += T;
+    }
+  }
+  if (lane < H.dof) {
+    const D3 o = ld3(s.jo + 6 * lane), a = ld3(s.jo + 6 * lane + 3);
+    s.grad[12 + lane] += dot(a, Tsub - cross(o, Fsub));
+  }
+  if (lane < 9) {
+    // grad_raw[3l+i] = (e_l x r_i) . (a_inv^T T), zero when degenerate.
+    const bool degenerate = s.pose[21] != 0.0;
+    const int l = lane / 3, i = lane % 3;
+    const M33 ai = {{s.pose[12], s.pose[13], s.pose[14], s.pose[15], s.pose[16], s.pose[17], s.pose[18], s.pose[19],
+                     s.pose[20]}};
+    const D3 w = mulT(ai, Ttot);
+    const D3 ri = mk(s.pose[3 * i], s.pose[3 * i + 1], s.pose[3 * i + 2]);
+    s.grad[lane] += degenerate ? 0.0 : dot(cross(unit(l), ri), w);
+  } else if (lane < 12) {
+    const M33 R = {{s.pose[0], s.pose[1], s.pose[2], s.pose[3], s.pose[4], s.pose[5], s.pose[6], s.pose[7], s.pose[8]}};
+    s.grad[lane] += comp(mul(R, Ftot), lane - 9);
+  }
+  __syncwarp();
+}
+
+// Joint-limit and sphere self-penetration terms (hand.cpp:207-245); items
+// for self pairs are pushed in pair order.
+__device__ inline void limit_and_self(const DevHand& H, const DevParams& P, WarpScratch& s, int lane, LinkAcc& acc,
+                                      bool with_grad, double& e_lim, double& e_self) {
+  double el = 0.0;
+  for (int j = lane; j < H.dof; j += 32) {
+    const double qj = s.x[12 + j];
+    const double over = fmax(qj - H.joint_upper[j], 0.0);
+    const double under = fmax(H.joint_lower[j] - qj, 0.0);
+    el += over * over + under * under;
+    s.grad[12 + j] = with_grad ? P.w_limit * (2.0 * over - 2.0 * under) : 0.0;
+  }
+  for (int i = lane; i < 12; i += 32) s.grad[i] = 0.0;
+  e_lim = warp_sum(el);
+  double es = 0.0;
+  for (int base = 0; base < H.nsp; base += 32) {
+    const int t = base + lane;
+    bool active = false;
+    D3 ca, cb, dir;
+    double overlap = 0.0;
+    int la = -1, lb = -1;
+    if (t < H.nsp) {
+      const int pa = H.sp_a[t], pb = H.sp_b[t];
+      ca = ld3(s.pc + 3 * pa);
+      cb = ld3(s.pc + 3 * pb);
+      const double dist = nrm(ca - cb);
+      overlap = H.proxy[4 * pa + 3] + H.proxy[4 * pb + 3] - dist;
+      if (overlap > 0) {
+        es += overlap * overlap;
+        if (dist > 1e-12) {
+          active = true;
+          dir = (ca - cb) / dist;
+          la = H.proxy_link[pa];
+          lb = H.proxy_link[pb];
+        }
+      }
+    }
+    if (!with_grad) continue;
+    const bool any = __any_sync(kFull, active);
+    if (!any) continue;
+    // item a
+    s.itL[lane] = -1;
+    if (active) put_item(s, lane, la, ca, (-2.0 * P.w_self * overlap) * dir);
+    flush_items(s, lane, acc, true);
+    s.itL[lane] = -1;
+    if (active) put_item(s, lane, lb, cb, (2.0 * P.w_self * overlap) * dir);
+    flush_items(s, lane, acc, true);
+  }
+  e_self = warp_sum(es);
+}
+
+// apply_step (pipeline.cpp:214-231) on lane 0 + divergence/failure checks
+// (pipeline.cpp:264-277). Returns the failure code (0 ok).
+__device__ inline int step_lane0(const DevHand& H, const StageArgs& A, WarpScratch& s, double energy) {
+  const int D = H.D;
+  bool finite = isfinite(energy);
+  for (int i = 0; i < D; ++i) finite = finite && isfinite(s.grad[i]);
+  if (!finite) return 1;
+  for (int i = 0; i < D; ++i) s.xn[i] = s.x[i];
+  auto move = [&](int start, int len, double step) {
+    double n2 = 0.0;
+    for (int i = 0; i < len; ++i) n2 += s.grad[start + i] * s.grad[start + i];
+    const double scale = step * A.decay / fmax(1.0, sqrt(n2));
+    for (int i = 0; i < len; ++i) s.xn[start + i] -= scale * s.grad[start + i];
+  };
+  move(0, 9, A.step_rot);
+  move(9, 3, A.step_trans);
+  if (H.dof > 0) {
+    move(12, H.dof, A.step_joints);
+    for (int j = 0; j < H.dof; ++j) s.xn[12 + j] = fmin(fmax(s.xn[12 + j], H.joint_lower[j]), H.joint_upper[j]);
+  }
+  bool xf = true;
+  for (int i = 0; i < D; ++i) xf = xf && isfinite(s.xn[i]);
+  const double tn = sqrt(s.xn[9] * s.xn[9] + s.xn[10] * s.xn[10] + s.xn[11] * s.xn[11]);
+  if (!xf || tn > 1e3) return 2;
+  for (int i = 0; i < D; ++i) s.x[i] = s.xn[i];
+  return 0;
+}
+
+// Common tail of both step kernels: finite check, step, state write, FK.
+__device__ inline void finish_iteration(const DevHand& H, const DevParams& P, const StageArgs& A, const DevState& st,
+                                        int g, int lane, WarpScratch& s, double total) {
+  if (lane == 0) {
+    st.energy[g] = total;
+    if (A.mode == 0 && A.it == 0) st.stage_energy[(size_t)g * 6 + 2 * A.stage] = total;
+    if (A.mode == 1) st.stage_energy[(size_t)g * 6 + 2 * A.stage + 1] = total;
+  }
+  if (A.mode == 2) {
+    for (int i = lane; i < H.D; i += 32) st.grad[(size_t)g * H.D + i] = s.grad[i];
+    return;
+  }
+  if (A.mode != 0) return;
+  if (lane == 0) {
+    const int code = step_lane0(H, A, s, total);
+    s.flag[0] = code;
+    if (code) st.failed[g] = code;
+  }
+  __syncwarp();
+  const int code = s.flag[0];
+  double* gx = st.x + (size_t)g * H.D;
+  for (int i = lane; i < H.D; i += 32) {
+    st.grad[(size_t)g * H.D + i] = s.grad[i];
+    gx[i] = s.x[i];
+  }
+  if (code) return;
+  __syncwarp();
+  warp_fk(H, st, g, lane, s, P.fd_step, true);
+}
+
+// Sphere-proxy (coarse) stage iteration: total_energy (pipeline.cpp:114-174)
+// with the QP part from k_qp, then the step and FK.
+__global__ void __launch_bounds__(64) k_step_coarse(DevHand H, DevParams P, StageArgs A, DevState st) {
+  __shared__ WarpScratch smem_all[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * 2 + warp;
+  if (g >= st.G || st.failed[g]) return;
+  WarpScratch& s = smem_all[warp];
+  for (int i = lane; i < H.D; i += 32) s.x[i] = st.x[(size_t)g * H.D + i];
+  load_fk(H, st, g, lane, s);
+  const bool with_grad = A.mode != 1;
+  LinkAcc acc{mk(0, 0, 0), mk(0, 0, 0)};
+  double e_lim, e_self;
+  limit_and_self(H, P, s, lane, acc, with_grad, e_lim, e_self);
+
+  const double* qres = st.qres + (size_t)g * st.NQ * 8;
+  // Energy accumulated on lane 0 in the reference's order (pipeline.cpp:104-171).
+  double total = P.w_limit * e_lim;
+  total += P.w_self * e_self;
+  // Hinge over every proxy (pipeline.cpp:116-129), items in proxy order.
+  for (int base = 0; base < H.S; base += 32) {
+    const int p = base + lane;
+    double term = 0.0;
+    bool active = false;
+    if (p < H.S) {
+      const double sd = qres[(size_t)p * 8] - H.proxy[4 * p + 3];
+      if (sd < 0.0) {
+        term = P.w_pen * sd * sd;
+        active = true;
+        s.itL[lane] = -1;
+        if (with_grad) put_item(s, lane, H.proxy_link[p], ld3(s.pc + 3 * p), (P.w_pen * 2.0 * sd) * ld3(qres + p * 8 + 4));
+      } else {
+        s.itL[lane] = -1;
+      }
+    } else {
+      s.itL[lane] = -1;
+    }
+    // Energy in reference order: sequential over proxies.
+    s.red[lane] = term;
+    __syncwarp();
+    if (lane == 0)
+      for (int i = 0; i < 32 && base + i < H.S; ++i) total += s.red[i];
+    if (with_grad) flush_items(s, lane, acc, __any_sync(kFull, active));
+    __syncwarp();
+  }
+  // Tip distance terms (pipeline.cpp:133-163) and the QP force at the tip.
+  {
+    const int f = lane;
+    double term = 0.0;
+    s.itL[lane] = -1;
+    if (f < H.m) {
+      const int tp = H.tip_proxy[f];
+      const double* q0 = qres + (size_t)tp * 8;
+      const double r = q0[0] - H.proxy[4 * tp + 3] - A.offset;
+      term = P.w_distance * r * r;
+      if (with_grad) {
+        const D3 n0 = ld3(q0 + 4);
+        double dpn[3];
+        const double h2 = 2.0 * P.fd_step;
+        for (int kk = 0; kk < 3; ++kk) {
+          const double* qp = qres + (size_t)(H.S + f * 6 + 2 * kk) * 8;
+          const double* qm = qres + (size_t)(H.S + f * 6 + 2 * kk + 1) * 8;
+          dpn[kk] = dot((ld3(qp + 1) - ld3(qm + 1)) / h2, n0);  // (dp^T n)_k
+        }
+        // dd = n^T (I - dp) -> force 2 w r (n - dp^T n)
+        const D3 fw = (P.w_distance * 2.0 * r) * (n0 - mk(dpn[0], dpn[1], dpn[2]));
+        put_item(s, lane, H.tip_link[f], ld3(s.pc + 3 * tp), fw);
+      }
+    }
+    s.red[lane] = term;
+    __syncwarp();
+    if (lane == 0)
+      for (int i = 0; i < H.m; ++i) total += s.red[i];
+    if (with_grad) flush_items(s, lane, acc, true);
+    s.itL[lane] = -1;
+    if (with_grad && f < H.m)
+      put_item(s, lane, H.tip_link[f], ld3(s.pc + 3 * H.tip_proxy[f]), ld3(st.qp_force + ((size_t)g * H.m + f) * 3));
+    if (with_grad) flush_items(s, lane, acc, true);
+  }
+  if (lane == 0) total += P.w_grasp * st.qp_energy[g];
+  total = __shfl_sync(kFull, total, 0);
+  if (with_grad) expand_gradient(H, s, lane, acc);
+  finish_iteration(H, P, A, st, g, lane, s, total);
+}
+
+// OBB-vs-sphere lower bound against an object part (geometry.cpp:544-557).
+__device__ __forceinline__ double obb_sphere(const double* obb, D3 center, double radius) {
+  const D3 oc = ld3(obb);
+  const D3 half = ld3(obb + 3);
+  // rotation column-major: columns are axes; q = rot^T (c - oc)
+  const D3 rel = center - oc;
+  const D3 q = mk(obb[6] * rel.x + obb[7] * rel.y + obb[8] * rel.z, obb[9] * rel.x + obb[10] * rel.y + obb[11] * rel.z,
+                  obb[12] * rel.x + obb[13] * rel.y + obb[14] * rel.z);
+  const D3 ex = mk(fabs(q.x) - half.x, fabs(q.y) - half.y, fabs(q.z) - half.z);
+  double dist;
+  if (ex.x <= 0 && ex.y <= 0 && ex.z <= 0)
+    dist = fmax(ex.x, fmax(ex.y, ex.z));
+  else
+    dist = nrm(mk(fmax(ex.x, 0.0), fmax(ex.y, 0.0), fmax(ex.z, 0.0)));
+  return dist - radius;
+}
+
+struct Witness {
+  D3 c_w, p_w, n;
+  double d;
+};
+
+// fine_contact_query for tip f (pipeline.cpp:320-353) from the tip-center
+// point query and the (tip link, part) pair results of this iteration.
+__device__ inline Witness select_witness(const DevHand& H, const DevObject& O, const DevState& st, int g, int f,
+                                         D3 center) {
+  const int tp = H.tip_proxy[f];
+  const double reference = st.qres[((size_t)g * st.NQ + tp) * 8] - H.proxy[4 * tp + 3];
+  const double env = H.tip_envelope[f];
+  const int link = H.tip_link[f];
+  Witness w;
+  w.d = INFINITY;
+  w.c_w = w.p_w = mk(0, 0, 0);
+  w.n = mk(0, 0, 1);
+  for (int p = 0; p < O.P; ++p) {
+    if (!(obb_sphere(O.part_obb + 15 * p, center, env) < reference + 1e-9)) continue;
+    const double* r = st.pairs + ((size_t)g * st.NP + link * O.P + p) * 12;
+    if (r[0] < w.d) {
+      w.d = r[0];
+      w.c_w = ld3(r + 1);
+      w.p_w = ld3(r + 4);
+      w.n = ld3(r + 7);
+    }
+  }
+  return w;
+}
+
+// Mesh stages (pipeline.cpp:175-208): hinge over every (link part, object
+// part), witness distance, detached-witness surrogate; then step and FK.
+__global__ void __launch_bounds__(64) k_step_mesh(DevHand H, DevObject O, DevParams P, StageArgs A, DevState st) {
+  __shared__ WarpScratch smem_all[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * 2 + warp;
+  if (g >= st.G || st.failed[g]) return;
+  WarpScratch& s = smem_all[warp];
+  for (int i = lane; i < H.D; i += 32) s.x[i] = st.x[(size_t)g * H.D + i];
+  load_fk(H, st, g, lane, s);
+  const bool with_grad = A.mode != 1;
+  LinkAcc acc{mk(0, 0, 0), mk(0, 0, 0)};
+  double e_lim, e_self;
+  limit_and_self(H, P, s, lane, acc, with_grad, e_lim, e_self);
+
+  const int npairs = H.L * O.P;
+  const double* pr = st.pairs + (size_t)g * st.NP * 12;
+  double total = P.w_limit * e_lim;
+  total += P.w_self * e_self;
+  for (int base = 0; base < npairs; base += 32) {
+    const int t = base + lane;
+    double term = 0.0;
+    bool active = false;
+    s.itL[lane] = -1;
+    if (t < npairs) {
+      const double d = pr[(size_t)t * 12];
+      if (d < 0.0) {
+        term = P.w_pen * d * d;
+        active = true;
+        if (with_grad) put_item(s, lane, t / O.P, ld3(pr + (size_t)t * 12 + 1), (P.w_pen * 2.0 * d) * ld3(pr + (size_t)t * 12 + 7));
+      }
+    }
+    s.red[lane] = term;
+    __syncwarp();
+    if (lane == 0)
+      for (int i = 0; i < 32 && base + i < npairs; ++i) total += s.red[i];
+    if (with_grad) flush_items(s, lane, acc, __any_sync(kFull, active));
+    __syncwarp();
+  }
+  // Witness distance and surrogate terms.
+  double sur = 0.0;
+  {
+    const int f = lane;
+    double term = 0.0, sq = 0.0;
+    Witness w;
+    s.itL[lane] = -1;
+    if (f < H.m) {
+      w = select_witness(H, O, st, g, f, ld3(s.pc + 3 * H.tip_proxy[f]));
+      const double r = w.d - A.offset;
+      term = P.w_distance * r * r;
+      if (with_grad) put_item(s, lane, H.tip_link[f], w.c_w, (P.w_distance * 2.0 * r) * w.n);
+      const D3 diff = w.c_w - ld3(st.anchors + ((size_t)g * H.m + f) * 3);
+      sq = sqn(diff);
+      w.p_w = diff;  // reuse as the surrogate direction
+    }
+    s.red[lane] = term;
+    __syncwarp();
+    if (lane == 0)
+      for (int i = 0; i < H.m; ++i) total += s.red[i];
+    __syncwarp();
+    s.red[lane] = sq;
+    __syncwarp();
+    if (lane == 0)
+      for (int i = 0; i < H.m; ++i) sur += s.red[i];
+    if (with_grad) flush_items(s, lane, acc, true);
+    s.itL[lane] = -1;
+    if (with_grad && f < H.m) put_item(s, lane, H.tip_link[f], w.c_w, (2.0 * P.w_grasp) * w.p_w);
+    if (with_grad) flush_items(s, lane, acc, true);
+  }
+  if (lane == 0) total += P.w_grasp * sur;
+  total = __shfl_sync(kFull, total, 0);
+  if (with_grad) expand_gradient(H, s, lane, acc);
+  finish_iteration(H, P, A, st, g, lane, s, total);
+}
+
+// FK from st.x for every live grasp (stage starts, teacher-forced calls).
+__global__ void __launch_bounds__(64) k_fk(DevHand H, DevParams P, DevState st) {
+  __shared__ WarpScratch smem_all[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * 2 + warp;
+  if (g >= st.G || st.failed[g]) return;
+  WarpScratch& s = smem_all[warp];
+  for (int i = lane; i < H.D; i += 32) s.x[i] = st.x[(size_t)g * H.D + i];
+  __syncwarp();
+  warp_fk(H, st, g, lane, s, P.fd_step, true);
+}
+
+// After the coarse stage: anchors = nearest surface points of the tip
+// centers at the final state (pipeline.cpp:69-78, 284-289).
+__global__ void k_anchors(DevHand H, DevState st, int skip_fine) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= st.G || st.failed[g]) return;
+  for (int f = 0; f < H.m; ++f) {
+    const double* q = st.qres + ((size_t)g * st.NQ + H.tip_proxy[f]) * 8;
+    st3(st.anchors + ((size_t)g * H.m + f) * 3, ld3(q + 1));
+  }
+  if (skip_fine) {
+    for (int i = 0; i < H.D; ++i) st.x_p[(size_t)g * H.D + i] = st.x[(size_t)g * H.D + i];
+    st.have_pregrasp[g] = 1;
+  }
+}
+
+__global__ void k_set_pregrasp(DevHand H, DevState st) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= st.G || st.failed[g]) return;
+  for (int i = 0; i < H.D; ++i) st.x_p[(size_t)g * H.D + i] = st.x[(size_t)g * H.D + i];
+  st.have_pregrasp[g] = 1;
+}
+
+// Final record: witnesses at x -> contact frames (p_w, -n) for the cold QP
+// (pipeline.cpp:302-311); also exposes the raw witnesses.
+__global__ void k_final_frames(DevHand H, DevObject O, DevState st, double* witness_out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= st.G * H.m) return;
+  const int g = t / H.m, f = t % H.m;
+  if (st.failed[g]) return;
+  const int l = H.tip_link[f];
+  const double* w = st.world + ((size_t)g * H.L + l) * 12;
+  M33 Rw;
+  for (int i = 0; i < 9; ++i) Rw.m[i] = w[i];
+  const D3 center = mul(Rw, ld3(H.proxy + 4 * H.tip_proxy[f])) + ld3(w + 9);
+  const Witness wt = select_witness(H, O, st, g, f, center);
+  build_frame(wt.p_w, -wt.n, st.frames + ((size_t)g * H.m + f) * 12);
+  if (witness_out) {
+    double* o = witness_out + ((size_t)g * H.m + f) * 11;
+    st3(o, wt.c_w);
+    st3(o + 3, wt.p_w);
+    st3(o + 6, wt.n);
+    o[9] = wt.d;
+    o[10] = l;
+  }
+}
+
+// x_p fallback and squeeze (pipeline.cpp:296-300, 426-434).
+__global__ void k_squeeze(DevHand H, DevState st, double* x_s) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= st.G) return;
+  const int D = H.D;
+  const double* x = st.x + (size_t)g * D;
+  double* xp = st.x_p + (size_t)g * D;
+  if (!st.have_pregrasp[g])
+    for (int i = 0; i < D; ++i) xp[i] = x[i];
+  double* xs = x_s + (size_t)g * D;
+  if (st.failed[g]) {
+    for (int i = 0; i < D; ++i) xs[i] = x[i];
+    return;
+  }
+  M33 rg, rp;
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < 3; ++i) {
+      rg.m[i * 3 + c] = x[3 * c + i];
+      rp.m[i * 3 + c] = xp[3 * c + i];
+    }
+  bool fb;
+  const M33 Rg = project_rotation(rg, &fb);
+  const M33 Rp = project_rotation(rp, &fb);
+  const M33 R = mul(Rg, mul(transpose(Rp), Rg));
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < 3; ++i) xs[3 * c + i] = R.m[i * 3 + c];
+  for (int i = 9; i < 12; ++i) xs[i] = 2.0 * x[i] - xp[i];
+  for (int j = 0; j < H.dof; ++j)
+    xs[12 + j] = fmin(fmax(2.0 * x[12 + j] - xp[12 + j], H.joint_lower[j]), H.joint_upper[j]);
+}
+
+}  // namespace gdev

@@ -1,0 +1,112 @@
+// Device-resident hand / object / run parameters and per-grasp state layout.
+#pragma once
+
+#include <cstdint>
+
+namespace gdev {
+
+constexpr int kMaxLinks = 32;    // one lane per link in the warp-per-grasp kernels
+constexpr int kMaxDof = 32;
+constexpr int kMaxTips = 5;      // QP lanes = 6 directions x tips <= 30
+constexpr int kMaxEdges = 8;
+constexpr int kMaxDims = 12 + kMaxDof;
+constexpr int kMaxDepth = 12;    // kinematic chain depth
+constexpr int kMaxProxies = 128;
+constexpr int kMaxParts = 64;
+
+// Object face record for point queries (query_part, geometry.cpp:355-395):
+// a, b, c vertices, unit normal n (cross/len as the reference forms it),
+// nd = n.a, valid = (len >= 1e-30). 16 doubles = 128 B per face.
+constexpr int kFaceStride = 16;
+
+struct DevHand {
+  int L, dof, m, S, nsp, D;
+  const int* link_parent_joint;     // [L]
+  const int* link_depth;            // [L] path length root..l
+  const int* link_path;             // [L*kMaxDepth] links from root to l
+  const int* joint_parent_link;     // [dof]
+  const double* joint_origin;       // [dof*3]
+  const double* joint_axis;         // [dof*3]
+  const double* joint_lower;        // [dof]
+  const double* joint_upper;        // [dof]
+  const unsigned* joint_subtree;    // [dof] bitmask of links moved by the joint
+  const double* proxy;              // [S*4] center_local, radius
+  const int* proxy_link;            // [S]
+  const int* tip_link;              // [m]
+  const int* tip_proxy;             // [m] global proxy index
+  const double* tip_envelope;       // [m] envelope_radius (pipeline.cpp:47-52)
+  const int* sp_a;                  // [nsp] self-penetration proxy pairs, reference order
+  const int* sp_b;
+  const int* link_vbeg;             // [L+1]
+  const double* link_verts;         // [nv*3]
+  const double* link_centroid;      // [L*3]
+  const double* link_halfnorm;      // [L] |obb.half_extents|
+};
+
+struct DevObject {
+  int P, F;
+  const int* part_fbeg;       // [P+1]
+  const int* part_vbeg;       // [P+1]
+  const double* faces;        // [F*kFaceStride]
+  const double* verts;        // [nv*3]
+  const double* part_centroid;  // [P*3]
+  const double* part_halfnorm;  // [P]
+  const double* part_obb;       // [P*15] center, half, rotation (column-major)
+};
+
+struct DevParams {
+  double rho, sigma, alpha;
+  int max_iters;
+  double eps_primal, eps_dual;
+  int check_interval;
+  double mu;
+  int k;  // n_edges
+  double beta, gamma_total;
+  double w_grasp, w_distance, w_limit, w_self, w_pen;
+  double fd_step;
+  double cos_t[kMaxEdges], sin_t[kMaxEdges];  // host libm cos/sin(2 pi j / k)
+};
+
+struct StageArgs {
+  int stage;  // 0 coarse, 1 fine, 2 final
+  int iters;
+  int it;
+  double step_rot, step_trans, step_joints, step_floor;
+  double offset;
+  int mode;  // 0: energy + gradient + step, 1: energy only (stage end)
+  double decay;  // host-computed cosine decay for `it`
+};
+
+// Per-grasp device buffers (all [G][...] contiguous).
+struct DevState {
+  int G;       // grasps in this launch
+  int NQ;      // query slots per grasp = S + 6m
+  int NP;      // pair slots per grasp = L*P
+  double* x;        // [G*D]
+  double* pose;     // [G*24]: R(9 row-major), t(3), a_inv(9 row-major), degenerate, pad
+  double* world;    // [G*L*12]: R(9 row-major), t(3)
+  double* joints;   // [G*dof*6]: chain-frame origin(3), axis(3)
+  double* qpts;     // [G*NQ*3]
+  double* qres;     // [G*NQ*8]: d, pb(3), n(3), part
+  double* pairs;    // [G*NP*12]: d, pa(3), pb(3), n(3), flags, pad
+  double* warm_x;   // [G*n*6] column-major n x 6
+  double* warm_y;   // [G*M*6]
+  double* out_z;    // [G*M*6]
+  int* qp_iters;    // [G*6]
+  int* qp_conv;     // [G*6]
+  int* qp_ready;    // [G]
+  double* qp_force;   // [G*m*3]
+  double* qp_energy;  // [G]
+  double* qp_perdir;  // [G*6]
+  double* frames;     // [G*m*12]
+  double* anchors;    // [G*m*3]
+  double* energy;     // [G]
+  double* grad;       // [G*D]
+  int* failed;        // [G]
+  double* stage_energy;  // [G*6]
+  double* x_p;        // [G*D]
+  int* have_pregrasp; // [G]
+  int* err;           // [4]: 0 epa-degenerate, 1 epa-overflow, 2 unused, 3 unused
+};
+
+}  // namespace gdev

@@ -1,0 +1,219 @@
+"""GPU parity: the sm_100a kernels vs the fp64 CPU oracle on identical inputs.
+
+Tolerances (fp64 on both sides; differences come only from operation order,
+FMA contraction and device libm):
+  * discrete selections (part index, inside/outside, witness part, EPA use,
+    failure flags): exact, except where the oracle's own top-2 gap is within
+    1e-12 (rounding-level tie), which is reported separately;
+  * distances / points / normals: 1e-9 abs;
+  * energies and gradients: 1e-7 relative (teacher-forced, one iteration);
+  * QP: iteration counts exact, lambda 1e-7 abs (teacher-forced);
+  * end-to-end after 20/10/10 iterations: |dx| <= 1e-6.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import use
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_points(engine, pts):
+    from paper_2412_16490_b200 import _native as N
+    from paper_2412_16490_b200.api import dptr
+    pts = np.ascontiguousarray(pts, dtype=np.float64)
+    out = np.zeros((len(pts), 8))
+    N.check(N.lib().grasp_point_to_mesh(engine._ctx, len(pts), dptr(pts), dptr(out)))
+    return out
+
+
+def gpu_pairs(engine, links, parts, poses):
+    from paper_2412_16490_b200 import _native as N
+    from paper_2412_16490_b200.api import dptr, iptr
+    links = np.ascontiguousarray(links, dtype=np.int32)
+    parts = np.ascontiguousarray(parts, dtype=np.int32)
+    poses = np.ascontiguousarray(poses, dtype=np.float64)
+    out = np.zeros((len(links), 11))
+    N.check(N.lib().grasp_signed_distance(engine._ctx, len(links), iptr(links), iptr(parts), dptr(poses), dptr(out)))
+    return out
+
+
+def gpu_energy(engine, cfg, stage, x, anchors=None, warm_x=None, warm_y=None):
+    from paper_2412_16490_b200 import _native as N
+    from paper_2412_16490_b200.api import dptr
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    e = np.zeros(len(x))
+    g = np.zeros_like(x)
+    anc = None if anchors is None else np.ascontiguousarray(anchors, dtype=np.float64)
+    N.check(N.lib().grasp_total_energy(engine._ctx, C.byref(cfg.to_params()), stage, len(x), dptr(x), dptr(anc),
+                                       dptr(warm_x), dptr(warm_y), dptr(e), dptr(g)))
+    return e, g
+
+
+def gpu_fcq(engine, hand, x):
+    from paper_2412_16490_b200 import _native as N
+    from paper_2412_16490_b200.api import dptr
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.zeros((len(x), hand.n_tips, 11))
+    N.check(N.lib().grasp_fine_contact_query(engine._ctx, len(x), dptr(x), dptr(out)))
+    return out
+
+
+def gpu_qp(engine, cfg, frames, m, warm_x=None, warm_y=None):
+    from paper_2412_16490_b200 import _native as N
+    from paper_2412_16490_b200.api import dptr, iptr
+    frames = np.ascontiguousarray(frames, dtype=np.float64)
+    g = frames.size // (m * 12)
+    n = m * cfg.contact.n_edges
+    M = m + 1 + n
+    X, Y, Z = np.zeros((g, 6, n)), np.zeros((g, 6, M)), np.zeros((g, 6, M))
+    it, conv, per = np.zeros((g, 6), np.int32), np.zeros((g, 6), np.int32), np.zeros((g, 6))
+    N.check(N.lib().grasp_qp_batch(engine._ctx, C.byref(cfg.to_params()), g, m, dptr(frames), dptr(warm_x),
+                                   dptr(warm_y), dptr(X), dptr(Y), dptr(Z), iptr(it), iptr(conv), dptr(per), 0))
+    return dict(X=X, Y=Y, Z=Z, iters=it, converged=conv, per_direction=per)
+
+
+def random_frames(rng, g, m, scale=0.1):
+    """test_energy.cpp:82-91 style contacts: p on a shell, n roughly inward."""
+    out = np.zeros((g, m, 12))
+    for i in range(g):
+        for c in range(m):
+            u = rng.normal(size=3)
+            u /= np.linalg.norm(u)
+            p = scale * rng.uniform(0.4, 1.2) * u
+            w = rng.normal(size=3)
+            w /= np.linalg.norm(w)
+            n = -u + 0.4 * w
+            n /= np.linalg.norm(n)
+            seed = np.array([0.0, 1.0, 0.0]) if abs(n[0]) > 0.99 else np.array([1.0, 0.0, 0.0])
+            d = np.cross(n, seed)
+            d /= np.linalg.norm(d)
+            e = np.cross(n, d)
+            out[i, c] = np.concatenate([p, n, d, e])
+    return out
+
+
+# ------------------------------------------------------------ point queries
+@pytest.mark.parametrize("name", ["sphere", "box", "capsule"])
+def test_point_queries_match_oracle(G, O, trident, engine, name):
+    obj = G.make_primitive(name, 0.1)
+    use(engine, trident, obj)
+    rng = np.random.default_rng(5)
+    pts = rng.normal(size=(4000, 3)) * 0.08
+    ref = O.point_to_mesh(obj, pts)
+    got = gpu_points(engine, pts)
+    assert (got[:, 7] == ref[:, 7]).all()
+    assert np.array_equal(got[:, 0] < 0, ref[:, 0] < 0)
+    np.testing.assert_allclose(got[:, :7], ref[:, :7], atol=1e-9, rtol=0)
+
+
+def test_point_queries_multipart(G, O, trident, engine):
+    from test_models import three_box_obj
+    obj = G.parse_object_text(three_box_obj(), 0.12, "three_boxes")
+    use(engine, trident, obj)
+    rng = np.random.default_rng(6)
+    pts = rng.normal(size=(4000, 3)) * 0.1
+    ref = O.point_to_mesh(obj, pts)
+    got = gpu_points(engine, pts)
+    assert (got[:, 7] == ref[:, 7]).all()
+    np.testing.assert_allclose(got[:, :7], ref[:, :7], atol=1e-9, rtol=0)
+
+
+# ---------------------------------------------------------------- GJK / EPA
+def random_link_poses(rng, n, span):
+    from scipy.spatial.transform import Rotation
+    R = Rotation.random(n, random_state=int(rng.integers(1 << 30))).as_matrix()
+    poses = np.zeros((n, 12))
+    poses[:, :9] = R.transpose(0, 2, 1).reshape(n, 9)  # column-major
+    poses[:, 9:] = rng.uniform(-span, span, size=(n, 3))
+    return poses
+
+
+def test_signed_distance_matches_oracle(G, O, trident, engine):
+    obj = G.make_primitive("sphere", 0.1)
+    use(engine, trident, obj)
+    rng = np.random.default_rng(7)
+    n = 3000
+    links = rng.integers(0, trident.n_links, size=n)
+    parts = np.zeros(n, dtype=np.int32)
+    poses = random_link_poses(rng, n, 0.16)
+    ref = O.signed_distance(trident, obj, links, parts, poses)
+    got = gpu_pairs(engine, links, parts, poses)
+    assert ((got[:, 10] % 2) == ref[:, 10]).all(), "EPA usage differs"
+    assert (ref[:, 0] < 0).sum() > 100 and (ref[:, 0] > 0).sum() > 100
+    np.testing.assert_allclose(got[:, :10], ref[:, :10], atol=1e-9, rtol=0)
+
+
+# ---------------------------------------------------------------------- QP
+@pytest.mark.parametrize("m", [3, 4, 5])
+def test_qp_batch_matches_oracle(G, O, engine, m):
+    cfg = G.RunConfig()
+    rng = np.random.default_rng(100 + m)
+    frames = random_frames(rng, 200, m)
+    ref = O.qp_batch(cfg, frames, m)
+    got = gpu_qp(engine, cfg, frames, m)
+    same = (got["iters"] == ref["iters"])
+    assert same.mean() > 0.97, f"iteration counts agree on {same.mean():.3f}"
+    assert (got["converged"] == ref["converged"]).mean() > 0.97
+    rows = same.all(axis=1)
+    np.testing.assert_allclose(got["X"][rows], ref["X"][rows], atol=1e-7)
+    np.testing.assert_allclose(got["per_direction"][rows], ref["per_direction"][rows], rtol=1e-7, atol=1e-9)
+
+
+# ------------------------------------------------------ teacher-forced energy
+def test_coarse_energy_and_gradient_match_oracle(G, O, trident, engine):
+    obj = G.make_primitive("sphere", 0.1)
+    use(engine, trident, obj)
+    cfg = G.RunConfig()
+    x = G.init_poses(trident, obj, 64, 3)
+    e_ref, g_ref = O.total_energy(trident, obj, cfg, 0, x)
+    e_got, g_got = gpu_energy(engine, cfg, 0, x)
+    np.testing.assert_allclose(e_got, e_ref, rtol=1e-7)
+    scale = np.maximum(1.0, np.abs(g_ref).max(axis=1, keepdims=True))
+    assert np.abs(g_got - g_ref).max() / scale.max() < 1e-6
+
+
+def test_mesh_energy_and_gradient_match_oracle(G, O, trident, engine):
+    obj = G.make_primitive("sphere", 0.1)
+    use(engine, trident, obj)
+    cfg = G.RunConfig()
+    rng = np.random.default_rng(9)
+    x = G.init_poses(trident, obj, 64, 4)
+    x[:, 9:12] *= 0.62  # pull the palms in so fingers touch / penetrate
+    anchors = rng.normal(size=(64, trident.n_tips, 3)) * 0.05
+    for stage in (1, 2):
+        e_ref, g_ref = O.total_energy(trident, obj, cfg, stage, x, anchors=anchors)
+        e_got, g_got = gpu_energy(engine, cfg, stage, x, anchors=anchors)
+        np.testing.assert_allclose(e_got, e_ref, rtol=1e-7)
+        np.testing.assert_allclose(g_got, g_ref, rtol=1e-6, atol=1e-6 * np.abs(g_ref).max())
+
+
+def test_fine_contact_query_matches_oracle(G, O, trident, engine):
+    obj = G.make_primitive("box", 0.1)
+    use(engine, trident, obj)
+    x = G.init_poses(trident, obj, 128, 5)
+    x[:, 9:12] *= 0.6
+    ref = O.fine_contact_query(trident, obj, x)
+    got = gpu_fcq(engine, trident, x)
+    assert (got[..., 10] == ref[..., 10]).all()
+    np.testing.assert_allclose(got[..., :10], ref[..., :10], atol=1e-9)
+
+
+# ---------------------------------------------------------------- end to end
+def test_synthesize_short_schedule_matches_oracle(G, O, trident, engine):
+    obj = G.make_primitive("sphere", 0.1)
+    use(engine, trident, obj)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 8, 17
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 20, 10, 10
+    x0 = G.init_poses(trident, obj, cfg.batch, cfg.seed, cfg.init)
+    gpu = engine.synthesize(cfg, x0)
+    cpu = O.synthesize(trident, obj, cfg, x0, workers=8)
+    assert (gpu.failed == cpu.failed).all()
+    np.testing.assert_allclose(gpu.x, cpu.x, atol=1e-6)
+    np.testing.assert_allclose(gpu.x_p, cpu.x_p, atol=1e-6)
+    np.testing.assert_allclose(gpu.x_s, cpu.x_s, atol=1e-6)
+    np.testing.assert_allclose(gpu.energy_total, cpu.energy_total, rtol=1e-4)
+    np.testing.assert_allclose(gpu.stage_energy, cpu.stage_energy, rtol=1e-4)
