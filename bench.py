@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark: batched bilevel grasp synthesis on B200 (BASELINE.json metric
+"grasps/sec (Shadow, 1/2/4/8 B200) vs CPU ref").
+
+One step = one full synthesize() over this rank's batch: the reference's
+three-stage schedule (300 coarse / 100 fine / 100 final iterations), the
+final cold-QP record and the squeeze pose, for every grasp. Workload =
+BASELINE config 2 (Shadow-like hand, one multi-part convex mesh, 4096 grasps
+per GPU); with torchrun each rank takes a contiguous shard of one global
+init_poses stream (weak scaling: 4096 grasps per GPU, 32768 on 8 GPUs =
+config 4). There is no per-iteration collective; results are gathered to
+rank 0 once at the end (inside the e2e region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HAND = ROOT / "paper_2412_16490_b200" / "assets" / "hands" / "shadow_like.json"
+OBJECT = ROOT / "paper_2412_16490_b200" / "assets" / "objects" / "drill_like.obj"
+SCALE = 0.10
+SEED = 17
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--batch", type=int, default=4096, help="grasps per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-json", default="", help="also dump the per-kernel profile here")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(G, batch_per_gpu, n_gpus):
+    hand = G.HandModel.from_file(HAND)
+    obj = G.load_object(OBJECT, SCALE)
+    cfg = G.RunConfig()
+    cfg.seed = SEED
+    cfg.batch = batch_per_gpu * n_gpus
+    return hand, obj, cfg
+
+
+def config_dict(hand, obj, cfg, batch_per_gpu, n_gpus):
+    return {
+        "workload": "BASELINE config 2 (config 4 at 8 GPUs): shadow_like hand (22 DoF, 5 tips, 23 links) grasping "
+                    "drill_like 6-part convex mesh (%d faces) at scale %.2f; full 300/100/100 schedule + final "
+                    "record per grasp" % (len(obj.faces), SCALE),
+        "hand": "assets/hands/shadow_like.json",
+        "object": "assets/objects/drill_like.obj",
+        "batch_per_gpu": batch_per_gpu,
+        "global_batch": batch_per_gpu * n_gpus,
+        "iters": [cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters],
+        "seed": SEED,
+        "l2": "flushed between timed steps (512 MiB device write); per-step working set ~40 MB",
+        "parallelism": "dp%d: contiguous grasp shards, no per-iteration collective, one final gather" % n_gpus,
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._thread = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.QUERY,
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([c.strip() for c in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._thread = threading.Thread(target=run, daemon=True)
+        self._thread.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._thread:
+            self._thread.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def roofline(prof, hand, cfg, peak_tflops):
+    """Dominant kernel class by device time; achieved = algorithmic flops
+    (SURVEY.md 8(d) constants x op counters of this run) / its time."""
+    ms = prof["ms"]
+    dom = max(ms, key=ms.get)
+    ops = prof["ops"]
+    m = hand.n_tips
+    n = m * cfg.contact.n_edges
+    M = m + 1 + n
+    flops = {
+        "point_query": 7.0 * ops["plane_tests"] + 64.0 * ops["triangle_tests"],
+        "qp": (45.0 * n + 6.0 * M + 100.0 + 3.0 * n) * ops["qp_column_sweeps"] + (80.0 * n + 400.0) * ops["qp_solves"],
+        "pairs": 6.0 * ops["support_verts"] + 200.0 * ops["gjk_iters"] + 200.0 * ops["epa_iters"],
+    }
+    f = flops.get(dom)
+    total_ms = sum(ms.values())
+    if f is None or ms[dom] <= 0:
+        return dom, None
+    achieved = f / (ms[dom] * 1e-3) / 1e12
+    return dom, {
+        "bound": "fp64",
+        "kernel": dom,
+        "achieved": round(achieved, 3),
+        "peak": round(peak_tflops, 3),
+        "unit": "TFLOP/s",
+        "frac": round(achieved / peak_tflops, 4),
+        "traffic": None,
+        "share_of_step": round(ms[dom] / total_ms, 3),
+        "peak_source": "measured fp64 FMA micro-benchmark on this GPU (MEASURED_PEAKS.json has no fp64 entry)",
+        "flop_model": "SURVEY 8(d): plane test 7, closest-on-triangle 64, ADMM column-sweep 45n+6M+100+3n, "
+                      "QP setup 80n+400, support vertex 6, GJK/EPA iteration 200",
+        "kernel_ms": {k: round(v, 2) for k, v in ms.items()},
+        "ops": ops,
+    }
+
+
+def cpu_baseline(G, hand, obj, cfg, threads, n_grasps):
+    from oracle import oracle as O
+    x0 = G.init_poses(hand, obj, n_grasps, SEED)
+    t0 = time.perf_counter()
+    O.synthesize(hand, obj, cfg, x0, workers=threads)
+    dt = time.perf_counter() - t0
+    return {"value": round(n_grasps / dt, 4), "unit": "grasps/s", "cores": threads, "kind": "port",
+            "sample": "%d grasps (full schedule) of the same workload on %d host threads, %.1f s" % (
+                n_grasps, threads, dt)}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU implementation (the
+    fp64 oracle port; the C++ reference needs Eigen3 and does not build
+    here), all host threads, bounded sample per step. Rank 0 only."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import paper_2412_16490_b200 as G
+    hand, obj, cfg = workload(G, args.batch, args.gpus)
+    threads = os.cpu_count() or 1
+    per_step = threads
+    from oracle import oracle as O
+    x0 = G.init_poses(hand, obj, per_step, SEED)
+    for _ in range(args.warmup):
+        O.synthesize(hand, obj, cfg, x0[: max(1, threads // 4)], workers=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.synthesize(hand, obj, cfg, x0, workers=threads)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(times)
+    value = per_step / (ms * 1e-3)
+    line = {
+        "metric": "grasps/sec", "value": round(value, 4), "unit": "grasps/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (init_poses seed 17)",
+        "impl": "reference",
+        "config": config_dict(hand, obj, cfg, args.batch, args.gpus),
+        "cpu_baseline": {"value": round(value, 4), "unit": "grasps/s", "cores": threads, "kind": "port",
+                         "sample": "%d grasps per step (one per host thread), full schedule" % per_step},
+        "e2e": {"value": round(value, 4), "unit": "grasps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2412_16490_b200 as G
+    from paper_2412_16490_b200 import _native as N
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world if world > 1 else args.gpus
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    hand, obj, cfg = workload(G, args.batch, world)
+    B, D, m = args.batch, hand.dims(), hand.n_tips
+    n = m * cfg.contact.n_edges
+
+    # One global init_poses stream; this rank's contiguous shard.
+    x0_all = G.init_poses(hand, obj, B * world, SEED, cfg.init)
+    x0_host = np.ascontiguousarray(x0_all[rank * B:(rank + 1) * B])
+    import dataclasses
+    shard_cfg = dataclasses.replace(cfg, batch=B)
+
+    eng = G.Engine(local)
+    eng.set_hand(hand)
+    eng.set_object(obj)
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)
+
+    x0 = torch.from_numpy(x0_host).to(dev)
+    outs = {
+        "x_p": torch.empty(B, D, dtype=torch.float64, device=dev),
+        "x": torch.empty(B, D, dtype=torch.float64, device=dev),
+        "x_s": torch.empty(B, D, dtype=torch.float64, device=dev),
+        "energy_total": torch.empty(B, dtype=torch.float64, device=dev),
+        "per_direction": torch.empty(B, 6, dtype=torch.float64, device=dev),
+        "contact_forces": torch.empty(B, 6 * n, dtype=torch.float64, device=dev),
+        "contacts": torch.empty(B, m * 12, dtype=torch.float64, device=dev),
+        "stage_energy": torch.empty(B, 6, dtype=torch.float64, device=dev),
+        "failed": torch.empty(B, dtype=torch.int32, device=dev),
+        "qp_converged": torch.empty(B, 6, dtype=torch.int32, device=dev),
+    }
+    ptrs = {k: v.data_ptr() for k, v in outs.items()}
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        eng.synthesize_device(shard_cfg, x0.data_ptr(), B, ptrs)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # ---- device-resident timed region (value)
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = eng.launch_count()
+    ev = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        ev.append((a, b))
+    barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    launches = eng.launch_count() - launches0
+    clk = clocks.stop()
+    ms = statistics.mean(step_ms)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = B * world / (ms_max * 1e-3)
+
+    # ---- end-to-end through the C ABI with host buffers (value e2e)
+    host_out = G.SynthesisOutput(B, D, m, cfg.contact.n_edges)
+    gather = [torch.empty(B, D, dtype=torch.float64, device=dev) for _ in range(world)] if world > 1 else None
+    e2e_times = []
+    for _ in range(max(1, args.steps)):
+        barrier()
+        t0 = time.perf_counter()
+        x0_e2e = G.init_poses(hand, obj, B * world, SEED, cfg.init)[rank * B:(rank + 1) * B]
+        s = host_out.as_struct()
+        import ctypes as C
+        N.check(N.lib().grasp_synthesize(eng._ctx, C.byref(shard_cfg.to_params()), B,
+                                         np.ascontiguousarray(x0_e2e).ctypes.data_as(C.POINTER(C.c_double)),
+                                         C.byref(s)))
+        if world > 1:
+            dist.all_gather(gather, torch.from_numpy(host_out.x).to(dev))
+            torch.cuda.synchronize(dev)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_t = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = B * world / float(e2e_t.item())
+    h2d = B * D * 8
+    d2h = sum(a.nbytes for a in (host_out.x_p, host_out.x, host_out.x_s, host_out.energy_total,
+                                 host_out.per_direction, host_out.contact_forces, host_out.contacts,
+                                 host_out.stage_energy, host_out.failed, host_out.qp_converged))
+
+    # ---- profiling pass (not timed): per-kernel share + roofline
+    rl = None
+    prof = None
+    if rank == 0:
+        peak = C_double_fp64_peak(N, local)
+        eng.set_profiling(True)
+        step()
+        torch.cuda.synchronize(dev)
+        prof = eng.profile()
+        eng.set_profiling(False)
+        _, rl = roofline(prof, hand, shard_cfg, peak)
+        if args.profile_json:
+            Path(args.profile_json).write_text(json.dumps({"profile": prof, "fp64_peak_tflops": peak,
+                                                            "step_ms": step_ms}, indent=1))
+
+    if rank == 0:
+        failed = int((outs["failed"] != 0).sum().item())
+        line = {
+            "metric": "grasps/sec", "value": round(value, 3), "unit": "grasps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: init_poses(seed 17) start states, generated hand/object assets",
+            "config": config_dict(hand, obj, cfg, B, world),
+            "e2e": {"value": round(e2e_value, 3), "unit": "grasps/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "path": "init_poses + grasp_synthesize (C ABI, host buffers)" + (
+                        " + NCCL all_gather of x to every rank" if world > 1 else "")},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "failed_grasps": failed,
+        }
+        if rl:
+            line["roofline"] = rl
+        if world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            line["cpu_baseline"] = cpu_baseline(G, hand, obj, cfg, threads, threads)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def C_double_fp64_peak(N, device):
+    import ctypes as C
+    v = C.c_double()
+    N.check(N.lib().grasp_measure_fp64_peak(device, C.byref(v)))
+    return v.value
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -445,6 +445,37 @@ class Engine:
         N.check(N.lib().grasp_synthesize(self._ctx, C.byref(cfg.to_params()), batch, dptr(x0), C.byref(s)))
         return out
 
+    def synthesize_device(self, cfg: RunConfig, x0_ptr: int, batch: int, out_ptrs: dict) -> None:
+        """grasp_synthesize_device: x0 and outputs are device pointers (ints)."""
+        vp = lambda k: C.cast(C.c_void_p(out_ptrs[k]), _dp) if out_ptrs.get(k) else None
+        ip = lambda k: C.cast(C.c_void_p(out_ptrs[k]), _ip) if out_ptrs.get(k) else None
+        s = N.Out(vp("x_p"), vp("x"), vp("x_s"), vp("energy_total"), vp("per_direction"), vp("contact_forces"),
+                  vp("contacts"), vp("stage_energy"), ip("failed"), ip("qp_converged"))
+        N.check(N.lib().grasp_synthesize_device(self._ctx, C.byref(cfg.to_params()), int(batch),
+                                                C.cast(C.c_void_p(x0_ptr), _dp), C.byref(s)))
+
+    def stream_handle(self) -> int:
+        return N.lib().grasp_ctx_stream(self._ctx) or 0
+
+    def set_profiling(self, on: bool) -> None:
+        N.check(N.lib().grasp_ctx_set_profiling(self._ctx, int(bool(on))))
+
+    KERNEL_CLASSES = ("point_query", "qp", "step_coarse", "pairs", "step_mesh", "fk", "finalize")
+    OP_NAMES = ("plane_tests", "triangle_tests", "qp_column_sweeps", "qp_solves", "gjk_iters", "support_verts",
+                "epa_iters", "point_queries")
+
+    def profile(self) -> dict:
+        ms = (C.c_double * 7)()
+        launches = (C.c_longlong * 7)()
+        ops = (C.c_ulonglong * 8)()
+        N.check(N.lib().grasp_ctx_profile(self._ctx, ms, launches, ops))
+        return {"ms": dict(zip(self.KERNEL_CLASSES, list(ms))),
+                "launches": dict(zip(self.KERNEL_CLASSES, list(launches))),
+                "ops": dict(zip(self.OP_NAMES, list(ops)))}
+
+    def launch_count(self) -> int:
+        return int(N.lib().grasp_ctx_launch_count(self._ctx))
+
     def close(self):
         if self._ctx:
             N.lib().grasp_ctx_destroy(self._ctx)

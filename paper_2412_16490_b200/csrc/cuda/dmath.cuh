@@ -5,53 +5,72 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#if defined(__CUDA_ARCH__)
+#define GDEV_LDG(p) __ldg(p)
+#else
+#define GDEV_LDG(p) (*(p))
+#endif
+#define GDEV_FN __host__ __device__ __forceinline__
+#define GDEV_INL __host__ __device__ inline
+
 namespace gdev {
 
 struct D3 {
   double x, y, z;
 };
 
-__device__ __forceinline__ D3 mk(double x, double y, double z) { return D3{x, y, z}; }
-__device__ __forceinline__ D3 operator+(D3 a, D3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
-__device__ __forceinline__ D3 operator-(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
-__device__ __forceinline__ D3 operator-(D3 a) { return {-a.x, -a.y, -a.z}; }
-__device__ __forceinline__ D3 operator*(double s, D3 a) { return {s * a.x, s * a.y, s * a.z}; }
-__device__ __forceinline__ D3 operator*(D3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
-__device__ __forceinline__ D3 operator/(D3 a, double s) { return {a.x / s, a.y / s, a.z / s}; }
-__device__ __forceinline__ D3& operator+=(D3& a, D3 b) { a.x += b.x; a.y += b.y; a.z += b.z; return a; }
-__device__ __forceinline__ D3& operator-=(D3& a, D3 b) { a.x -= b.x; a.y -= b.y; a.z -= b.z; return a; }
-__device__ __forceinline__ double dot(D3 a, D3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-__device__ __forceinline__ double sqn(D3 a) { return dot(a, a); }
-__device__ __forceinline__ double nrm(D3 a) { return sqrt(sqn(a)); }
-__device__ __forceinline__ D3 cross(D3 a, D3 b) {
+GDEV_FN D3 mk(double x, double y, double z) { return D3{x, y, z}; }
+GDEV_FN D3 operator+(D3 a, D3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+GDEV_FN D3 operator-(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+GDEV_FN D3 operator-(D3 a) { return {-a.x, -a.y, -a.z}; }
+GDEV_FN D3 operator*(double s, D3 a) { return {s * a.x, s * a.y, s * a.z}; }
+GDEV_FN D3 operator*(D3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+GDEV_FN D3 operator/(D3 a, double s) { return {a.x / s, a.y / s, a.z / s}; }
+GDEV_FN D3& operator+=(D3& a, D3 b) { a.x += b.x; a.y += b.y; a.z += b.z; return a; }
+GDEV_FN D3& operator-=(D3& a, D3 b) { a.x -= b.x; a.y -= b.y; a.z -= b.z; return a; }
+GDEV_FN double dot(D3 a, D3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+GDEV_FN double sqn(D3 a) { return dot(a, a); }
+GDEV_FN double nrm(D3 a) { return sqrt(sqn(a)); }
+GDEV_FN D3 cross(D3 a, D3 b) {
   return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
-__device__ __forceinline__ D3 normalized(D3 a) {
+GDEV_FN D3 normalized(D3 a) {
   const double n2 = sqn(a);
   return n2 > 0 ? a / sqrt(n2) : a;
 }
-__device__ __forceinline__ bool finite3(D3 a) { return isfinite(a.x) && isfinite(a.y) && isfinite(a.z); }
-__device__ __forceinline__ double comp(D3 a, int k) { return k == 0 ? a.x : (k == 1 ? a.y : a.z); }
-__device__ __forceinline__ D3 unit(int k) { return {k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0}; }
+GDEV_FN bool finite3(D3 a) { return isfinite(a.x) && isfinite(a.y) && isfinite(a.z); }
+GDEV_FN double comp(D3 a, int k) { return k == 0 ? a.x : (k == 1 ? a.y : a.z); }
+GDEV_FN D3 unit(int k) { return {k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0}; }
 
-__device__ __forceinline__ D3 ld3(const double* p) { return {p[0], p[1], p[2]}; }
-__device__ __forceinline__ void st3(double* p, D3 v) { p[0] = v.x; p[1] = v.y; p[2] = v.z; }
-__device__ __forceinline__ D3 ldg3(const double* __restrict__ p) { return {__ldg(p), __ldg(p + 1), __ldg(p + 2)}; }
+GDEV_FN D3 ld3(const double* p) { return {p[0], p[1], p[2]}; }
+GDEV_FN void st3(double* p, D3 v) { p[0] = v.x; p[1] = v.y; p[2] = v.z; }
+GDEV_FN D3 ldg3(const double* __restrict__ p) { return {GDEV_LDG(p), GDEV_LDG(p + 1), GDEV_LDG(p + 2)}; }
+
+// Contact frame p, n, d, e (contact.cpp:9-21); n is the inward normal.
+GDEV_FN void build_frame(D3 p, D3 n, double* f) {
+  const D3 seed = fabs(n.x) > 0.99 ? mk(0, 1, 0) : mk(1, 0, 0);
+  const D3 d = normalized(cross(n, seed));
+  const D3 e = cross(n, d);
+  st3(f, p);
+  st3(f + 3, n);
+  st3(f + 6, d);
+  st3(f + 9, e);
+}
 
 // Row-major 3x3.
 struct M33 {
   double m[9];
 };
-__device__ __forceinline__ M33 eye() { return {{1, 0, 0, 0, 1, 0, 0, 0, 1}}; }
-__device__ __forceinline__ D3 mul(const M33& a, D3 v) {
+GDEV_FN M33 eye() { return {{1, 0, 0, 0, 1, 0, 0, 0, 1}}; }
+GDEV_FN D3 mul(const M33& a, D3 v) {
   return {a.m[0] * v.x + a.m[1] * v.y + a.m[2] * v.z, a.m[3] * v.x + a.m[4] * v.y + a.m[5] * v.z,
           a.m[6] * v.x + a.m[7] * v.y + a.m[8] * v.z};
 }
-__device__ __forceinline__ D3 mulT(const M33& a, D3 v) {  // a^T v
+GDEV_FN D3 mulT(const M33& a, D3 v) {  // a^T v
   return {a.m[0] * v.x + a.m[3] * v.y + a.m[6] * v.z, a.m[1] * v.x + a.m[4] * v.y + a.m[7] * v.z,
           a.m[2] * v.x + a.m[5] * v.y + a.m[8] * v.z};
 }
-__device__ __forceinline__ M33 mul(const M33& a, const M33& b) {
+GDEV_FN M33 mul(const M33& a, const M33& b) {
   M33 r;
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -60,21 +79,26 @@ __device__ __forceinline__ M33 mul(const M33& a, const M33& b) {
       r.m[i * 3 + j] = a.m[i * 3] * b.m[j] + a.m[i * 3 + 1] * b.m[3 + j] + a.m[i * 3 + 2] * b.m[6 + j];
   return r;
 }
-__device__ __forceinline__ M33 transpose(const M33& a) {
+GDEV_FN M33 transpose(const M33& a) {
   return {{a.m[0], a.m[3], a.m[6], a.m[1], a.m[4], a.m[7], a.m[2], a.m[5], a.m[8]}};
 }
-__device__ __forceinline__ double det(const M33& a) {
+GDEV_FN double det(const M33& a) {
   return a.m[0] * (a.m[4] * a.m[8] - a.m[5] * a.m[7]) - a.m[1] * (a.m[3] * a.m[8] - a.m[5] * a.m[6]) +
          a.m[2] * (a.m[3] * a.m[7] - a.m[4] * a.m[6]);
 }
-__device__ __forceinline__ D3 col(const M33& a, int c) { return {a.m[c], a.m[3 + c], a.m[6 + c]}; }
-__device__ __forceinline__ D3 row(const M33& a, int r) { return {a.m[3 * r], a.m[3 * r + 1], a.m[3 * r + 2]}; }
-__device__ __forceinline__ void set_col(M33& a, int c, D3 v) { a.m[c] = v.x; a.m[3 + c] = v.y; a.m[6 + c] = v.z; }
+GDEV_FN D3 col(const M33& a, int c) { return {a.m[c], a.m[3 + c], a.m[6 + c]}; }
+GDEV_FN D3 row(const M33& a, int r) { return {a.m[3 * r], a.m[3 * r + 1], a.m[3 * r + 2]}; }
+GDEV_FN void set_col(M33& a, int c, D3 v) { a.m[c] = v.x; a.m[3 + c] = v.y; a.m[6 + c] = v.z; }
 
 // Eigen::AngleAxisd::toRotationMatrix expression order (hand.cpp:144).
-__device__ __forceinline__ M33 angle_axis(double angle, D3 axis) {
+GDEV_FN M33 angle_axis(double angle, D3 axis) {
   double s, c;
+#if defined(__CUDA_ARCH__)
   sincos(angle, &s, &c);
+#else
+  s = ::sin(angle);
+  c = ::cos(angle);
+#endif
   const D3 sa = s * axis;
   const D3 ka = (1.0 - c) * axis;
   M33 r;
@@ -96,7 +120,7 @@ __device__ __forceinline__ M33 angle_axis(double angle, D3 axis) {
 // Nearest proper rotation to a raw 3x3 block (hand.cpp:45-73): polar factor
 // from a one-sided Jacobi SVD with the determinant fix on the smallest
 // singular direction; column Gram-Schmidt fallback when s2 < 1e-9 s0.
-__device__ inline M33 project_rotation(const M33& raw, bool* fallback) {
+GDEV_INL M33 project_rotation(const M33& raw, bool* fallback) {
   double c[3][3];  // c[col][row]
   double v[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
 #pragma unroll
@@ -181,7 +205,7 @@ __device__ inline M33 project_rotation(const M33& raw, bool* fallback) {
 }
 
 // make_pose_state tail (hand.cpp:81-93): a_inv = ((tr S) I - S)^-1, S = sym(R^T raw).
-__device__ inline bool pose_a_inv(const M33& R, const M33& raw, M33& a_inv) {
+GDEV_INL bool pose_a_inv(const M33& R, const M33& raw, M33& a_inv) {
   const M33 sf = mul(transpose(R), raw);
   M33 s;
 #pragma unroll

@@ -25,6 +25,12 @@
 
 using namespace gdev;
 
+namespace gdev {
+// qp.cu (compiled with FMA contraction).
+void launch_qp_kernel(const DevHand& H, const DevParams& P, const DevState& st, int m, int mode, int with_grad,
+                      cudaStream_t stream);
+}  // namespace gdev
+
 namespace {
 
 struct CudaError : std::runtime_error {
@@ -80,8 +86,63 @@ struct grasp_ctx {
       frames, anchors, energy, grad, stage_energy, x_p, x_s, witness;
   DevBuf<int> qp_iters, qp_conv, qp_ready, failed, have_pregrasp, err;
 
+  // Instrumentation: launch counts always; per-class CUDA-event time and
+  // algorithmic op counters only while profiling.
+  static constexpr int kClasses = 7;  // point_query, qp, step_coarse, pairs, step_mesh, fk, finalize
+  long long launches[kClasses] = {};
+  bool profiling = false;
+  double prof_ms[kClasses] = {};
+  long long prof_launches[kClasses] = {};
+  DevBuf<unsigned long long> ops;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> event_pool;
+
   ~grasp_ctx() {
+    for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
+    for (auto& p : pending) {
+      cudaEventDestroy(p.second.first);
+      cudaEventDestroy(p.second.second);
+    }
     if (stream) cudaStreamDestroy(stream);
+  }
+
+  cudaEvent_t take_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+  }
+
+  template <class F>
+  void launch(int cls, F&& f) {
+    ++launches[cls];
+    if (!profiling) {
+      f();
+      return;
+    }
+    cudaEvent_t a = take_event(), b = take_event();
+    ck(cudaEventRecord(a, stream), "event");
+    f();
+    ck(cudaEventRecord(b, stream), "event");
+    pending.push_back({cls, {a, b}});
+  }
+
+  void collect_profile() {
+    if (pending.empty()) return;
+    ck(cudaStreamSynchronize(stream), "sync");
+    for (auto& p : pending) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, p.second.first, p.second.second), "elapsed");
+      prof_ms[p.first] += ms;
+      prof_launches[p.first] += 1;
+      event_pool.push_back(p.second.first);
+      event_pool.push_back(p.second.second);
+    }
+    pending.clear();
   }
 
   void set_device() { ck(cudaSetDevice(device), "cudaSetDevice"); }
@@ -297,6 +358,8 @@ struct grasp_ctx {
     failed.ensure(g);
     have_pregrasp.ensure(g);
     err.ensure(4);
+    ops.ensure(kNumOps);
+    st.ops = profiling ? ops.p : nullptr;
     st.G = G;
     st.NQ = NQ;
     st.NP = NP;
@@ -375,22 +438,28 @@ struct grasp_ctx {
   void launch_queries(bool tips_only) {
     const int per = tips_only ? H.m : st.NQ;
     const long long n = static_cast<long long>(st.G) * per;
-    k_point_query<<<blocks(n, 128), 128, 0, stream>>>(O, st, tips_only ? h_tip_slots.p : nullptr, per);
+    launch(0, [&] {
+      k_point_query<<<blocks(n, 128), 128, 0, stream>>>(O, st, tips_only ? h_tip_slots.p : nullptr, per);
+    });
   }
   void launch_pairs(bool tips_only) {
     const int nl = tips_only ? H.m : H.L;
     const long long n = static_cast<long long>(st.G) * nl * O.P;
-    k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, tips_only ? h_tip_links_sorted.p : nullptr, nl);
+    launch(3, [&] {
+      k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, tips_only ? h_tip_links_sorted.p : nullptr, nl);
+    });
   }
   void launch_qp(const DevParams& P, int m, int mode, int with_grad) {
-    k_qp<<<blocks(st.G, 4), 128, 0, stream>>>(H, P, st, m, mode, with_grad);
+    launch(1, [&] { launch_qp_kernel(H, P, st, m, mode, with_grad, stream); });
   }
-  void launch_fk(const DevParams& P) { k_fk<<<blocks(st.G, 2), 64, 0, stream>>>(H, P, st); }
+  void launch_fk(const DevParams& P) {
+    launch(5, [&] { k_fk<<<blocks(st.G, 2), 64, 0, stream>>>(H, P, st); });
+  }
   void launch_step(const DevParams& P, const StageArgs& A, bool coarse) {
     if (coarse)
-      k_step_coarse<<<blocks(st.G, 2), 64, 0, stream>>>(H, P, A, st);
+      launch(2, [&] { k_step_coarse<<<blocks(st.G, 2), 64, 0, stream>>>(H, P, A, st); });
     else
-      k_step_mesh<<<blocks(st.G, 2), 64, 0, stream>>>(H, O, P, A, st);
+      launch(4, [&] { k_step_mesh<<<blocks(st.G, 2), 64, 0, stream>>>(H, O, P, A, st); });
   }
 
   void check_errors() {
@@ -443,17 +512,21 @@ struct grasp_ctx {
         launch_pairs(false);
       }
       launch_step(P, A, coarse);
-      if (s == 0) k_anchors<<<blocks(st.G, 128), 128, 0, stream>>>(H, st, p->skip_fine_stages ? 1 : 0);
-      if (s == 1) k_set_pregrasp<<<blocks(st.G, 128), 128, 0, stream>>>(H, st);
+      if (s == 0)
+        launch(6, [&] { k_anchors<<<blocks(st.G, 128), 128, 0, stream>>>(H, st, p->skip_fine_stages ? 1 : 0); });
+      if (s == 1) launch(6, [&] { k_set_pregrasp<<<blocks(st.G, 128), 128, 0, stream>>>(H, st); });
     }
     // Final record: witnesses at x, cold QP on their frames, squeeze.
     launch_fk(P);
     launch_queries(true);
     launch_pairs(true);
-    k_final_frames<<<blocks(static_cast<long long>(st.G) * H.m, 128), 128, 0, stream>>>(H, O, st, nullptr);
+    launch(6, [&] {
+      k_final_frames<<<blocks(static_cast<long long>(st.G) * H.m, 128), 128, 0, stream>>>(H, O, st, nullptr);
+    });
     launch_qp(P, H.m, 1, 0);
-    k_squeeze<<<blocks(st.G, 128), 128, 0, stream>>>(H, st, x_s.p);
+    launch(6, [&] { k_squeeze<<<blocks(st.G, 128), 128, 0, stream>>>(H, st, x_s.p); });
     ck(cudaGetLastError(), "kernel launch");
+    collect_profile();
   }
 };
 
@@ -735,6 +808,181 @@ int grasp_fine_contact_query(grasp_ctx* ctx, int n, const double* x, double* out
     ctx->check_errors();
     copy_out(out, ctx->witness.p, sizeof(double) * n * ctx->H.m * 11, cudaMemcpyDeviceToHost, s);
     ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+}  // extern "C"
+
+// Debug-only (not in the public header): EPA internals for pair queries.
+namespace {
+__global__ void k_pairs_debug(DevHand H, DevObject O, int n, const int* links, const int* parts, const double* poses,
+                              double* out, EpaDebug* dbg) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  M33 Rw;
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < 3; ++i) Rw.m[i * 3 + c] = poses[12 * t + 3 * c + i];
+  const D3 tw = ld3(poses + 12 * t + 9);
+  Hull A;
+  A.verts = H.link_verts + 3 * (size_t)H.link_vbeg[links[t]];
+  A.nv = H.link_vbeg[links[t] + 1] - H.link_vbeg[links[t]];
+  A.posed = true;
+  A.R = Rw;
+  A.t = tw;
+  Hull B;
+  B.verts = O.verts + 3 * (size_t)O.part_vbeg[parts[t]];
+  B.nv = O.part_vbeg[parts[t] + 1] - O.part_vbeg[parts[t]];
+  B.posed = false;
+  B.R = eye();
+  B.t = mk(0, 0, 0);
+  double scale = 1.0;
+  scale = fmax(scale, scale_of(mul(Rw, ld3(H.link_centroid + 3 * links[t])) + tw, H.link_halfnorm[links[t]]));
+  scale = fmax(scale, scale_of(ld3(O.part_centroid + 3 * parts[t]), O.part_halfnorm[parts[t]]));
+  EpaScratch scratch;
+  const PairResult r = signed_distance(A, B, scale, scratch, dbg + t);
+  store_pair(out + 11 * t, r);
+}
+}  // namespace
+
+extern "C" int grasp_debug_epa(grasp_ctx* ctx, int n, const int* link_ids, const int* part_ids, const double* poses,
+                               double* out, void* dbg_out) {
+  return guard([&] {
+    require_models(ctx);
+    ctx->set_device();
+    DevBuf<int> dl, dpi;
+    DevBuf<double> dpose, dout;
+    DevBuf<EpaDebug> ddbg;
+    dl.upload(std::vector<int>(link_ids, link_ids + n), ctx->stream);
+    dpi.upload(std::vector<int>(part_ids, part_ids + n), ctx->stream);
+    dpose.upload(std::vector<double>(poses, poses + 12 * static_cast<size_t>(n)), ctx->stream);
+    dout.ensure(static_cast<size_t>(n) * 11);
+    ddbg.ensure(n);
+    ck(cudaMemsetAsync(ddbg.p, 0, sizeof(EpaDebug) * n, ctx->stream), "memset");
+    k_pairs_debug<<<grasp_ctx::blocks(n, 64), 64, 0, ctx->stream>>>(ctx->H, ctx->O, n, dl.p, dpi.p, dpose.p, dout.p,
+                                                                    ddbg.p);
+    ck(cudaGetLastError(), "launch");
+    ck(cudaMemcpyAsync(out, dout.p, sizeof(double) * n * 11, cudaMemcpyDeviceToHost, ctx->stream), "out");
+    ck(cudaMemcpyAsync(dbg_out, ddbg.p, sizeof(EpaDebug) * n, cudaMemcpyDeviceToHost, ctx->stream), "dbg");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+namespace {
+__global__ void k_cos_debug(int n, const double* w, double* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  SP tri[3];
+  for (int i = 0; i < 3; ++i) {
+    tri[i].w = ld3(w + 9 * t + 3 * i);
+    tri[i].a = tri[i].w;
+    tri[i].b = mk(0, 0, 0);
+  }
+  const Simplex s = closest_on_simplex(tri, 3);
+  double* o = out + 8 * t;
+  o[0] = s.nkeep;
+  for (int i = 0; i < s.nkeep && i < 3; ++i) {
+    o[1 + i] = s.keep[i];
+    o[4 + i] = s.wts[i];
+  }
+}
+}  // namespace
+
+extern "C" int grasp_debug_cos(int n, const double* w, double* out) {
+  return guard([&] {
+    DevBuf<double> dw, dout;
+    dw.upload(std::vector<double>(w, w + 9 * static_cast<size_t>(n)), 0);
+    dout.ensure(static_cast<size_t>(n) * 8);
+    ck(cudaMemset(dout.p, 0, sizeof(double) * 8 * n), "memset");
+    k_cos_debug<<<1, 64>>>(n, dw.p, dout.p);
+    ck(cudaGetLastError(), "launch");
+    ck(cudaMemcpy(out, dout.p, sizeof(double) * n * 8, cudaMemcpyDeviceToHost), "out");
+  });
+}
+
+// ---------------------------------------------------------------- instrumentation
+namespace {
+__global__ void k_fp64_peak(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+  double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+  const double b = 0.999999999, c = 1e-12;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+    a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 42.0) out[0] = s;  // keep the chains alive
+}
+}  // namespace
+
+extern "C" {
+
+void* grasp_ctx_stream(grasp_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int grasp_ctx_set_profiling(grasp_ctx* ctx, int on) {
+  return guard([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    ctx->set_device();
+    ctx->collect_profile();
+    ctx->profiling = on != 0;
+    for (int c = 0; c < grasp_ctx::kClasses; ++c) {
+      ctx->prof_ms[c] = 0.0;
+      ctx->prof_launches[c] = 0;
+    }
+    ctx->ops.ensure(kNumOps);
+    ck(cudaMemsetAsync(ctx->ops.p, 0, sizeof(unsigned long long) * kNumOps, ctx->stream), "memset");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->st.ops = ctx->profiling ? ctx->ops.p : nullptr;
+  });
+}
+
+int grasp_ctx_profile(grasp_ctx* ctx, double* ms, long long* launches, unsigned long long* ops) {
+  return guard([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    ctx->set_device();
+    ctx->collect_profile();
+    for (int c = 0; c < grasp_ctx::kClasses; ++c) {
+      if (ms) ms[c] = ctx->prof_ms[c];
+      if (launches) launches[c] = ctx->prof_launches[c];
+    }
+    if (ops) {
+      ck(cudaMemcpy(ops, ctx->ops.p, sizeof(unsigned long long) * kNumOps, cudaMemcpyDeviceToHost), "ops");
+    }
+  });
+}
+
+long long grasp_ctx_launch_count(grasp_ctx* ctx) {
+  long long n = 0;
+  if (ctx)
+    for (long long v : ctx->launches) n += v;
+  return n;
+}
+
+int grasp_measure_fp64_peak(int device, double* tflops) {
+  return guard([&] {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    int sms = 0;
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    DevBuf<double> out;
+    out.ensure(1);
+    const int iters = 1 << 16, threads = 256, blocks = sms * 8;
+    k_fp64_peak<<<blocks, threads>>>(out.p, 256);  // warm-up
+    cudaEvent_t a, b;
+    ck(cudaEventCreate(&a), "event");
+    ck(cudaEventCreate(&b), "event");
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+      ck(cudaEventRecord(a), "record");
+      k_fp64_peak<<<blocks, threads>>>(out.p, iters);
+      ck(cudaEventRecord(b), "record");
+      ck(cudaEventSynchronize(b), "sync");
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+      best = std::min(best, ms);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 8.0 * iters * static_cast<double>(threads) * blocks;
+    *tflops = flops / (best * 1e-3) / 1e12;
   });
 }
 

@@ -36,12 +36,12 @@ struct SP {
   D3 w, a, b;
 };
 
-__device__ __forceinline__ D3 support(const Hull& h, D3 dir) {
+GDEV_FN D3 support(const Hull& h, D3 dir) {
   const D3 dl = h.posed ? mulT(h.R, dir) : dir;
   double best = -INFINITY;
   int arg = 0;
   for (int i = 0; i < h.nv; ++i) {
-    const double s = dl.x * __ldg(h.verts + 3 * i) + dl.y * __ldg(h.verts + 3 * i + 1) + dl.z * __ldg(h.verts + 3 * i + 2);
+    const double s = dl.x * GDEV_LDG(h.verts + 3 * i) + dl.y * GDEV_LDG(h.verts + 3 * i + 1) + dl.z * GDEV_LDG(h.verts + 3 * i + 2);
     if (s > best) {
       best = s;
       arg = i;
@@ -51,7 +51,7 @@ __device__ __forceinline__ D3 support(const Hull& h, D3 dir) {
   return h.posed ? mul(h.R, v) + h.t : v;
 }
 
-__device__ __forceinline__ SP support_pair(const Hull& A, const Hull& B, D3 dir) {
+GDEV_FN SP support_pair(const Hull& A, const Hull& B, D3 dir) {
   SP s;
   s.a = support(A, dir);
   s.b = support(B, -dir);
@@ -59,18 +59,29 @@ __device__ __forceinline__ SP support_pair(const Hull& A, const Hull& B, D3 dir)
   return s;
 }
 
-// Eigen::FullPivLU::solve restated (complete pivoting, first max in
-// column-major order, rank threshold max_pivot * n * eps, free unknowns 0).
-__device__ inline void fullpiv_solve(int n, double* m, const double* rhs, double* sol) {
-  int rowt[5], colt[5];
-  int nonzero = n;
+// Eigen::FullPivLU::solve restated for a compile-time size S (complete
+// pivoting on the largest |entry|, first in column-major order on ties;
+// rank = #{|u_ii| > max_pivot * S * eps}; unit-lower then upper substitution
+// on the rank block; free unknowns 0). Every index is compile-time or a
+// predicated select, so the matrix stays in registers.
+template <int S>
+GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (&sol)[S]) {
+  int rowt[S], colt[S];
+  int nonzero = S;
   double maxpivot = 0.0;
-  for (int k = 0; k < n; ++k) {
+  bool stopped = false;
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    rowt[k] = k;
+    colt[k] = k;
+    if (stopped) continue;
     double biggest = -1.0;
     int br = k, bc = k;
-    for (int c = k; c < n; ++c)
-      for (int r = k; r < n; ++r) {
-        const double v = fabs(m[c * n + r]);
+#pragma unroll
+    for (int c = k; c < S; ++c)
+#pragma unroll
+      for (int r = k; r < S; ++r) {
+        const double v = fabs(m[r][c]);
         if (v > biggest) {
           biggest = v;
           br = r;
@@ -79,62 +90,94 @@ __device__ inline void fullpiv_solve(int n, double* m, const double* rhs, double
       }
     if (biggest == 0.0) {
       nonzero = k;
-      for (int i = k; i < n; ++i) rowt[i] = colt[i] = i;
-      break;
+      stopped = true;
+      continue;
     }
     maxpivot = fmax(maxpivot, biggest);
     rowt[k] = br;
     colt[k] = bc;
-    if (br != k)
-      for (int c = 0; c < n; ++c) {
-        const double t = m[c * n + k];
-        m[c * n + k] = m[c * n + br];
-        m[c * n + br] = t;
-      }
-    if (bc != k)
-      for (int r = 0; r < n; ++r) {
-        const double t = m[k * n + r];
-        m[k * n + r] = m[bc * n + r];
-        m[bc * n + r] = t;
-      }
-    if (k < n - 1) {
-      const double piv = m[k * n + k];
-      for (int r = k + 1; r < n; ++r) m[k * n + r] /= piv;
-      for (int c = k + 1; c < n; ++c) {
-        const double mkc = m[c * n + k];
-        for (int r = k + 1; r < n; ++r) m[c * n + r] -= m[k * n + r] * mkc;
+#pragma unroll
+    for (int r = k + 1; r < S; ++r)
+      if (r == br)
+#pragma unroll
+        for (int c = 0; c < S; ++c) {
+          const double t = m[k][c];
+          m[k][c] = m[r][c];
+          m[r][c] = t;
+        }
+#pragma unroll
+    for (int c = k + 1; c < S; ++c)
+      if (c == bc)
+#pragma unroll
+        for (int r = 0; r < S; ++r) {
+          const double t = m[r][k];
+          m[r][k] = m[r][c];
+          m[r][c] = t;
+        }
+    if (k < S - 1) {
+      const double piv = m[k][k];
+#pragma unroll
+      for (int r = k + 1; r < S; ++r) m[r][k] /= piv;
+#pragma unroll
+      for (int c = k + 1; c < S; ++c) {
+        const double mkc = m[k][c];
+#pragma unroll
+        for (int r = k + 1; r < S; ++r) m[r][c] -= m[r][k] * mkc;
       }
     }
   }
-  const double thresh = maxpivot * (n * 2.220446049250313e-16);
+  const double thresh = maxpivot * (S * 2.220446049250313e-16);
   int rank = 0;
-  for (int i = 0; i < nonzero; ++i) rank += fabs(m[i * n + i]) > thresh;
+#pragma unroll
+  for (int i = 0; i < S; ++i) rank += (i < nonzero && fabs(m[i][i]) > thresh) ? 1 : 0;
   if (rank == 0) {
-    for (int i = 0; i < n; ++i) sol[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < S; ++i) sol[i] = 0.0;
     return;
   }
-  double c[5];
-  for (int i = 0; i < n; ++i) c[i] = rhs[i];
-  for (int k = 0; k < n; ++k) {
-    const double t = c[k];
-    c[k] = c[rowt[k]];
-    c[rowt[k]] = t;
-  }
-  for (int i = 0; i < n; ++i)
+  double c[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i) c[i] = rhs[i];
+#pragma unroll
+  for (int k = 0; k < S; ++k)
+#pragma unroll
+    for (int r = k + 1; r < S; ++r)
+      if (r == rowt[k]) {
+        const double t = c[k];
+        c[k] = c[r];
+        c[r] = t;
+      }
+#pragma unroll
+  for (int i = 0; i < S; ++i)
     if (c[i] != 0.0)
-      for (int r = i + 1; r < n; ++r) c[r] -= c[i] * m[i * n + r];
-  for (int i = rank - 1; i >= 0; --i)
-    if (c[i] != 0.0) {
-      c[i] /= m[i * n + i];
-      for (int r = 0; r < i; ++r) c[r] -= c[i] * m[i * n + r];
+#pragma unroll
+      for (int r = i + 1; r < S; ++r) c[r] -= c[i] * m[r][i];
+#pragma unroll
+  for (int i = S - 1; i >= 0; --i)
+    if (i < rank && c[i] != 0.0) {
+      c[i] /= m[i][i];
+#pragma unroll
+      for (int r = 0; r < i; ++r) c[r] -= c[i] * m[r][i];
     }
-  int perm[5] = {0, 1, 2, 3, 4};
-  for (int k = 0; k < n; ++k) {
-    const int t = perm[k];
-    perm[k] = perm[colt[k]];
-    perm[colt[k]] = t;
+  int perm[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i) perm[i] = i;
+#pragma unroll
+  for (int k = 0; k < S; ++k)
+#pragma unroll
+    for (int r = k + 1; r < S; ++r)
+      if (r == colt[k]) {
+        const int t = perm[k];
+        perm[k] = perm[r];
+        perm[r] = t;
+      }
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    const double v = i < rank ? c[i] : 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (perm[i] == j) sol[j] = v;
   }
-  for (int i = 0; i < n; ++i) sol[perm[i]] = i < rank ? c[i] : 0.0;
 }
 
 struct Simplex {
@@ -146,57 +189,105 @@ struct Simplex {
   bool contains;
 };
 
-// Closest point of conv(simp) to the origin by subset enumeration
-// (geometry.cpp:58-95), same acceptance and tie rules.
-__device__ inline Simplex closest_on_simplex(const SP* simp, int n) {
+// One subset of closest_on_simplex (geometry.cpp:61-93): solve the
+// (K+1)x(K+1) affine least-norm KKT system and apply the acceptance and
+// tie rules against the running best.
+template <int N, int MASK>
+GDEV_FN void simplex_subset(const SP* simp, const double (&gram)[4][4], Simplex& best) {
+  constexpr int K = (MASK & 1) + ((MASK >> 1) & 1) + ((MASK >> 2) & 1) + ((MASK >> 3) & 1);
+  int idx[K];
+  {
+    int k = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (MASK & (1 << i)) idx[k++] = i;
+  }
+  double m[K + 1][K + 1];
+  double rhs[K + 1];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) m[i][j] = gram[idx[i]][idx[j]];
+    m[i][K] = 1.0;
+    m[K][i] = 1.0;
+    rhs[i] = 0.0;
+  }
+  m[K][K] = 0.0;
+  rhs[K] = 1.0;
+  double sol[K + 1];
+  fullpiv_solve_t<K + 1>(m, rhs, sol);
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i <= K; ++i) ok = ok && isfinite(sol[i]);
+#pragma unroll
+  for (int i = 0; i < K; ++i) ok = ok && !(sol[i] < -1e-12);
+  if (!ok) return;
+  D3 v = mk(0, 0, 0);
+#pragma unroll
+  for (int i = 0; i < K; ++i) v += sol[i] * simp[idx[i]].w;
+  const double d2 = sqn(v);
+  if (d2 < best.dist2 - 1e-300 || (K < best.nkeep && d2 <= best.dist2 * (1.0 + 1e-12))) {
+    best.dist2 = d2;
+    best.v = v;
+    best.nkeep = K;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      best.keep[i] = i < K ? idx[i < K ? i : 0] : 0;
+      best.wts[i] = i < K ? sol[i < K ? i : 0] : 0.0;
+    }
+    best.contains = K == 4;
+  }
+}
+
+template <int N, int MASK>
+struct SubsetLoop {
+  GDEV_FN static void run(const SP* simp, const double (&gram)[4][4], Simplex& best) {
+    simplex_subset<N, MASK>(simp, gram, best);
+    SubsetLoop<N, MASK + 1>::run(simp, gram, best);
+  }
+};
+template <int N>
+struct SubsetLoop<N, (1 << N)> {
+  GDEV_FN static void run(const SP*, const double (&)[4][4], Simplex&) {}
+};
+
+// Closest point of conv(simp) to the origin by subset enumeration in mask
+// order 1..2^n-1 (geometry.cpp:58-95).
+template <int N>
+GDEV_FN Simplex closest_on_simplex_t(const SP* simp) {
+  double gram[4][4];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) gram[i][j] = dot(simp[i].w, simp[j].w);
   Simplex best;
   best.dist2 = INFINITY;
   best.v = mk(0, 0, 0);
   best.nkeep = 0;
   best.contains = false;
-  for (int mask = 1; mask < (1 << n); ++mask) {
-    int idx[4];
-    int k = 0;
-    for (int i = 0; i < n; ++i)
-      if (mask & (1 << i)) idx[k++] = i;
-    const int s = k + 1;
-    double M[25];
-    double rhs[5] = {0, 0, 0, 0, 0};
-    for (int i = 0; i < k; ++i) {
-      for (int j = 0; j < k; ++j) M[j * s + i] = dot(simp[idx[i]].w, simp[idx[j]].w);
-      M[k * s + i] = 1.0;
-      M[i * s + k] = 1.0;
-    }
-    M[k * s + k] = 0.0;
-    rhs[k] = 1.0;
-    double sol[5];
-    fullpiv_solve(s, M, rhs, sol);
-    bool ok = true;
-    for (int i = 0; i < s; ++i) ok = ok && isfinite(sol[i]);
-    for (int i = 0; ok && i < k; ++i)
-      if (sol[i] < -1e-12) ok = false;
-    if (!ok) continue;
-    D3 v = mk(0, 0, 0);
-    for (int i = 0; i < k; ++i) v += sol[i] * simp[idx[i]].w;
-    const double d2 = sqn(v);
-    if (d2 < best.dist2 - 1e-300 || (k < best.nkeep && d2 <= best.dist2 * (1.0 + 1e-12))) {
-      best.dist2 = d2;
-      best.v = v;
-      best.nkeep = k;
-      for (int i = 0; i < k; ++i) {
-        best.keep[i] = idx[i];
-        best.wts[i] = sol[i];
-      }
-      if (k == 4) best.contains = true;
-    }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    best.keep[i] = 0;
+    best.wts[i] = 0.0;
   }
+  SubsetLoop<N, 1>::run(simp, gram, best);
   return best;
+}
+
+GDEV_INL Simplex closest_on_simplex(const SP* simp, int n) {
+  switch (n) {
+    case 1: return closest_on_simplex_t<1>(simp);
+    case 2: return closest_on_simplex_t<2>(simp);
+    case 3: return closest_on_simplex_t<3>(simp);
+    default: return closest_on_simplex_t<4>(simp);
+  }
 }
 
 struct PairResult {
   double d;
   D3 pa, pb, n;
   int flags;
+  unsigned n_support, gjk_iters, epa_iters;  // op counters
 };
 
 struct EpaFace {
@@ -205,7 +296,7 @@ struct EpaFace {
   double d;
 };
 
-__device__ __forceinline__ bool lex_less(D3 a, D3 b) {
+GDEV_FN bool lex_less(D3 a, D3 b) {
   if (a.x != b.x) return a.x < b.x;
   if (a.y != b.y) return a.y < b.y;
   return a.z < b.z;
@@ -217,7 +308,7 @@ struct EpaScratch {
   int hu[kEpaMaxHorizon], hv[kEpaMaxHorizon];
 };
 
-__device__ inline EpaFace epa_make_face(const SP* verts, D3 interior, int i0, int i1, int i2) {
+GDEV_INL EpaFace epa_make_face(const SP* verts, D3 interior, int i0, int i1, int i2) {
   EpaFace f;
   f.v0 = i0;
   f.v1 = i1;
@@ -237,8 +328,14 @@ __device__ inline EpaFace epa_make_face(const SP* verts, D3 interior, int i0, in
 }
 
 // geometry.cpp:168-205 + 227-324.
-__device__ inline bool epa(SP* simp, int ns, const Hull& A, const Hull& B, double scale, EpaScratch& s,
-                           PairResult& out) {
+struct EpaDebug {
+  int iters, nv, nf, v[3];
+  double n[3], d, tri_w[9], tri_a[9], wts[3];
+  int keep[3], nkeep;
+};
+
+GDEV_INL bool epa(SP* simp, int ns, const Hull& A, const Hull& B, double scale, EpaScratch& s,
+                           PairResult& out, EpaDebug* dbg = nullptr) {
   // pad_to_tetrahedron
   const double tol = 1e-12 * scale;
   D3 dirs[10];
@@ -268,6 +365,7 @@ __device__ inline bool epa(SP* simp, int ns, const Hull& A, const Hull& B, doubl
   int nv = ns;
   for (int k = 0; k < nd && nv < 4; ++k) {
     const SP cand = support_pair(A, B, dirs[k]);
+    ++out.n_support;
     bool indep;
     if (nv == 0) {
       indep = true;
@@ -313,6 +411,8 @@ __device__ inline bool epa(SP* simp, int ns, const Hull& A, const Hull& B, doubl
     }
     best_copy = s.faces[best];
     const SP w = support_pair(A, B, best_copy.n);
+    ++out.n_support;
+    ++out.epa_iters;
     if (dot(best_copy.n, w.w) - best_copy.d <= grow_tol) break;
     if (nv >= kEpaMaxVerts) {
       out.flags |= kPairOverflow;
@@ -382,13 +482,27 @@ __device__ inline bool epa(SP* simp, int ns, const Hull& A, const Hull& B, doubl
     out.pb = tri[0].b;
   }
   out.flags |= kPairEpa;
+  if (dbg) {
+    dbg->nv = nv;
+    dbg->nf = nf;
+    dbg->v[0] = best_copy.v0; dbg->v[1] = best_copy.v1; dbg->v[2] = best_copy.v2;
+    st3(dbg->n, best_copy.n);
+    dbg->d = best_copy.d;
+    for (int i = 0; i < 3; ++i) { st3(dbg->tri_w + 3 * i, tri[i].w); st3(dbg->tri_a + 3 * i, tri[i].a); }
+    dbg->nkeep = sx.nkeep;
+    for (int i = 0; i < sx.nkeep; ++i) { dbg->keep[i] = sx.keep[i]; dbg->wts[i] = sx.wts[i]; }
+  }
   return true;
 }
 
 // signed_distance(a, pose_a, b, identity) (geometry.cpp:500-525).
-__device__ inline PairResult signed_distance(const Hull& A, const Hull& B, double scale, EpaScratch& scratch) {
+GDEV_INL PairResult signed_distance(const Hull& A, const Hull& B, double scale, EpaScratch& scratch,
+                                    EpaDebug* dbg = nullptr) {
   PairResult out;
   out.flags = 0;
+  out.n_support = 1;
+  out.gjk_iters = 0;
+  out.epa_iters = 0;
   SP simp[4];
   int ns = 1;
   simp[0] = support_pair(A, B, mk(1, 0, 0));
@@ -407,6 +521,8 @@ __device__ inline PairResult signed_distance(const Hull& A, const Hull& B, doubl
       break;
     }
     const SP w = support_pair(A, B, -sx.v);
+    ++out.n_support;
+    ++out.gjk_iters;
     const double gap = sx.dist2 - dot(sx.v, w.w);
     bool repeat = false;
     for (int i = 0; i < ns; ++i)
@@ -445,7 +561,7 @@ __device__ inline PairResult signed_distance(const Hull& A, const Hull& B, doubl
     out.n = d > 1e-14 ? (wa - wb) / d : mk(0, 0, 1);
     return out;
   }
-  epa(simp, ns, A, B, scale, scratch, out);
+  epa(simp, ns, A, B, scale, scratch, out, dbg);
   return out;
 }
 

@@ -107,6 +107,21 @@ struct DevState {
   double* x_p;        // [G*D]
   int* have_pregrasp; // [G]
   int* err;           // [4]: 0 epa-degenerate, 1 epa-overflow, 2 unused, 3 unused
+  unsigned long long* ops;  // [kNumOps] algorithmic op counters, nullptr unless profiling
+};
+
+// Op counters (profiling mode) for the roofline's algorithmic flop count
+// (SURVEY.md 8(d) constants are applied on the host).
+enum OpCounter {
+  kOpPlaneTests = 0,     // inside-test face planes evaluated
+  kOpTriangleTests = 1,  // closest_on_triangle evaluations
+  kOpQpColumnSweeps = 2, // ADMM column-sweeps
+  kOpQpSolves = 3,
+  kOpGjkIters = 4,
+  kOpSupportVerts = 5,   // vertices scanned by support (GJK + EPA)
+  kOpEpaIters = 6,
+  kOpPointQueries = 7,
+  kNumOps = 8
 };
 
 }  // namespace gdev

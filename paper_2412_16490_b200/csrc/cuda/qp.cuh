@@ -1,0 +1,392 @@
+// Lower-level QP kernel (separate translation unit, compiled with FMA
+// contraction; the geometry/kinematics kernels in kernels.cuh are compiled
+// without it so their discrete decisions match the fp64 oracle bit for bit).
+#pragma once
+
+#include "dmath.cuh"
+#include "model.cuh"
+
+namespace gdev {
+
+#ifndef GDEV_FULL_MASK
+#define GDEV_FULL_MASK
+constexpr unsigned kFull = 0xffffffffu;
+#endif
+
+__device__ __forceinline__ double qp_group_sum(double v, int base, int cnt) {
+  double s = 0.0;
+  for (int b = 0; b < cnt; ++b) s += __shfl_sync(kFull, v, base + b);
+  return s;
+}
+__device__ __forceinline__ double qp_group_max(double v, int base, int cnt) {
+  double s = 0.0;
+  for (int b = 0; b < cnt; ++b) s = fmax(s, __shfl_sync(kFull, v, base + b));
+  return s;
+}
+
+// --------------------------------------------------------------- the QP
+// Lower-level QP batch of one grasp (energy.cpp:60-92, qpsolve.cpp:45-120,
+// 193-235). Lane (j, c) = (closure direction j, contact block c) owns the
+// k edge weights of contact c in column j, the identity rows of those
+// weights and the contact-cap row c; the total-weight row is replicated in
+// the m lanes of a column. The K = P + sigma I + rho A'A solve uses the
+// structure K = B + U U^T (B block-diagonal, U = [sqrt2 W^T | sqrt(rho) 1],
+// rank 7) through Woodbury with a 7x7 capacitance inverse, so a sweep costs
+// O(k) per lane plus 8 fixed-order column reductions.
+struct QpSmem {
+  double frame[kMaxTips * 12];
+  double W[6 * kMaxTips * kMaxEdges];   // row-major 6 x n
+  double Gm[kMaxTips * kMaxEdges * 7];  // B^-1 U, n x 7
+  double Hm[49];                        // (I + U^T B^-1 U)^-1
+  double C[49];
+};
+
+
+// mode 0: coarse (frames from the tip point queries, warm start from the
+// per-grasp scratch, envelope-gradient forces written when with_grad).
+// mode 1: final record (frames from st.frames, cold start).
+// mode 2: standalone batch (frames from st.frames, warm if qp_ready).
+__global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st, int m, int mode, int with_grad) {
+  __shared__ QpSmem smem_all[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * 4 + warp;
+  if (g >= st.G) return;
+  if (st.failed[g]) return;
+  QpSmem& s = smem_all[warp];
+  const int k = P.k, n = m * k, M = m + 1 + n;
+
+  // Frames.
+  if (lane < m) {
+    if (mode == 0) {
+      const double* q = st.qres + ((size_t)g * st.NQ + H.tip_proxy[lane]) * 8;
+      build_frame(ld3(q + 1), -ld3(q + 4), s.frame + 12 * lane);
+    } else {
+      const double* f = st.frames + ((size_t)g * m + lane) * 12;
+      for (int i = 0; i < 12; ++i) s.frame[12 * lane + i] = f[i];
+    }
+  }
+  __syncwarp();
+  const double a_diag = P.sigma + P.rho;
+  const double betap = P.rho / (a_diag + k * P.rho);
+  const double sqrt2 = 1.4142135623730951, sqrt_rho = sqrt(P.rho);
+  // Wrench basis block c (contact.cpp:47-53) and B^-1 U rows.
+  if (lane < m) {
+    const int c = lane;
+    const D3 p = ld3(s.frame + 12 * c), nn = ld3(s.frame + 12 * c + 3);
+    const D3 d = ld3(s.frame + 12 * c + 6), e = ld3(s.frame + 12 * c + 9);
+    for (int j = 0; j < k; ++j) {
+      const D3 edge = nn + P.mu * (P.cos_t[j] * d + P.sin_t[j] * e);
+      const D3 tq = cross(p, edge);
+      const int col = c * k + j;
+      s.W[0 * n + col] = edge.x;
+      s.W[1 * n + col] = edge.y;
+      s.W[2 * n + col] = edge.z;
+      s.W[3 * n + col] = tq.x;
+      s.W[4 * n + col] = tq.y;
+      s.W[5 * n + col] = tq.z;
+    }
+    for (int q = 0; q < 7; ++q) {
+      double bs = 0.0;
+      for (int j = 0; j < k; ++j) bs += q < 6 ? sqrt2 * s.W[q * n + c * k + j] : sqrt_rho;
+      for (int j = 0; j < k; ++j) {
+        const double u = q < 6 ? sqrt2 * s.W[q * n + c * k + j] : sqrt_rho;
+        s.Gm[(c * k + j) * 7 + q] = (u - betap * bs) / a_diag;
+      }
+    }
+  }
+  __syncwarp();
+  // Capacitance C = I + U^T G (symmetric, 28 unique entries).
+  if (lane < 28) {
+    int p = 0, q = lane;
+    while (q >= 7 - p) {
+      q -= 7 - p;
+      ++p;
+    }
+    q += p;
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double u = p < 6 ? sqrt2 * s.W[p * n + i] : sqrt_rho;
+      acc += u * s.Gm[i * 7 + q];
+    }
+    const double v = acc + (p == q ? 1.0 : 0.0);
+    s.C[p * 7 + q] = v;
+    s.C[q * 7 + p] = v;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    // Cholesky of C, then H = C^-1 column by column.
+    double L[49];
+    for (int i = 0; i < 49; ++i) L[i] = 0.0;
+    for (int j = 0; j < 7; ++j) {
+      double dsum = s.C[j * 7 + j];
+      for (int q = 0; q < j; ++q) dsum -= L[j * 7 + q] * L[j * 7 + q];
+      const double ljj = sqrt(dsum);
+      L[j * 7 + j] = ljj;
+      for (int i = j + 1; i < 7; ++i) {
+        double v = s.C[i * 7 + j];
+        for (int q = 0; q < j; ++q) v -= L[i * 7 + q] * L[j * 7 + q];
+        L[i * 7 + j] = v / ljj;
+      }
+    }
+    for (int cidx = 0; cidx < 7; ++cidx) {
+      double y[7];
+      for (int i = 0; i < 7; ++i) {
+        double v = i == cidx ? 1.0 : 0.0;
+        for (int q = 0; q < i; ++q) v -= L[i * 7 + q] * y[q];
+        y[i] = v / L[i * 7 + i];
+      }
+      for (int i = 6; i >= 0; --i) {
+        double v = y[i];
+        for (int q = i + 1; q < 7; ++q) v -= L[q * 7 + i] * y[q];
+        y[i] = v / L[i * 7 + i];
+      }
+      for (int i = 0; i < 7; ++i) s.Hm[i * 7 + cidx] = y[i];
+    }
+  }
+  __syncwarp();
+
+  const bool active = lane < 6 * m;
+  const int j = active ? lane / m : 0;
+  const int c = active ? lane % m : 0;
+  const int base = j * m;
+  const int axis = j >> 1;
+  const double tsign = (j & 1) ? -1.0 : 1.0;
+  const double rho = P.rho, sigma = P.sigma, alpha = P.alpha;
+  const double inv_a = 1.0 / a_diag;
+  const double inv_rho = 1.0 / rho;
+
+  double x[kMaxEdges], zid[kMaxEdges], yid[kMaxEdges], q[kMaxEdges], xs[kMaxEdges];
+  double zc, yc, ztot, ytot;
+  const bool warm = (mode == 0 || mode == 2) && st.qp_ready[g];
+  const double* wx = st.warm_x + (size_t)g * n * 6;
+  const double* wy = st.warm_y + (size_t)g * M * 6;
+#pragma unroll
+  for (int e = 0; e < kMaxEdges; ++e) {
+    if (e < k) {
+      const int i = c * k + e;
+      x[e] = warm ? wx[j * n + i] : 0.0;
+      yid[e] = warm ? wy[j * M + m + 1 + i] : 0.0;
+      q[e] = (-2.0 * P.beta) * (tsign * s.W[axis * n + i]);
+    } else {
+      x[e] = yid[e] = q[e] = 0.0;
+    }
+    zid[e] = x[e];
+    xs[e] = x[e];
+  }
+  yc = warm ? wy[j * M + c] : 0.0;
+  ytot = warm ? wy[j * M + m] : 0.0;
+  {
+    double bs = 0.0;
+    for (int e = 0; e < k; ++e) bs += x[e];
+    zc = bs;
+    ztot = qp_group_sum(bs, base, m);
+  }
+  const double gamma = P.gamma_total;
+  bool frozen = !active;
+  double* ox = st.warm_x + (size_t)g * n * 6;
+  double* oy = st.warm_y + (size_t)g * M * 6;
+  double* oz = st.out_z + (size_t)g * M * 6;
+
+  int sweeps = 0;
+  for (int iter = 1; iter <= P.max_iters; ++iter) {
+    sweeps = iter;
+    // rhs = A'(rho z - y) + sigma x - q
+    const double vc = rho * zc - yc, vt = rho * ztot - ytot;
+    double rhs[kMaxEdges];
+    double bsum = 0.0;
+#pragma unroll
+    for (int e = 0; e < kMaxEdges; ++e) {
+      if (e < k) {
+        const double vi = rho * zid[e] - yid[e];
+        rhs[e] = ((vc + vt) + vi) + (sigma * x[e] - q[e]);
+        bsum += rhs[e];
+      } else {
+        rhs[e] = 0.0;
+      }
+    }
+    // t = G^T rhs over the column, s = H t
+    double tv[7];
+#pragma unroll
+    for (int p = 0; p < 7; ++p) {
+      double acc = 0.0;
+      for (int e = 0; e < k; ++e) acc += s.Gm[(c * k + e) * 7 + p] * rhs[e];
+      tv[p] = qp_group_sum(acc, base, m);
+    }
+    double sv[7];
+#pragma unroll
+    for (int p = 0; p < 7; ++p) {
+      double acc = 0.0;
+#pragma unroll
+      for (int r = 0; r < 7; ++r) acc += s.Hm[p * 7 + r] * tv[r];
+      sv[p] = acc;
+    }
+    // xt = B^-1 rhs - G s ; zt = A xt
+    double xt[kMaxEdges];
+    double ztc = 0.0;
+#pragma unroll
+    for (int e = 0; e < kMaxEdges; ++e) {
+      if (e < k) {
+        double gs = 0.0;
+#pragma unroll
+        for (int p = 0; p < 7; ++p) gs += s.Gm[(c * k + e) * 7 + p] * sv[p];
+        xt[e] = (rhs[e] - betap * bsum) * inv_a - gs;
+        ztc += xt[e];
+      } else {
+        xt[e] = 0.0;
+      }
+    }
+    const double ztt = qp_group_sum(ztc, base, m);
+    // Relaxed updates and projection.
+#pragma unroll
+    for (int e = 0; e < kMaxEdges; ++e) {
+      if (e < k) {
+        x[e] = alpha * xt[e] + (1.0 - alpha) * x[e];
+        const double zbar = alpha * xt[e] + (1.0 - alpha) * zid[e];
+        const double zn = fmax(zbar + yid[e] * inv_rho, 0.0);
+        yid[e] += rho * (zbar - zn);
+        zid[e] = zn;
+      }
+    }
+    {
+      const double zbar = alpha * ztc + (1.0 - alpha) * zc;
+      const double zn = fmin(fmax(zbar + yc * inv_rho, 0.0), 1.0);
+      yc += rho * (zbar - zn);
+      zc = zn;
+    }
+    {
+      const double zbar = alpha * ztt + (1.0 - alpha) * ztot;
+      const double zn = fmax(zbar + ytot * inv_rho, gamma);
+      ytot += rho * (zbar - zn);
+      ztot = zn;
+    }
+    if (iter % P.check_interval == 0 || iter == P.max_iters) {
+      double axc = 0.0;
+      for (int e = 0; e < k; ++e) axc += x[e];
+      const double axt = qp_group_sum(axc, base, m);
+      double rp = fmax(fabs(axc - zc), fabs(axt - ztot));
+      for (int e = 0; e < k; ++e) rp = fmax(rp, fabs(x[e] - zid[e]));
+      rp = qp_group_max(rp, base, m);
+      double wx6[6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        double acc = 0.0;
+        for (int e = 0; e < k; ++e) acc += s.W[r * n + c * k + e] * x[e];
+        wx6[r] = qp_group_sum(acc, base, m);
+      }
+      double rd = 0.0;
+      for (int e = 0; e < k; ++e) {
+        double px = 0.0;
+#pragma unroll
+        for (int r = 0; r < 6; ++r) px += s.W[r * n + c * k + e] * wx6[r];
+        const double dual = (2.0 * px + ((yc + ytot) + yid[e])) + q[e];
+        rd = fmax(rd, fabs(dual));
+      }
+      rd = qp_group_max(rd, base, m);
+      if (!frozen) {
+        const bool ok = rp <= P.eps_primal && rd <= P.eps_dual;
+        if (ok || iter == P.max_iters) {
+          frozen = true;
+          for (int e = 0; e < k; ++e) {
+            const int i = c * k + e;
+            xs[e] = x[e];
+            ox[j * n + i] = x[e];
+            oy[j * M + m + 1 + i] = yid[e];
+            oz[j * M + m + 1 + i] = zid[e];
+          }
+          oy[j * M + c] = yc;
+          oz[j * M + c] = zc;
+          if (c == 0) {
+            oy[j * M + m] = ytot;
+            oz[j * M + m] = ztot;
+            st.qp_iters[(size_t)g * 6 + j] = iter;
+            st.qp_conv[(size_t)g * 6 + j] = ok ? 1 : 0;
+          }
+        }
+      }
+      if (__all_sync(kFull, frozen)) break;
+    }
+  }
+  if (lane == 0) {
+    st.qp_ready[g] = 1;
+    if (st.ops) {
+      atomicAdd(st.ops + kOpQpColumnSweeps, 6ull * sweeps);
+      atomicAdd(st.ops + kOpQpSolves, 1ull);
+    }
+  }
+
+  // Energy report from the snapshot (energy.cpp:78-90).
+  double res[6];
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+    double acc = 0.0;
+    for (int e = 0; e < k; ++e) acc += s.W[r * n + c * k + e] * xs[e];
+    const double wl = qp_group_sum(acc, base, m);
+    res[r] = P.beta * (r == axis ? tsign : 0.0) - wl;
+  }
+  double pd = 0.0;
+#pragma unroll
+  for (int r = 0; r < 6; ++r) pd += res[r] * res[r];
+  if (active && c == 0) st.qp_perdir[(size_t)g * 6 + j] = pd;
+  double total = 0.0;
+  for (int jj = 0; jj < 6; ++jj) total += __shfl_sync(kFull, pd, jj * m);
+  if (lane == 0) st.qp_energy[g] = total;
+  if (!with_grad) return;
+
+  // Envelope gradient (energy.cpp:94-145) reduced to one force per tip.
+  const D3 p = ld3(s.frame + 12 * c), nn = ld3(s.frame + 12 * c + 3);
+  const D3 dd = ld3(s.frame + 12 * c + 6), ee = ld3(s.frame + 12 * c + 9);
+  const D3 seed = fabs(nn.x) > 0.99 ? mk(0, 1, 0) : mk(1, 0, 0);
+  const double cnorm = nrm(cross(nn, seed));
+  const D3 rf = mk(res[0], res[1], res[2]), rt = mk(res[3], res[4], res[5]);
+  double sum = 0.0, sum_cos = 0.0, sum_sin = 0.0;
+  D3 fsum = mk(0, 0, 0);
+  for (int e = 0; e < k; ++e) {
+    sum += xs[e];
+    sum_cos += xs[e] * P.cos_t[e];
+    sum_sin += xs[e] * P.sin_t[e];
+    fsum += xs[e] * (nn + P.mu * (P.cos_t[e] * dd + P.sin_t[e] * ee));
+  }
+  const D3 gv = rf + cross(rt, p);
+  // md^T g with md = -(I - d d^T)[seed]x / cnorm  ->  md^T g = (seed x ((I - d d^T) g)) / cnorm
+  const D3 proj = gv - dd * dot(dd, gv);
+  const D3 mdTg = cross(seed, proj) / cnorm;
+  // me = [n]x md - [d]x  ->  me^T g = md^T([n]x^T g) - [d]x^T g = md^T(g x n) + d x g ... expanded:
+  const D3 gxn = cross(gv, nn);
+  const D3 proj2 = gxn - dd * dot(dd, gxn);
+  const D3 meTg = cross(seed, proj2) / cnorm + cross(dd, gv);
+  const D3 an = sum * gv + (P.mu * sum_cos) * mdTg + (P.mu * sum_sin) * meTg;
+  const D3 ap = cross(fsum, rt);
+  // Sum over the 6 directions of contact c, fixed order.
+  D3 AN = mk(0, 0, 0), AP;
+  AP = mk(0, 0, 0);
+  for (int jj = 0; jj < 6; ++jj) {
+    const int src = jj * m + c;
+    AN.x += __shfl_sync(kFull, an.x, src);
+    AN.y += __shfl_sync(kFull, an.y, src);
+    AN.z += __shfl_sync(kFull, an.z, src);
+    AP.x += __shfl_sync(kFull, ap.x, src);
+    AP.y += __shfl_sync(kFull, ap.y, src);
+    AP.z += __shfl_sync(kFull, ap.z, src);
+  }
+  if (active && j == 0) {
+    const double* qb = st.qres + (size_t)g * st.NQ * 8;
+    const double h2 = 2.0 * P.fd_step;
+    D3 dpT_AP, dnT_AN;  // (dp^T AP)_k = dp.col(k) . AP
+    double vals_p[3], vals_n[3];
+    for (int kk = 0; kk < 3; ++kk) {
+      const double* qp = qb + (size_t)(H.S + c * 6 + 2 * kk) * 8;
+      const double* qm = qb + (size_t)(H.S + c * 6 + 2 * kk + 1) * 8;
+      const D3 dpc = (ld3(qp + 1) - ld3(qm + 1)) / h2;
+      const D3 dnc = (ld3(qp + 4) - ld3(qm + 4)) / h2;
+      vals_p[kk] = dot(dpc, AP);
+      vals_n[kk] = dot(dnc, AN);
+    }
+    dpT_AP = mk(vals_p[0], vals_p[1], vals_p[2]);
+    dnT_AN = mk(vals_n[0], vals_n[1], vals_n[2]);
+    const D3 F = (-2.0 * P.w_grasp) * (dpT_AP - dnT_AN);
+    st3(st.qp_force + ((size_t)g * m + c) * 3, F);
+  }
+}
+
+
+}  // namespace gdev
