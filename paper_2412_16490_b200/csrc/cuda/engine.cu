@@ -72,19 +72,47 @@ struct grasp_ctx {
   // hand
   DevHand H{};
   DevBuf<int> h_lpj, h_depth, h_path, h_jpl, h_proxy_link, h_tip_link, h_tip_proxy, h_spa, h_spb, h_lvbeg,
-      h_tip_slots, h_tip_links_sorted;
+      h_tip_slots, h_tip_links_sorted, h_link_tip;
   DevBuf<unsigned> h_subtree;
-  DevBuf<double> h_jorigin, h_jaxis, h_jlo, h_jhi, h_proxy, h_envelope, h_lverts, h_lcentroid, h_lhalf;
+  DevBuf<double> h_jorigin, h_jaxis, h_jlo, h_jhi, h_proxy, h_envelope, h_lverts, h_lcentroid, h_lhalf,
+      h_link_bsphere;
   // object
   DevObject O{};
   DevBuf<int> o_fbeg, o_vbeg;
-  DevBuf<double> o_faces, o_verts, o_centroid, o_half, o_obb;
+  DevBuf<double> o_faces, o_verts, o_centroid, o_half, o_obb, o_part_sphere, o_face_sphere;
+
+  // Bounding sphere (AABB center, max vertex distance, relative slack) of
+  // each vertex range [begin[i], begin[i+1]).
+  static std::vector<double> bounding_spheres(const double* verts, const int* begin, int count) {
+    std::vector<double> out(4 * static_cast<size_t>(count));
+    for (int i = 0; i < count; ++i) {
+      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+      for (int v = begin[i]; v < begin[i + 1]; ++v)
+        for (int k = 0; k < 3; ++k) {
+          lo[k] = std::min(lo[k], verts[3 * v + k]);
+          hi[k] = std::max(hi[k], verts[3 * v + k]);
+        }
+      double c[3], r = 0.0;
+      for (int k = 0; k < 3; ++k) c[k] = 0.5 * (lo[k] + hi[k]);
+      for (int v = begin[i]; v < begin[i + 1]; ++v) {
+        const double dx = verts[3 * v] - c[0], dy = verts[3 * v + 1] - c[1], dz = verts[3 * v + 2] - c[2];
+        r = std::max(r, std::sqrt(dx * dx + dy * dy + dz * dz));
+      }
+      out[4 * i] = c[0];
+      out[4 * i + 1] = c[1];
+      out[4 * i + 2] = c[2];
+      out[4 * i + 3] = r * (1.0 + 1e-12) + 1e-15;
+    }
+    return out;
+  }
 
   // per-grasp state
   DevState st{};
   DevBuf<double> x, pose, world, joints, qpts, qres, pairs, warm_x, warm_y, out_z, qp_force, qp_energy, qp_perdir,
       frames, anchors, energy, grad, stage_energy, x_p, x_s, witness;
-  DevBuf<int> qp_iters, qp_conv, qp_ready, failed, have_pregrasp, err;
+  DevBuf<int> qp_iters, qp_conv, qp_ready, failed, have_pregrasp, err, ovf_count, ovf_list;
+  DevBuf<EpaScratchBig> big_scratch;
+  static constexpr int kBigSlots = 1024;
 
   // Instrumentation: launch counts always; per-class CUDA-event time and
   // algorithmic op counters only while profiling.
@@ -206,6 +234,9 @@ struct grasp_ctx {
       const double* o = d->link_obb + 15 * l;
       half[l] = std::sqrt(o[3] * o[3] + o[4] * o[4] + o[5] * o[5]);
     }
+    std::vector<int> link_tip(L, -1);
+    for (int f = 0; f < m; ++f) link_tip[tip_link[f]] = f;
+    std::vector<double> bsphere = bounding_spheres(d->verts, d->link_vert_begin, L);
     cudaStream_t s = stream;
     h_lpj.upload(std::vector<int>(d->link_parent_joint, d->link_parent_joint + L), s);
     h_depth.upload(depth, s);
@@ -229,7 +260,11 @@ struct grasp_ctx {
     h_lcentroid.upload(centroid, s);
     h_lhalf.upload(half, s);
     h_tip_links_sorted.upload(tip_link, s);
+    h_link_tip.upload(link_tip, s);
+    h_link_bsphere.upload(bsphere, s);
     ck(cudaStreamSynchronize(s), "hand upload");
+    H.link_tip = h_link_tip.p;
+    H.link_bsphere = h_link_bsphere.p;
     H.L = L;
     H.dof = dof;
     H.m = m;
@@ -296,6 +331,23 @@ struct grasp_ctx {
     }
     std::vector<int> fbeg(d->part_face_begin, d->part_face_begin + P + 1);
     std::vector<int> vbeg(d->part_vert_begin, d->part_vert_begin + P + 1);
+    const std::vector<double> part_sphere = bounding_spheres(d->verts, d->part_vert_begin, P);
+    // Per-face sphere: triangle centroid, max vertex distance (+ slack).
+    std::vector<double> face_sphere(static_cast<size_t>(d->n_faces) * 4);
+    for (int f = 0; f < d->n_faces; ++f) {
+      const double* F = faces.data() + static_cast<size_t>(f) * kFaceStride;
+      double c[3];
+      for (int k = 0; k < 3; ++k) c[k] = (F[k] + F[3 + k] + F[6 + k]) / 3.0;
+      double r = 0.0;
+      for (int v = 0; v < 3; ++v) {
+        const double dx = F[3 * v] - c[0], dy = F[3 * v + 1] - c[1], dz = F[3 * v + 2] - c[2];
+        r = std::max(r, std::sqrt(dx * dx + dy * dy + dz * dz));
+      }
+      face_sphere[4 * f] = c[0];
+      face_sphere[4 * f + 1] = c[1];
+      face_sphere[4 * f + 2] = c[2];
+      face_sphere[4 * f + 3] = r * (1.0 + 1e-12) + 1e-15;
+    }
     std::vector<double> half(P);
     for (int p = 0; p < P; ++p) {
       const double* o = d->part_obb + 15 * p;
@@ -309,7 +361,11 @@ struct grasp_ctx {
     o_centroid.upload(std::vector<double>(d->part_centroid, d->part_centroid + 3 * P), s);
     o_half.upload(half, s);
     o_obb.upload(std::vector<double>(d->part_obb, d->part_obb + 15 * P), s);
+    o_part_sphere.upload(part_sphere, s);
+    o_face_sphere.upload(face_sphere, s);
     ck(cudaStreamSynchronize(s), "object upload");
+    O.part_sphere = o_part_sphere.p;
+    O.face_sphere = o_face_sphere.p;
     O.P = P;
     O.F = d->n_faces;
     O.part_fbeg = o_fbeg.p;
@@ -360,6 +416,14 @@ struct grasp_ctx {
     err.ensure(4);
     ops.ensure(kNumOps);
     st.ops = profiling ? ops.p : nullptr;
+    ovf_count.ensure(1);
+    ovf_list.ensure(g * NP);
+    big_scratch.ensure(kBigSlots);
+    st.ovf_count = ovf_count.p;
+    st.ovf_list = ovf_list.p;
+    st.ovf_cap = static_cast<int>(g * NP);
+    st.big_scratch = big_scratch.p;
+    st.big_slots = kBigSlots;
     st.G = G;
     st.NQ = NQ;
     st.NP = NP;
@@ -446,7 +510,9 @@ struct grasp_ctx {
     const int nl = tips_only ? H.m : H.L;
     const long long n = static_cast<long long>(st.G) * nl * O.P;
     launch(3, [&] {
+      ck(cudaMemsetAsync(ovf_count.p, 0, sizeof(int), stream), "memset");
       k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, tips_only ? h_tip_links_sorted.p : nullptr, nl);
+      k_pairs_big<<<kBigSlots / 128, 128, 0, stream>>>(H, O, st);
     });
   }
   void launch_qp(const DevParams& P, int m, int mode, int with_grad) {
@@ -736,7 +802,9 @@ int grasp_signed_distance(grasp_ctx* ctx, int n, const int* link_ids, const int*
     dpi.upload(std::vector<int>(part_ids, part_ids + n), ctx->stream);
     dpose.upload(std::vector<double>(poses, poses + 12 * static_cast<size_t>(n)), ctx->stream);
     dout.ensure(static_cast<size_t>(n) * 11);
-    k_pairs_raw<<<grasp_ctx::blocks(n, 128), 128, 0, ctx->stream>>>(ctx->H, ctx->O, n, dl.p, dpi.p, dpose.p, dout.p);
+    ctx->big_scratch.ensure(grasp_ctx::kBigSlots);
+    k_pairs_raw<<<grasp_ctx::kBigSlots / 128, 128, 0, ctx->stream>>>(ctx->H, ctx->O, n, dl.p, dpi.p, dpose.p, dout.p,
+                                                                     ctx->big_scratch.p);
     ck(cudaGetLastError(), "launch");
     ck(cudaMemcpyAsync(out, dout.p, sizeof(double) * n * 11, cudaMemcpyDeviceToHost, ctx->stream), "out");
     ck(cudaStreamSynchronize(ctx->stream), "sync");

@@ -15,14 +15,12 @@ constexpr double kTouchTol = 1e-10;   // geometry.cpp:12
 constexpr double kGjkRelTol = 1e-14;  // geometry.cpp:13
 constexpr int kGjkMaxIters = 128;     // geometry.cpp:14
 constexpr int kEpaMaxIters = 512;     // geometry.cpp:15
-constexpr int kEpaMaxVerts = 72;
-constexpr int kEpaMaxFaces = 160;
-constexpr int kEpaMaxHorizon = 120;
 
 // Pair status bits written next to each result.
 constexpr int kPairEpa = 1;
 constexpr int kPairOverflow = 2;
 constexpr int kPairDegenerate = 4;
+constexpr int kPairCulled = 8;  // provably separated, GJK skipped (d stored as +inf)
 
 struct Hull {
   const double* __restrict__ verts;  // nv*3
@@ -302,11 +300,18 @@ GDEV_FN bool lex_less(D3 a, D3 b) {
   return a.z < b.z;
 }
 
-struct EpaScratch {
-  SP verts[kEpaMaxVerts];
-  EpaFace faces[kEpaMaxFaces];
-  int hu[kEpaMaxHorizon], hv[kEpaMaxHorizon];
+// EPA polytope storage. The common case fits a small per-thread buffer;
+// pairs that outgrow it are redone with the large buffer (global memory),
+// which covers the reference's 512-iteration cap (geometry.cpp:15).
+template <int V, int F, int HZ>
+struct EpaScratchT {
+  static constexpr int kV = V, kF = F, kH = HZ;
+  SP verts[V];
+  EpaFace faces[F];
+  int hu[HZ], hv[HZ];
 };
+using EpaScratch = EpaScratchT<64, 128, 96>;
+using EpaScratchBig = EpaScratchT<kEpaMaxIters + 8, 4 * kEpaMaxIters, 4 * kEpaMaxIters>;
 
 GDEV_INL EpaFace epa_make_face(const SP* verts, D3 interior, int i0, int i1, int i2) {
   EpaFace f;
@@ -334,8 +339,10 @@ struct EpaDebug {
   int keep[3], nkeep;
 };
 
-GDEV_INL bool epa(SP* simp, int ns, const Hull& A, const Hull& B, double scale, EpaScratch& s,
-                           PairResult& out, EpaDebug* dbg = nullptr) {
+template <class Scratch>
+GDEV_INL bool epa(SP* simp, int ns, const Hull& A, const Hull& B, double scale, Scratch& s, PairResult& out,
+                  EpaDebug* dbg = nullptr) {
+  constexpr int kEpaMaxVerts = Scratch::kV, kEpaMaxFaces = Scratch::kF, kEpaMaxHorizon = Scratch::kH;
   // pad_to_tetrahedron
   const double tol = 1e-12 * scale;
   D3 dirs[10];
@@ -496,7 +503,8 @@ GDEV_INL bool epa(SP* simp, int ns, const Hull& A, const Hull& B, double scale, 
 }
 
 // signed_distance(a, pose_a, b, identity) (geometry.cpp:500-525).
-GDEV_INL PairResult signed_distance(const Hull& A, const Hull& B, double scale, EpaScratch& scratch,
+template <class Scratch>
+GDEV_INL PairResult signed_distance(const Hull& A, const Hull& B, double scale, Scratch& scratch,
                                     EpaDebug* dbg = nullptr) {
   PairResult out;
   out.flags = 0;

@@ -220,6 +220,14 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
   unsigned planes = 0, tris = 0;
   for (int part = 0; part < O.P; ++part) {
     const int f0 = __ldg(O.part_fbeg + part), f1 = __ldg(O.part_fbeg + part + 1);
+    // Part-level cull: every point of the part is at least |p - c| - r
+    // away; a part that cannot reach below the current best cannot win the
+    // strict '<' across parts (geometry.cpp:533), so skipping it is exact.
+    {
+      const double* S = O.part_sphere + 4 * part;
+      const double lb = nrm(p - ldg3(S)) - __ldg(S + 3) - kCullSlack;
+      if (lb > best.d) continue;
+    }
     bool inside = true;
     double min_depth = INFINITY;
     D3 best_n = mk(0, 0, 1);
@@ -245,10 +253,25 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
       nn = best_n;
       pt = p + best_n * min_depth;
     } else {
+      // Brute-force closest point over the faces in index order with strict
+      // '<' (geometry.cpp:384-392), evaluated exactly only where it can
+      // matter: a cheap pass over per-face bounding spheres gives an upper
+      // bound ub >= min_f d_f; a face whose lower bound |p-c_f| - r_f exceeds
+      // min(ub, running best) is strictly worse than the final minimum and
+      // is skipped. The argmin and its value are therefore unchanged.
+      double ub = INFINITY;
+      for (int f = f0; f < f1; ++f) {
+        const double* S = O.face_sphere + 4 * (size_t)f;
+        ub = fmin(ub, nrm(p - ldg3(S)) + __ldg(S + 3));
+      }
+      ub += kCullSlack;
       sd = INFINITY;
       pt = mk(0, 0, 0);
-      tris += f1 - f0;
       for (int f = f0; f < f1; ++f) {
+        const double* S = O.face_sphere + 4 * (size_t)f;
+        const double lb = nrm(p - ldg3(S)) - __ldg(S + 3) - kCullSlack;
+        if (lb > ub || lb > sd) continue;
+        ++tris;
         const double* F = O.faces + (size_t)f * kFaceStride;
         const D3 c = closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6));
         const double d = nrm(p - c);
@@ -311,8 +334,9 @@ __device__ __forceinline__ double scale_of(D3 centroid_world, double halfnorm) {
   return nrm(centroid_world) + 2.0 * halfnorm;
 }
 
+template <class Scratch>
 __device__ inline PairResult link_part_distance(const DevHand& H, const DevObject& O, int link, int part,
-                                                const M33& Rw, D3 tw, EpaScratch& scratch) {
+                                                const M33& Rw, D3 tw, Scratch& scratch) {
   Hull A;
   A.verts = H.link_verts + 3 * (size_t)H.link_vbeg[link];
   A.nv = H.link_vbeg[link + 1] - H.link_vbeg[link];
@@ -340,6 +364,42 @@ __device__ __forceinline__ void store_pair(double* o, const PairResult& r) {
   o[10] = r.flags;
 }
 
+// OBB-vs-sphere lower bound against an object part (geometry.cpp:544-557).
+__device__ __forceinline__ double obb_sphere(const double* obb, D3 center, double radius) {
+  const D3 oc = ld3(obb);
+  const D3 half = ld3(obb + 3);
+  // rotation column-major: columns are axes; q = rot^T (c - oc)
+  const D3 rel = center - oc;
+  const D3 q = mk(obb[6] * rel.x + obb[7] * rel.y + obb[8] * rel.z, obb[9] * rel.x + obb[10] * rel.y + obb[11] * rel.z,
+                  obb[12] * rel.x + obb[13] * rel.y + obb[14] * rel.z);
+  const D3 ex = mk(fabs(q.x) - half.x, fabs(q.y) - half.y, fabs(q.z) - half.z);
+  double dist;
+  if (ex.x <= 0 && ex.y <= 0 && ex.z <= 0)
+    dist = fmax(ex.x, fmax(ex.y, ex.z));
+  else
+    dist = nrm(mk(fmax(ex.x, 0.0), fmax(ex.y, 0.0), fmax(ex.z, 0.0)));
+  return dist - radius;
+}
+
+// True when the exact signed distance of (link, part) is needed: the pair
+// is in a fingertip's witness keep-set (the same OBB test select_witness
+// applies, pipeline.cpp:332-334), or it may penetrate. Everything else has
+// d > 0 by the link-sphere vs part-OBB lower bound, and the reference only
+// reads d < 0 from it (hinge, pipeline.cpp:182), so it is stored as +inf.
+__device__ __forceinline__ bool pair_needed(const DevHand& H, const DevObject& O, const DevState& st, int g,
+                                            int link, int part, const M33& Rw, D3 tw) {
+  const int f = H.link_tip[link];
+  if (f >= 0) {
+    const int tp = H.tip_proxy[f];
+    const D3 center = mul(Rw, ld3(H.proxy + 4 * tp)) + tw;
+    const double reference = st.qres[((size_t)g * st.NQ + tp) * 8] - H.proxy[4 * tp + 3];
+    if (obb_sphere(O.part_obb + 15 * part, center, H.tip_envelope[f]) < reference + 1e-9) return true;
+  }
+  const double* bs = H.link_bsphere + 4 * link;
+  const D3 c = mul(Rw, ld3(bs)) + tw;
+  return !(obb_sphere(O.part_obb + 15 * part, c, bs[3]) > kCullSlack);
+}
+
 // One thread per (grasp, link, part); consecutive threads share (link, part)
 // so the support scans read the same vertices across the warp.
 __global__ void __launch_bounds__(128) k_pairs(DevHand H, DevObject O, DevState st, const int* __restrict__ links,
@@ -354,9 +414,15 @@ __global__ void __launch_bounds__(128) k_pairs(DevHand H, DevObject O, DevState 
   const double* w = st.world + ((size_t)g * H.L + link) * 12;
   M33 Rw;
   for (int i = 0; i < 9; ++i) Rw.m[i] = w[i];
+  double* o = st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12;
+  if (!pair_needed(H, O, st, g, link, part, Rw, ld3(w + 9))) {
+    o[0] = INFINITY;
+    o[10] = kPairCulled;
+    return;
+  }
   EpaScratch scratch;
   const PairResult r = link_part_distance(H, O, link, part, Rw, ld3(w + 9), scratch);
-  store_pair(st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12, r);
+  store_pair(o, r);
   if (st.ops) {
     const unsigned nv = (H.link_vbeg[link + 1] - H.link_vbeg[link]) + (O.part_vbeg[part + 1] - O.part_vbeg[part]);
     atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * nv);
@@ -364,21 +430,49 @@ __global__ void __launch_bounds__(128) k_pairs(DevHand H, DevObject O, DevState 
     atomicAdd(st.ops + kOpEpaIters, (unsigned long long)r.epa_iters);
   }
   if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
-  if (r.flags & kPairOverflow) atomicAdd(st.err + 1, 1);
+  if (r.flags & kPairOverflow) {
+    // Outgrew the per-thread polytope: queue for k_pairs_big.
+    const int slot = atomicAdd(st.ovf_count, 1);
+    if (slot < st.ovf_cap)
+      st.ovf_list[slot] = (int)((size_t)g * st.NP + link * O.P + part);
+    else
+      atomicAdd(st.err + 1, 1);
+  }
 }
 
-// Standalone pair surface (teacher-forced tests): poses[n*12] column-major R + t.
+// Redoes the queued pairs with the large global-memory EPA buffer.
+__global__ void __launch_bounds__(128) k_pairs_big(DevHand H, DevObject O, DevState st) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int count = min(*st.ovf_count, st.ovf_cap);
+  if (tid >= st.big_slots) return;
+  EpaScratchBig& scratch = static_cast<EpaScratchBig*>(st.big_scratch)[tid];
+  for (int i = tid; i < count; i += st.big_slots) {
+    const int slot = st.ovf_list[i];
+    const int g = slot / st.NP, lp = slot % st.NP;
+    const int link = lp / O.P, part = lp % O.P;
+    const double* w = st.world + ((size_t)g * H.L + link) * 12;
+    M33 Rw;
+    for (int k = 0; k < 9; ++k) Rw.m[k] = w[k];
+    const PairResult r = link_part_distance(H, O, link, part, Rw, ld3(w + 9), scratch);
+    store_pair(st.pairs + (size_t)slot * 12, r);
+    if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
+    if (r.flags & kPairOverflow) atomicAdd(st.err + 1, 1);
+  }
+}
+
+// Standalone pair surface (teacher-forced tests): poses[n*12] column-major R
+// + t; grid-stride over n with one large EPA buffer per thread.
 __global__ void k_pairs_raw(DevHand H, DevObject O, int n, const int* __restrict__ links, const int* __restrict__ parts,
-                            const double* __restrict__ poses, double* out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  M33 Rw;
-  for (int c = 0; c < 3; ++c)
-    for (int i = 0; i < 3; ++i) Rw.m[i * 3 + c] = poses[12 * t + 3 * c + i];
-  EpaScratch scratch;
-  const PairResult r = link_part_distance(H, O, links[t], parts[t], Rw, ld3(poses + 12 * t + 9), scratch);
-  store_pair(out + 11 * t, r);
-  out[11 * t + 10] = r.flags;
+                            const double* __restrict__ poses, double* out, EpaScratchBig* big) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int t = tid; t < n; t += gridDim.x * blockDim.x) {
+    M33 Rw;
+    for (int c = 0; c < 3; ++c)
+      for (int i = 0; i < 3; ++i) Rw.m[i * 3 + c] = poses[12 * t + 3 * c + i];
+    const PairResult r = link_part_distance(H, O, links[t], parts[t], Rw, ld3(poses + 12 * t + 9), big[tid]);
+    store_pair(out + 11 * t, r);
+    out[11 * t + 10] = r.flags;
+  }
 }
 
 // ------------------------------------------------------ gradient assembly
@@ -643,23 +737,6 @@ __global__ void __launch_bounds__(64) k_step_coarse(DevHand H, DevParams P, Stag
   total = __shfl_sync(kFull, total, 0);
   if (with_grad) expand_gradient(H, s, lane, acc);
   finish_iteration(H, P, A, st, g, lane, s, total);
-}
-
-// OBB-vs-sphere lower bound against an object part (geometry.cpp:544-557).
-__device__ __forceinline__ double obb_sphere(const double* obb, D3 center, double radius) {
-  const D3 oc = ld3(obb);
-  const D3 half = ld3(obb + 3);
-  // rotation column-major: columns are axes; q = rot^T (c - oc)
-  const D3 rel = center - oc;
-  const D3 q = mk(obb[6] * rel.x + obb[7] * rel.y + obb[8] * rel.z, obb[9] * rel.x + obb[10] * rel.y + obb[11] * rel.z,
-                  obb[12] * rel.x + obb[13] * rel.y + obb[14] * rel.z);
-  const D3 ex = mk(fabs(q.x) - half.x, fabs(q.y) - half.y, fabs(q.z) - half.z);
-  double dist;
-  if (ex.x <= 0 && ex.y <= 0 && ex.z <= 0)
-    dist = fmax(ex.x, fmax(ex.y, ex.z));
-  else
-    dist = nrm(mk(fmax(ex.x, 0.0), fmax(ex.y, 0.0), fmax(ex.z, 0.0)));
-  return dist - radius;
 }
 
 struct Witness {

@@ -19,6 +19,11 @@ constexpr int kMaxParts = 64;
 // nd = n.a, valid = (len >= 1e-30). 16 doubles = 128 B per face.
 constexpr int kFaceStride = 16;
 
+// Absolute slack on every conservative culling bound (metres). Bounds are
+// computed in fp64 from quantities of size ~0.1-1, so their rounding error is
+// ~1e-16; the slack only has to dominate that.
+constexpr double kCullSlack = 1e-9;
+
 struct DevHand {
   int L, dof, m, S, nsp, D;
   const int* link_parent_joint;     // [L]
@@ -41,6 +46,8 @@ struct DevHand {
   const double* link_verts;         // [nv*3]
   const double* link_centroid;      // [L*3]
   const double* link_halfnorm;      // [L] |obb.half_extents|
+  const int* link_tip;              // [L] fingertip index of the link, -1 if none
+  const double* link_bsphere;       // [L*4] bounding sphere of the link hull (link frame): center, radius
 };
 
 struct DevObject {
@@ -52,6 +59,8 @@ struct DevObject {
   const double* part_centroid;  // [P*3]
   const double* part_halfnorm;  // [P]
   const double* part_obb;       // [P*15] center, half, rotation (column-major)
+  const double* part_sphere;    // [P*4] bounding sphere of the part: center, radius
+  const double* face_sphere;    // [F*4] bounding sphere of each triangle: center, radius
 };
 
 struct DevParams {
@@ -108,6 +117,11 @@ struct DevState {
   int* have_pregrasp; // [G]
   int* err;           // [4]: 0 epa-degenerate, 1 epa-overflow, 2 unused, 3 unused
   unsigned long long* ops;  // [kNumOps] algorithmic op counters, nullptr unless profiling
+  int* ovf_count;      // pairs whose EPA outgrew the per-thread polytope this launch
+  int* ovf_list;       // [ovf_cap] their slots: (g * NP + link * P + part)
+  int ovf_cap;
+  void* big_scratch;   // [big_slots] EpaScratchBig in global memory
+  int big_slots;
 };
 
 // Op counters (profiling mode) for the roofline's algorithmic flop count
