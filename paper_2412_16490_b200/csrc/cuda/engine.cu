@@ -80,6 +80,7 @@ struct grasp_ctx {
   DevObject O{};
   DevBuf<int> o_fbeg, o_vbeg;
   DevBuf<double> o_faces, o_verts, o_centroid, o_half, o_obb, o_part_sphere, o_face_sphere;
+  DevBuf<float4> o_face_sphere32;
 
   // Bounding sphere (AABB center, max vertex distance, relative slack) of
   // each vertex range [begin[i], begin[i+1]).
@@ -113,6 +114,11 @@ struct grasp_ctx {
   DevBuf<int> qp_iters, qp_conv, qp_ready, failed, have_pregrasp, err, ovf_count, ovf_list;
   DevBuf<EpaScratchBig> big_scratch;
   static constexpr int kBigSlots = 1024;
+  // Pair kernel variant (GRASP_PAIRS=thread|warp, default thread).
+  int pairs_variant = [] {
+    const char* v = std::getenv("GRASP_PAIRS");
+    return v && std::string(v) == "warp" ? 1 : 0;
+  }();
 
   // Instrumentation: launch counts always; per-class CUDA-event time and
   // algorithmic op counters only while profiling.
@@ -363,9 +369,18 @@ struct grasp_ctx {
     o_obb.upload(std::vector<double>(d->part_obb, d->part_obb + 15 * P), s);
     o_part_sphere.upload(part_sphere, s);
     o_face_sphere.upload(face_sphere, s);
+    std::vector<float4> face32(d->n_faces);
+    for (int f = 0; f < d->n_faces; ++f) {
+      const float r = static_cast<float>(face_sphere[4 * f + 3]);
+      face32[f] = make_float4(static_cast<float>(face_sphere[4 * f]), static_cast<float>(face_sphere[4 * f + 1]),
+                              static_cast<float>(face_sphere[4 * f + 2]),
+                              std::nextafter(std::nextafter(r, 1e30f), 1e30f) * (1.0f + 1e-6f));
+    }
+    o_face_sphere32.upload(face32, s);
     ck(cudaStreamSynchronize(s), "object upload");
     O.part_sphere = o_part_sphere.p;
     O.face_sphere = o_face_sphere.p;
+    O.face_sphere32 = o_face_sphere32.p;
     O.P = P;
     O.F = d->n_faces;
     O.part_fbeg = o_fbeg.p;
@@ -511,7 +526,10 @@ struct grasp_ctx {
     const long long n = static_cast<long long>(st.G) * nl * O.P;
     launch(3, [&] {
       ck(cudaMemsetAsync(ovf_count.p, 0, sizeof(int), stream), "memset");
-      k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, tips_only ? h_tip_links_sorted.p : nullptr, nl);
+      if (pairs_variant == 1)
+        k_pairs_warp<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, tips_only ? h_tip_links_sorted.p : nullptr, nl);
+      else
+        k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, tips_only ? h_tip_links_sorted.p : nullptr, nl);
       k_pairs_big<<<kBigSlots / 128, 128, 0, stream>>>(H, O, st);
     });
   }

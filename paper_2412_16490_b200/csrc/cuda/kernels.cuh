@@ -12,6 +12,7 @@
 
 #include "dmath.cuh"
 #include "gjk.cuh"
+#include "gjk_warp.cuh"
 #include "model.cuh"
 
 namespace gdev {
@@ -259,24 +260,30 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
       // bound ub >= min_f d_f; a face whose lower bound |p-c_f| - r_f exceeds
       // min(ub, running best) is strictly worse than the final minimum and
       // is skipped. The argmin and its value are therefore unchanged.
-      double ub = INFINITY;
+      // Bounds in fp32 with kCullSlack32 (conservative); exact work in fp64.
+      const float px = (float)p.x, py = (float)p.y, pz = (float)p.z;
+      float ub32 = INFINITY;
       for (int f = f0; f < f1; ++f) {
-        const double* S = O.face_sphere + 4 * (size_t)f;
-        ub = fmin(ub, nrm(p - ldg3(S)) + __ldg(S + 3));
+        const float4 S = __ldg(O.face_sphere32 + f);
+        const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
+        ub32 = fminf(ub32, sqrtf(dx * dx + dy * dy + dz * dz) + S.w);
       }
-      ub += kCullSlack;
+      ub32 += kCullSlack32;
       sd = INFINITY;
+      float sd32 = INFINITY;
       pt = mk(0, 0, 0);
       for (int f = f0; f < f1; ++f) {
-        const double* S = O.face_sphere + 4 * (size_t)f;
-        const double lb = nrm(p - ldg3(S)) - __ldg(S + 3) - kCullSlack;
-        if (lb > ub || lb > sd) continue;
+        const float4 S = __ldg(O.face_sphere32 + f);
+        const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
+        const float lb = sqrtf(dx * dx + dy * dy + dz * dz) - S.w - kCullSlack32;
+        if (lb > ub32 || lb > sd32) continue;
         ++tris;
         const double* F = O.faces + (size_t)f * kFaceStride;
         const D3 c = closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6));
         const double d = nrm(p - c);
         if (d < sd) {
           sd = d;
+          sd32 = __double2float_ru(d) + kCullSlack32;
           pt = c;
         }
       }
@@ -437,6 +444,81 @@ __global__ void __launch_bounds__(128) k_pairs(DevHand H, DevObject O, DevState 
       st.ovf_list[slot] = (int)((size_t)g * st.NP + link * O.P + part);
     else
       atomicAdd(st.err + 1, 1);
+  }
+}
+
+// Warp-cooperative variant: each warp takes 32 consecutive pair slots, every
+// lane runs the cull test for its slot, then the whole warp evaluates the
+// needed pairs one after another (gjk_warp.cuh).
+__global__ void __launch_bounds__(128) k_pairs_warp(DevHand H, DevObject O, DevState st,
+                                                    const int* __restrict__ links, int n_links) {
+  __shared__ WarpEpa epa_smem[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long total = (long long)st.G * n_links * O.P;
+  const long long base = ((long long)blockIdx.x * 4 + warp) * 32;
+  if (base >= total) return;
+  const long long t = base + lane;
+  bool need = false;
+  if (t < total) {
+    const int g = (int)(t % st.G);
+    const int lp = (int)(t / st.G);
+    const int link = links ? links[lp / O.P] : lp / O.P;
+    const int part = lp % O.P;
+    if (!st.failed[g]) {
+      const double* w = st.world + ((size_t)g * H.L + link) * 12;
+      M33 Rw;
+      for (int i = 0; i < 9; ++i) Rw.m[i] = w[i];
+      need = pair_needed(H, O, st, g, link, part, Rw, ld3(w + 9));
+      if (!need) {
+        double* o = st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12;
+        o[0] = INFINITY;
+        o[10] = kPairCulled;
+      }
+    }
+  }
+  unsigned mask = __ballot_sync(kFull, need);
+  while (mask) {
+    const int src = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const long long ts = base + src;
+    const int g = (int)(ts % st.G);
+    const int lp = (int)(ts / st.G);
+    const int link = links ? links[lp / O.P] : lp / O.P;
+    const int part = lp % O.P;
+    const double* w = st.world + ((size_t)g * H.L + link) * 12;
+    Hull A;
+    A.verts = H.link_verts + 3 * (size_t)H.link_vbeg[link];
+    A.nv = H.link_vbeg[link + 1] - H.link_vbeg[link];
+    A.posed = true;
+    for (int i = 0; i < 9; ++i) A.R.m[i] = w[i];
+    A.t = ld3(w + 9);
+    Hull B;
+    B.verts = O.verts + 3 * (size_t)O.part_vbeg[part];
+    B.nv = O.part_vbeg[part + 1] - O.part_vbeg[part];
+    B.posed = false;
+    B.R = eye();
+    B.t = mk(0, 0, 0);
+    double scale = 1.0;
+    scale = fmax(scale, scale_of(mul(A.R, ld3(H.link_centroid + 3 * link)) + A.t, H.link_halfnorm[link]));
+    scale = fmax(scale, scale_of(ld3(O.part_centroid + 3 * part), O.part_halfnorm[part]));
+    const PairResult r = warp_signed_distance(A, B, scale, epa_smem[warp], lane);
+    if (lane == 0) {
+      store_pair(st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12, r);
+      if (st.ops) {
+        atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * (A.nv + B.nv));
+        atomicAdd(st.ops + kOpGjkIters, (unsigned long long)r.gjk_iters + 1);
+        atomicAdd(st.ops + kOpEpaIters, (unsigned long long)r.epa_iters);
+      }
+      if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
+      if (r.flags & kPairOverflow) {
+        const int slot = atomicAdd(st.ovf_count, 1);
+        if (slot < st.ovf_cap)
+          st.ovf_list[slot] = (int)((size_t)g * st.NP + link * O.P + part);
+        else
+          atomicAdd(st.err + 1, 1);
+      }
+    }
+    __syncwarp();
   }
 }
 

@@ -61,7 +61,12 @@ struct DevObject {
   const double* part_obb;       // [P*15] center, half, rotation (column-major)
   const double* part_sphere;    // [P*4] bounding sphere of the part: center, radius
   const double* face_sphere;    // [F*4] bounding sphere of each triangle: center, radius
+  const float4* face_sphere32;  // [F] same in fp32, radius rounded up (culling bounds only)
 };
+
+// Slack on the fp32 culling bounds: fp32 distances of <= 1 m carry < 1e-7 m
+// rounding error, so 1e-5 m keeps every bound conservative.
+constexpr float kCullSlack32 = 1e-5f;
 
 struct DevParams {
   double rho, sigma, alpha;

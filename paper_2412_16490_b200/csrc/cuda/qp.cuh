@@ -1,6 +1,17 @@
 // Lower-level QP kernel (separate translation unit, compiled with FMA
 // contraction; the geometry/kinematics kernels in kernels.cuh are compiled
 // without it so their discrete decisions match the fp64 oracle bit for bit).
+//
+// One warp = one grasp's batch of 6 closure-direction QPs (energy.cpp:60-92,
+// qpsolve.cpp:45-120, 193-235). Lane (j, c) = (direction j, contact c) owns
+// the K edge weights of contact c in column j, their identity rows and the
+// cap row c; the total-weight row is replicated in the M lanes of a column.
+// K = P + sigma I + rho A'A is B + U U^T with B block-diagonal (closed-form
+// inverse) and U = [sqrt2 W^T | sqrt(rho) 1] of rank 7, so
+//   K^-1 r = B^-1 r - Z (G^T r),  G = B^-1 U,  Z = G (I + U^T G)^-1,
+// i.e. each ADMM sweep is a handful of K-long dot products per lane plus
+// 8 fixed-order column reductions. Templated on (K, M) so every per-lane
+// array is register-resident; (0, 0) is the generic runtime-size fallback.
 #pragma once
 
 #include "dmath.cuh"
@@ -13,47 +24,50 @@ namespace gdev {
 constexpr unsigned kFull = 0xffffffffu;
 #endif
 
+// Fixed-order sum over lanes base..base+cnt-1 (identical on all lanes).
+template <int CNT>
 __device__ __forceinline__ double qp_group_sum(double v, int base, int cnt) {
   double s = 0.0;
-  for (int b = 0; b < cnt; ++b) s += __shfl_sync(kFull, v, base + b);
+  const int n = CNT > 0 ? CNT : cnt;
+#pragma unroll
+  for (int b = 0; b < (CNT > 0 ? CNT : kMaxTips); ++b)
+    if (b < n) s += __shfl_sync(kFull, v, base + b);
   return s;
 }
+template <int CNT>
 __device__ __forceinline__ double qp_group_max(double v, int base, int cnt) {
   double s = 0.0;
-  for (int b = 0; b < cnt; ++b) s = fmax(s, __shfl_sync(kFull, v, base + b));
+  const int n = CNT > 0 ? CNT : cnt;
+#pragma unroll
+  for (int b = 0; b < (CNT > 0 ? CNT : kMaxTips); ++b)
+    if (b < n) s = fmax(s, __shfl_sync(kFull, v, base + b));
   return s;
 }
 
-// --------------------------------------------------------------- the QP
-// Lower-level QP batch of one grasp (energy.cpp:60-92, qpsolve.cpp:45-120,
-// 193-235). Lane (j, c) = (closure direction j, contact block c) owns the
-// k edge weights of contact c in column j, the identity rows of those
-// weights and the contact-cap row c; the total-weight row is replicated in
-// the m lanes of a column. The K = P + sigma I + rho A'A solve uses the
-// structure K = B + U U^T (B block-diagonal, U = [sqrt2 W^T | sqrt(rho) 1],
-// rank 7) through Woodbury with a 7x7 capacitance inverse, so a sweep costs
-// O(k) per lane plus 8 fixed-order column reductions.
 struct QpSmem {
   double frame[kMaxTips * 12];
   double W[6 * kMaxTips * kMaxEdges];   // row-major 6 x n
   double Gm[kMaxTips * kMaxEdges * 7];  // B^-1 U, n x 7
-  double Hm[49];                        // (I + U^T B^-1 U)^-1
+  double Zm[kMaxTips * kMaxEdges * 7];  // G (I + U^T G)^-1, n x 7
   double C[49];
 };
-
 
 // mode 0: coarse (frames from the tip point queries, warm start from the
 // per-grasp scratch, envelope-gradient forces written when with_grad).
 // mode 1: final record (frames from st.frames, cold start).
 // mode 2: standalone batch (frames from st.frames, warm if qp_ready).
-__global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st, int m, int mode, int with_grad) {
+template <int KT, int MT>
+__global__ void __launch_bounds__(128) k_qp_t(DevHand H, DevParams P, DevState st, int m_rt, int mode, int with_grad) {
   __shared__ QpSmem smem_all[4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * 4 + warp;
   if (g >= st.G) return;
   if (st.failed[g]) return;
   QpSmem& s = smem_all[warp];
-  const int k = P.k, n = m * k, M = m + 1 + n;
+  constexpr int KMAX = KT > 0 ? KT : kMaxEdges;
+  const int k = KT > 0 ? KT : P.k;
+  const int m = MT > 0 ? MT : m_rt;
+  const int n = m * k, M = m + 1 + n;
 
   // Frames.
   if (lane < m) {
@@ -69,7 +83,7 @@ __global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st,
   const double a_diag = P.sigma + P.rho;
   const double betap = P.rho / (a_diag + k * P.rho);
   const double sqrt2 = 1.4142135623730951, sqrt_rho = sqrt(P.rho);
-  // Wrench basis block c (contact.cpp:47-53) and B^-1 U rows.
+  // Wrench basis block c (contact.cpp:47-53) and G = B^-1 U rows.
   if (lane < m) {
     const int c = lane;
     const D3 p = ld3(s.frame + 12 * c), nn = ld3(s.frame + 12 * c + 3);
@@ -113,34 +127,43 @@ __global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st,
     s.C[q * 7 + p] = v;
   }
   __syncwarp();
-  if (lane == 0) {
-    // Cholesky of C, then H = C^-1 column by column.
-    double L[49];
-    for (int i = 0; i < 49; ++i) L[i] = 0.0;
+  // Each lane inverts C redundantly (Cholesky, 7x7) and forms its Z rows.
+  {
+    double L[7][7];
+#pragma unroll
     for (int j = 0; j < 7; ++j) {
       double dsum = s.C[j * 7 + j];
-      for (int q = 0; q < j; ++q) dsum -= L[j * 7 + q] * L[j * 7 + q];
+#pragma unroll
+      for (int q = 0; q < j; ++q) dsum -= L[j][q] * L[j][q];
       const double ljj = sqrt(dsum);
-      L[j * 7 + j] = ljj;
+      L[j][j] = ljj;
+#pragma unroll
       for (int i = j + 1; i < 7; ++i) {
         double v = s.C[i * 7 + j];
-        for (int q = 0; q < j; ++q) v -= L[i * 7 + q] * L[j * 7 + q];
-        L[i * 7 + j] = v / ljj;
+#pragma unroll
+        for (int q = 0; q < j; ++q) v -= L[i][q] * L[j][q];
+        L[i][j] = v / ljj;
       }
     }
-    for (int cidx = 0; cidx < 7; ++cidx) {
+    // Z^T = C^-1 G^T: solve C z = g for each of this lane's rows of G.
+    for (int i = lane; i < n; i += 32) {
       double y[7];
-      for (int i = 0; i < 7; ++i) {
-        double v = i == cidx ? 1.0 : 0.0;
-        for (int q = 0; q < i; ++q) v -= L[i * 7 + q] * y[q];
-        y[i] = v / L[i * 7 + i];
+#pragma unroll
+      for (int r = 0; r < 7; ++r) {
+        double v = s.Gm[i * 7 + r];
+#pragma unroll
+        for (int q = 0; q < r; ++q) v -= L[r][q] * y[q];
+        y[r] = v / L[r][r];
       }
-      for (int i = 6; i >= 0; --i) {
-        double v = y[i];
-        for (int q = i + 1; q < 7; ++q) v -= L[q * 7 + i] * y[q];
-        y[i] = v / L[i * 7 + i];
+#pragma unroll
+      for (int r = 6; r >= 0; --r) {
+        double v = y[r];
+#pragma unroll
+        for (int q = r + 1; q < 7; ++q) v -= L[q][r] * y[q];
+        y[r] = v / L[r][r];
       }
-      for (int i = 0; i < 7; ++i) s.Hm[i * 7 + cidx] = y[i];
+#pragma unroll
+      for (int r = 0; r < 7; ++r) s.Zm[i * 7 + r] = y[r];
     }
   }
   __syncwarp();
@@ -154,14 +177,16 @@ __global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st,
   const double rho = P.rho, sigma = P.sigma, alpha = P.alpha;
   const double inv_a = 1.0 / a_diag;
   const double inv_rho = 1.0 / rho;
+  const double* Gl = s.Gm + c * k * 7;
+  const double* Zl = s.Zm + c * k * 7;
 
-  double x[kMaxEdges], zid[kMaxEdges], yid[kMaxEdges], q[kMaxEdges], xs[kMaxEdges];
+  double x[KMAX], zid[KMAX], yid[KMAX], q[KMAX], xs[KMAX];
   double zc, yc, ztot, ytot;
   const bool warm = (mode == 0 || mode == 2) && st.qp_ready[g];
   const double* wx = st.warm_x + (size_t)g * n * 6;
   const double* wy = st.warm_y + (size_t)g * M * 6;
 #pragma unroll
-  for (int e = 0; e < kMaxEdges; ++e) {
+  for (int e = 0; e < KMAX; ++e) {
     if (e < k) {
       const int i = c * k + e;
       x[e] = warm ? wx[j * n + i] : 0.0;
@@ -177,9 +202,11 @@ __global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st,
   ytot = warm ? wy[j * M + m] : 0.0;
   {
     double bs = 0.0;
-    for (int e = 0; e < k; ++e) bs += x[e];
+#pragma unroll
+    for (int e = 0; e < KMAX; ++e)
+      if (e < k) bs += x[e];
     zc = bs;
-    ztot = qp_group_sum(bs, base, m);
+    ztot = qp_group_sum<MT>(bs, base, m);
   }
   const double gamma = P.gamma_total;
   bool frozen = !active;
@@ -192,10 +219,10 @@ __global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st,
     sweeps = iter;
     // rhs = A'(rho z - y) + sigma x - q
     const double vc = rho * zc - yc, vt = rho * ztot - ytot;
-    double rhs[kMaxEdges];
+    double rhs[KMAX];
     double bsum = 0.0;
 #pragma unroll
-    for (int e = 0; e < kMaxEdges; ++e) {
+    for (int e = 0; e < KMAX; ++e) {
       if (e < k) {
         const double vi = rho * zid[e] - yid[e];
         rhs[e] = ((vc + vt) + vi) + (sigma * x[e] - q[e]);
@@ -204,41 +231,35 @@ __global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st,
         rhs[e] = 0.0;
       }
     }
-    // t = G^T rhs over the column, s = H t
+    // t = G^T rhs over the column
     double tv[7];
 #pragma unroll
     for (int p = 0; p < 7; ++p) {
       double acc = 0.0;
-      for (int e = 0; e < k; ++e) acc += s.Gm[(c * k + e) * 7 + p] * rhs[e];
-      tv[p] = qp_group_sum(acc, base, m);
-    }
-    double sv[7];
 #pragma unroll
-    for (int p = 0; p < 7; ++p) {
-      double acc = 0.0;
-#pragma unroll
-      for (int r = 0; r < 7; ++r) acc += s.Hm[p * 7 + r] * tv[r];
-      sv[p] = acc;
+      for (int e = 0; e < KMAX; ++e)
+        if (e < k) acc += Gl[e * 7 + p] * rhs[e];
+      tv[p] = qp_group_sum<MT>(acc, base, m);
     }
-    // xt = B^-1 rhs - G s ; zt = A xt
-    double xt[kMaxEdges];
+    // xt = B^-1 rhs - Z t ; zt = A xt
+    double xt[KMAX];
     double ztc = 0.0;
 #pragma unroll
-    for (int e = 0; e < kMaxEdges; ++e) {
+    for (int e = 0; e < KMAX; ++e) {
       if (e < k) {
-        double gs = 0.0;
+        double zs = 0.0;
 #pragma unroll
-        for (int p = 0; p < 7; ++p) gs += s.Gm[(c * k + e) * 7 + p] * sv[p];
-        xt[e] = (rhs[e] - betap * bsum) * inv_a - gs;
+        for (int p = 0; p < 7; ++p) zs += Zl[e * 7 + p] * tv[p];
+        xt[e] = (rhs[e] - betap * bsum) * inv_a - zs;
         ztc += xt[e];
       } else {
         xt[e] = 0.0;
       }
     }
-    const double ztt = qp_group_sum(ztc, base, m);
+    const double ztt = qp_group_sum<MT>(ztc, base, m);
     // Relaxed updates and projection.
 #pragma unroll
-    for (int e = 0; e < kMaxEdges; ++e) {
+    for (int e = 0; e < KMAX; ++e) {
       if (e < k) {
         x[e] = alpha * xt[e] + (1.0 - alpha) * x[e];
         const double zbar = alpha * xt[e] + (1.0 - alpha) * zid[e];
@@ -261,37 +282,49 @@ __global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st,
     }
     if (iter % P.check_interval == 0 || iter == P.max_iters) {
       double axc = 0.0;
-      for (int e = 0; e < k; ++e) axc += x[e];
-      const double axt = qp_group_sum(axc, base, m);
+#pragma unroll
+      for (int e = 0; e < KMAX; ++e)
+        if (e < k) axc += x[e];
+      const double axt = qp_group_sum<MT>(axc, base, m);
       double rp = fmax(fabs(axc - zc), fabs(axt - ztot));
-      for (int e = 0; e < k; ++e) rp = fmax(rp, fabs(x[e] - zid[e]));
-      rp = qp_group_max(rp, base, m);
+#pragma unroll
+      for (int e = 0; e < KMAX; ++e)
+        if (e < k) rp = fmax(rp, fabs(x[e] - zid[e]));
+      rp = qp_group_max<MT>(rp, base, m);
       double wx6[6];
 #pragma unroll
       for (int r = 0; r < 6; ++r) {
         double acc = 0.0;
-        for (int e = 0; e < k; ++e) acc += s.W[r * n + c * k + e] * x[e];
-        wx6[r] = qp_group_sum(acc, base, m);
+#pragma unroll
+        for (int e = 0; e < KMAX; ++e)
+          if (e < k) acc += s.W[r * n + c * k + e] * x[e];
+        wx6[r] = qp_group_sum<MT>(acc, base, m);
       }
       double rd = 0.0;
-      for (int e = 0; e < k; ++e) {
-        double px = 0.0;
 #pragma unroll
-        for (int r = 0; r < 6; ++r) px += s.W[r * n + c * k + e] * wx6[r];
-        const double dual = (2.0 * px + ((yc + ytot) + yid[e])) + q[e];
-        rd = fmax(rd, fabs(dual));
+      for (int e = 0; e < KMAX; ++e) {
+        if (e < k) {
+          double px = 0.0;
+#pragma unroll
+          for (int r = 0; r < 6; ++r) px += s.W[r * n + c * k + e] * wx6[r];
+          const double dual = (2.0 * px + ((yc + ytot) + yid[e])) + q[e];
+          rd = fmax(rd, fabs(dual));
+        }
       }
-      rd = qp_group_max(rd, base, m);
+      rd = qp_group_max<MT>(rd, base, m);
       if (!frozen) {
         const bool ok = rp <= P.eps_primal && rd <= P.eps_dual;
         if (ok || iter == P.max_iters) {
           frozen = true;
-          for (int e = 0; e < k; ++e) {
-            const int i = c * k + e;
-            xs[e] = x[e];
-            ox[j * n + i] = x[e];
-            oy[j * M + m + 1 + i] = yid[e];
-            oz[j * M + m + 1 + i] = zid[e];
+#pragma unroll
+          for (int e = 0; e < KMAX; ++e) {
+            if (e < k) {
+              const int i = c * k + e;
+              xs[e] = x[e];
+              ox[j * n + i] = x[e];
+              oy[j * M + m + 1 + i] = yid[e];
+              oz[j * M + m + 1 + i] = zid[e];
+            }
           }
           oy[j * M + c] = yc;
           oz[j * M + c] = zc;
@@ -319,8 +352,10 @@ __global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st,
 #pragma unroll
   for (int r = 0; r < 6; ++r) {
     double acc = 0.0;
-    for (int e = 0; e < k; ++e) acc += s.W[r * n + c * k + e] * xs[e];
-    const double wl = qp_group_sum(acc, base, m);
+#pragma unroll
+    for (int e = 0; e < KMAX; ++e)
+      if (e < k) acc += s.W[r * n + c * k + e] * xs[e];
+    const double wl = qp_group_sum<MT>(acc, base, m);
     res[r] = P.beta * (r == axis ? tsign : 0.0) - wl;
   }
   double pd = 0.0;
@@ -340,25 +375,27 @@ __global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st,
   const D3 rf = mk(res[0], res[1], res[2]), rt = mk(res[3], res[4], res[5]);
   double sum = 0.0, sum_cos = 0.0, sum_sin = 0.0;
   D3 fsum = mk(0, 0, 0);
-  for (int e = 0; e < k; ++e) {
-    sum += xs[e];
-    sum_cos += xs[e] * P.cos_t[e];
-    sum_sin += xs[e] * P.sin_t[e];
-    fsum += xs[e] * (nn + P.mu * (P.cos_t[e] * dd + P.sin_t[e] * ee));
+#pragma unroll
+  for (int e = 0; e < KMAX; ++e) {
+    if (e < k) {
+      sum += xs[e];
+      sum_cos += xs[e] * P.cos_t[e];
+      sum_sin += xs[e] * P.sin_t[e];
+      fsum += xs[e] * (nn + P.mu * (P.cos_t[e] * dd + P.sin_t[e] * ee));
+    }
   }
   const D3 gv = rf + cross(rt, p);
-  // md^T g with md = -(I - d d^T)[seed]x / cnorm  ->  md^T g = (seed x ((I - d d^T) g)) / cnorm
+  // md = -(I - d d^T)[seed]x / cnorm  ->  md^T g = seed x ((I - d d^T) g) / cnorm
   const D3 proj = gv - dd * dot(dd, gv);
   const D3 mdTg = cross(seed, proj) / cnorm;
-  // me = [n]x md - [d]x  ->  me^T g = md^T([n]x^T g) - [d]x^T g = md^T(g x n) + d x g ... expanded:
+  // me = [n]x md - [d]x  ->  me^T g = md^T (g x n) + d x g
   const D3 gxn = cross(gv, nn);
   const D3 proj2 = gxn - dd * dot(dd, gxn);
   const D3 meTg = cross(seed, proj2) / cnorm + cross(dd, gv);
   const D3 an = sum * gv + (P.mu * sum_cos) * mdTg + (P.mu * sum_sin) * meTg;
   const D3 ap = cross(fsum, rt);
   // Sum over the 6 directions of contact c, fixed order.
-  D3 AN = mk(0, 0, 0), AP;
-  AP = mk(0, 0, 0);
+  D3 AN = mk(0, 0, 0), AP = mk(0, 0, 0);
   for (int jj = 0; jj < 6; ++jj) {
     const int src = jj * m + c;
     AN.x += __shfl_sync(kFull, an.x, src);
@@ -371,8 +408,7 @@ __global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st,
   if (active && j == 0) {
     const double* qb = st.qres + (size_t)g * st.NQ * 8;
     const double h2 = 2.0 * P.fd_step;
-    D3 dpT_AP, dnT_AN;  // (dp^T AP)_k = dp.col(k) . AP
-    double vals_p[3], vals_n[3];
+    double vals_p[3], vals_n[3];  // (dp^T AP)_k = dp.col(k) . AP
     for (int kk = 0; kk < 3; ++kk) {
       const double* qp = qb + (size_t)(H.S + c * 6 + 2 * kk) * 8;
       const double* qm = qb + (size_t)(H.S + c * 6 + 2 * kk + 1) * 8;
@@ -381,12 +417,9 @@ __global__ void __launch_bounds__(128) k_qp(DevHand H, DevParams P, DevState st,
       vals_p[kk] = dot(dpc, AP);
       vals_n[kk] = dot(dnc, AN);
     }
-    dpT_AP = mk(vals_p[0], vals_p[1], vals_p[2]);
-    dnT_AN = mk(vals_n[0], vals_n[1], vals_n[2]);
-    const D3 F = (-2.0 * P.w_grasp) * (dpT_AP - dnT_AN);
+    const D3 F = (-2.0 * P.w_grasp) * (mk(vals_p[0], vals_p[1], vals_p[2]) - mk(vals_n[0], vals_n[1], vals_n[2]));
     st3(st.qp_force + ((size_t)g * m + c) * 3, F);
   }
 }
-
 
 }  // namespace gdev

@@ -1,0 +1,21 @@
+"""Short synthesis run for ncu captures (dev tool): Shadow-like + drill,
+batch 1024, 20/10/10 iterations."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_2412_16490_b200 as G  # noqa: E402
+
+ROOT = Path(__file__).resolve().parent.parent
+hand = G.HandModel.from_file(ROOT / "paper_2412_16490_b200/assets/hands/shadow_like.json")
+obj = G.load_object(ROOT / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+cfg = G.RunConfig()
+cfg.seed = 17
+batch = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+cfg.batch = batch
+cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 20, 10, 10
+eng = G.Engine(0)
+eng.set_hand(hand)
+eng.set_object(obj)
+out = eng.synthesize(cfg, G.init_poses(hand, obj, batch, 17))
+print("ok failed", int((out.failed != 0).sum()))
