@@ -216,12 +216,13 @@ int grasp_fine_contact_query(grasp_ctx* ctx, int n, const double* x, double* out
 void* grasp_ctx_stream(grasp_ctx* ctx);
 /* Enables per-kernel-class CUDA-event timing and algorithmic op counters;
  * resets the accumulators. Classes: 0 point_query, 1 qp, 2 step_coarse,
- * 3 pairs, 4 step_mesh, 5 fk, 6 finalize. Ops: 0 plane tests, 1 triangle
- * tests, 2 ADMM column-sweeps, 3 QP solves, 4 GJK iterations, 5 support
- * vertices scanned, 6 EPA iterations, 7 point queries. */
+ * 3 pairs, 4 step_mesh, 5 fk, 6 finalize, 7 pairs_big. Ops: 0 plane tests,
+ * 1 triangle tests, 2 ADMM column-sweeps, 3 QP solves, 4 GJK iterations,
+ * 5 support vertices scanned, 6 EPA iterations, 7 point queries, 8 pairs
+ * not culled, 9 EPA overflows. */
 int grasp_ctx_set_profiling(grasp_ctx* ctx, int on);
-int grasp_ctx_profile(grasp_ctx* ctx, double* ms /*[7]*/, long long* launches /*[7]*/,
-                      unsigned long long* ops /*[8]*/);
+int grasp_ctx_profile(grasp_ctx* ctx, double* ms /*[8]*/, long long* launches /*[8]*/,
+                      unsigned long long* ops /*[10]*/);
 /* Kernels launched by this context so far. */
 long long grasp_ctx_launch_count(grasp_ctx* ctx);
 /* Measured dense fp64 FMA throughput of the device (TFLOP/s). */

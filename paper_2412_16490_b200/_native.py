@@ -11,7 +11,7 @@ import os
 from pathlib import Path
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
-LIB_PATH = LIB_DIR / "libgrasp_b200.so"
+LIB_PATH = Path(os.environ.get("GRASP_LIB", str(LIB_DIR / "libgrasp_b200.so")))
 
 GRASP_OK = 0
 GRASP_EINVAL = 1

@@ -460,14 +460,14 @@ class Engine:
     def set_profiling(self, on: bool) -> None:
         N.check(N.lib().grasp_ctx_set_profiling(self._ctx, int(bool(on))))
 
-    KERNEL_CLASSES = ("point_query", "qp", "step_coarse", "pairs", "step_mesh", "fk", "finalize")
+    KERNEL_CLASSES = ("point_query", "qp", "step_coarse", "pairs", "step_mesh", "fk", "finalize", "pairs_big")
     OP_NAMES = ("plane_tests", "triangle_tests", "qp_column_sweeps", "qp_solves", "gjk_iters", "support_verts",
-                "epa_iters", "point_queries")
+                "epa_iters", "point_queries", "pairs_needed", "epa_overflow")
 
     def profile(self) -> dict:
-        ms = (C.c_double * 7)()
-        launches = (C.c_longlong * 7)()
-        ops = (C.c_ulonglong * 8)()
+        ms = (C.c_double * 8)()
+        launches = (C.c_longlong * 8)()
+        ops = (C.c_ulonglong * 10)()
         N.check(N.lib().grasp_ctx_profile(self._ctx, ms, launches, ops))
         return {"ms": dict(zip(self.KERNEL_CLASSES, list(ms))),
                 "launches": dict(zip(self.KERNEL_CLASSES, list(launches))),

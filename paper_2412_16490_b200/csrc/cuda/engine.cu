@@ -114,15 +114,20 @@ struct grasp_ctx {
   DevBuf<int> qp_iters, qp_conv, qp_ready, failed, have_pregrasp, err, ovf_count, ovf_list;
   DevBuf<EpaScratchBig> big_scratch;
   static constexpr int kBigSlots = 1024;
-  // Pair kernel variant (GRASP_PAIRS=thread|warp, default thread).
+  // Pair kernel variant (GRASP_PAIRS=list|warp|thread, default list).
   int pairs_variant = [] {
     const char* v = std::getenv("GRASP_PAIRS");
-    return v && std::string(v) == "warp" ? 1 : 0;
+    if (v && std::string(v) == "warp") return 1;
+    if (v && std::string(v) == "thread") return 2;
+    return 0;
   }();
+  DevBuf<int> pair_count, pair_list;
+  DevBuf<double> epa_jobs;
 
   // Instrumentation: launch counts always; per-class CUDA-event time and
   // algorithmic op counters only while profiling.
-  static constexpr int kClasses = 7;  // point_query, qp, step_coarse, pairs, step_mesh, fk, finalize
+  // point_query, qp, step_coarse, pairs, step_mesh, fk, finalize, pairs_big
+  static constexpr int kClasses = 8;
   long long launches[kClasses] = {};
   bool profiling = false;
   double prof_ms[kClasses] = {};
@@ -439,6 +444,17 @@ struct grasp_ctx {
     st.ovf_cap = static_cast<int>(g * NP);
     st.big_scratch = big_scratch.p;
     st.big_slots = kBigSlots;
+    pair_count.ensure(2);
+    pair_list.ensure(g * NP);
+    st.pair_count = pair_count.p;
+    st.pair_list = pair_list.p;
+    // EPA jobs: up to a quarter of all pair slots at once; beyond that the
+    // pair is redone by k_pairs_big (never observed).
+    const size_t epa_cap = std::max<size_t>(1024, g * NP / 4);
+    epa_jobs.ensure(epa_cap * kEpaJobStride);
+    st.epa_count = pair_count.p + 1;
+    st.epa_jobs = epa_jobs.p;
+    st.epa_cap = static_cast<int>(epa_cap);
     st.G = G;
     st.NQ = NQ;
     st.NP = NP;
@@ -526,12 +542,19 @@ struct grasp_ctx {
     const long long n = static_cast<long long>(st.G) * nl * O.P;
     launch(3, [&] {
       ck(cudaMemsetAsync(ovf_count.p, 0, sizeof(int), stream), "memset");
-      if (pairs_variant == 1)
-        k_pairs_warp<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, tips_only ? h_tip_links_sorted.p : nullptr, nl);
-      else
-        k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, tips_only ? h_tip_links_sorted.p : nullptr, nl);
-      k_pairs_big<<<kBigSlots / 128, 128, 0, stream>>>(H, O, st);
+      const int* lk = tips_only ? h_tip_links_sorted.p : nullptr;
+      if (pairs_variant == 1) {
+        k_pairs_warp<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
+      } else if (pairs_variant == 2) {
+        k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
+      } else {
+        ck(cudaMemsetAsync(pair_count.p, 0, 2 * sizeof(int), stream), "memset");  // pair_count, epa_count
+        k_pairs_cull<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
+        k_pairs_list<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
+        k_pairs_epa<<<blocks(std::min<long long>(n, st.epa_cap), 128), 128, 0, stream>>>(H, O, st);
+      }
     });
+    launch(7, [&] { k_pairs_big<<<kBigSlots / 128, 128, 0, stream>>>(H, O, st); });
   }
   void launch_qp(const DevParams& P, int m, int mode, int with_grad) {
     launch(1, [&] { launch_qp_kernel(H, P, st, m, mode, with_grad, stream); });

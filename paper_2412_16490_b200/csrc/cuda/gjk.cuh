@@ -340,8 +340,8 @@ struct EpaDebug {
 };
 
 template <class Scratch>
-GDEV_INL bool epa(SP* simp, int ns, const Hull& A, const Hull& B, double scale, Scratch& s, PairResult& out,
-                  EpaDebug* dbg = nullptr) {
+GDEV_FN bool epa(const SP (&simp)[4], int ns, const Hull& A, const Hull& B, double scale, Scratch& s,
+                 PairResult& out, EpaDebug* dbg = nullptr) {
   constexpr int kEpaMaxVerts = Scratch::kV, kEpaMaxFaces = Scratch::kF, kEpaMaxHorizon = Scratch::kH;
   // pad_to_tetrahedron
   const double tol = 1e-12 * scale;
@@ -368,7 +368,9 @@ GDEV_INL bool epa(SP* simp, int ns, const Hull& A, const Hull& B, double scale, 
   dirs[nd++] = mk(0, -1, 0);
   dirs[nd++] = mk(0, 0, 1);
   dirs[nd++] = mk(0, 0, -1);
-  for (int i = 0; i < ns; ++i) s.verts[i] = simp[i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < ns) s.verts[i] = simp[i];
   int nv = ns;
   for (int k = 0; k < nd && nv < 4; ++k) {
     const SP cand = support_pair(A, B, dirs[k]);
@@ -502,27 +504,36 @@ GDEV_INL bool epa(SP* simp, int ns, const Hull& A, const Hull& B, double scale, 
   return true;
 }
 
-// signed_distance(a, pose_a, b, identity) (geometry.cpp:500-525).
-template <class Scratch>
-GDEV_INL PairResult signed_distance(const Hull& A, const Hull& B, double scale, Scratch& scratch,
-                                    EpaDebug* dbg = nullptr) {
-  PairResult out;
+// GJK part of signed_distance (geometry.cpp:105-164, 500-516). Returns true
+// on overlap, leaving the terminal simplex (the EPA seed) in simp/ns;
+// otherwise `out` holds the separated result.
+GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& out, SP (&simp)[4], int& ns) {
   out.flags = 0;
   out.n_support = 1;
   out.gjk_iters = 0;
   out.epa_iters = 0;
-  SP simp[4];
-  int ns = 1;
+  // The simplex is only ever indexed by compile-time constants (unrolled
+  // loops with predicates) so it stays in registers.
+  ns = 1;
   simp[0] = support_pair(A, B, mk(1, 0, 0));
+  simp[1] = simp[2] = simp[3] = simp[0];
   bool done = false;
   bool overlap = false;
   Simplex sx;
   for (int iter = 0; iter < kGjkMaxIters && !done; ++iter) {
     sx = closest_on_simplex(simp, ns);
     SP red[4];
-    for (int i = 0; i < sx.nkeep; ++i) red[i] = simp[sx.keep[i]];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int src = sx.keep[i];
+      red[i] = simp[0];
+      if (src == 1) red[i] = simp[1];
+      if (src == 2) red[i] = simp[2];
+      if (src == 3) red[i] = simp[3];
+    }
     ns = sx.nkeep;
-    for (int i = 0; i < ns; ++i) simp[i] = red[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) simp[i] = red[i];
     if (sx.contains || sqrt(sx.dist2) < kTouchTol * scale) {
       overlap = true;
       done = true;
@@ -533,43 +544,68 @@ GDEV_INL PairResult signed_distance(const Hull& A, const Hull& B, double scale, 
     ++out.gjk_iters;
     const double gap = sx.dist2 - dot(sx.v, w.w);
     bool repeat = false;
-    for (int i = 0; i < ns; ++i)
-      if (nrm(simp[i].w - w.w) < 1e-14 * scale) repeat = true;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < ns && nrm(simp[i].w - w.w) < 1e-14 * scale) repeat = true;
     if (gap <= kGjkRelTol * sx.dist2 + 1e-300 || repeat || ns == 4) {
       done = true;
       break;
     }
-    simp[ns++] = w;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i == ns) simp[i] = w;
+    ++ns;
   }
   if (!done) {
     // Iteration cap: current estimate from the unreduced simplex.
     sx = closest_on_simplex(simp, ns);
     D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
-    for (int i = 0; i < sx.nkeep; ++i) {
-      wa += sx.wts[i] * simp[sx.keep[i]].a;
-      wb += sx.wts[i] * simp[sx.keep[i]].b;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (i < sx.nkeep) {
+        const int src = sx.keep[i];
+        SP p = simp[0];
+        if (src == 1) p = simp[1];
+        if (src == 2) p = simp[2];
+        if (src == 3) p = simp[3];
+        wa += sx.wts[i] * p.a;
+        wb += sx.wts[i] * p.b;
+      }
     }
     const double d = sqrt(sx.dist2);
     out.d = d;
     out.pa = wa;
     out.pb = wb;
     out.n = d > 1e-14 ? (wa - wb) / d : mk(0, 0, 1);
-    return out;
+    return false;
   }
   if (!overlap) {
     D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
-    for (int i = 0; i < ns; ++i) {
-      wa += sx.wts[i] * simp[i].a;
-      wb += sx.wts[i] * simp[i].b;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (i < ns) {
+        wa += sx.wts[i] * simp[i].a;
+        wb += sx.wts[i] * simp[i].b;
+      }
     }
     const double d = sqrt(sx.dist2);
     out.d = d;
     out.pa = wa;
     out.pb = wb;
     out.n = d > 1e-14 ? (wa - wb) / d : mk(0, 0, 1);
-    return out;
+    return false;
   }
-  epa(simp, ns, A, B, scale, scratch, out, dbg);
+  return true;
+}
+
+// signed_distance(a, pose_a, b, identity) (geometry.cpp:500-525).
+template <class Scratch>
+GDEV_INL PairResult signed_distance(const Hull& A, const Hull& B, double scale, Scratch& scratch,
+                                    EpaDebug* dbg = nullptr) {
+  PairResult out;
+  SP simp[4];
+  int ns;
+  if (gjk_phase(A, B, scale, out, simp, ns)) epa(simp, ns, A, B, scale, scratch, out, dbg);
   return out;
 }
 

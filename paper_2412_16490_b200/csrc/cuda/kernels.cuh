@@ -435,6 +435,8 @@ __global__ void __launch_bounds__(128) k_pairs(DevHand H, DevObject O, DevState 
     atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * nv);
     atomicAdd(st.ops + kOpGjkIters, (unsigned long long)r.gjk_iters + 1);
     atomicAdd(st.ops + kOpEpaIters, (unsigned long long)r.epa_iters);
+    atomicAdd(st.ops + kOpPairsNeeded, 1ull);
+    if (r.flags & kPairOverflow) atomicAdd(st.ops + kOpEpaOverflow, 1ull);
   }
   if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
   if (r.flags & kPairOverflow) {
@@ -445,6 +447,148 @@ __global__ void __launch_bounds__(128) k_pairs(DevHand H, DevObject O, DevState 
     else
       atomicAdd(st.err + 1, 1);
   }
+}
+
+// Compacted pair evaluation, pass 1: one thread per (grasp, link, part)
+// slot runs the cull test; culled slots get their (+inf) result directly,
+// the rest are appended to st.pair_list with one atomic per warp (lane order
+// kept, so list neighbours share (link, part) and read the same vertices).
+__global__ void __launch_bounds__(128) k_pairs_cull(DevHand H, DevObject O, DevState st,
+                                                    const int* __restrict__ links, int n_links) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  bool need = false;
+  int slot = 0;
+  if (t < (long long)st.G * n_links * O.P) {
+    const int g = (int)(t % st.G);
+    const int lp = (int)(t / st.G);
+    const int link = links ? links[lp / O.P] : lp / O.P;
+    const int part = lp % O.P;
+    slot = (int)((size_t)g * st.NP + link * O.P + part);
+    if (!st.failed[g]) {
+      const double* w = st.world + ((size_t)g * H.L + link) * 12;
+      M33 Rw;
+      for (int i = 0; i < 9; ++i) Rw.m[i] = w[i];
+      need = pair_needed(H, O, st, g, link, part, Rw, ld3(w + 9));
+      if (!need) {
+        double* o = st.pairs + (size_t)slot * 12;
+        o[0] = INFINITY;
+        o[10] = kPairCulled;
+      }
+    }
+  }
+  const unsigned mask = __ballot_sync(kFull, need);
+  if (!mask) return;
+  int base = 0;
+  if (lane == 0) base = atomicAdd(st.pair_count, __popc(mask));
+  base = __shfl_sync(kFull, base, 0);
+  if (need) st.pair_list[base + __popc(mask & ((1u << lane) - 1))] = slot;
+}
+
+// Hulls and cloud_scale (geometry.cpp:17-23) of a pair slot.
+__device__ __forceinline__ void slot_hulls(const DevHand& H, const DevObject& O, const DevState& st, int slot, Hull& A,
+                                           Hull& B, double& scale) {
+  const int g = slot / st.NP, lp = slot % st.NP;
+  const int link = lp / O.P, part = lp % O.P;
+  const double* w = st.world + ((size_t)g * H.L + link) * 12;
+  A.verts = H.link_verts + 3 * (size_t)H.link_vbeg[link];
+  A.nv = H.link_vbeg[link + 1] - H.link_vbeg[link];
+  A.posed = true;
+  for (int k = 0; k < 9; ++k) A.R.m[k] = w[k];
+  A.t = ld3(w + 9);
+  B.verts = O.verts + 3 * (size_t)O.part_vbeg[part];
+  B.nv = O.part_vbeg[part + 1] - O.part_vbeg[part];
+  B.posed = false;
+  B.R = eye();
+  B.t = mk(0, 0, 0);
+  scale = 1.0;
+  scale = fmax(scale, scale_of(mul(A.R, ld3(H.link_centroid + 3 * link)) + A.t, H.link_halfnorm[link]));
+  scale = fmax(scale, scale_of(ld3(O.part_centroid + 3 * part), O.part_halfnorm[part]));
+}
+
+__device__ __forceinline__ void queue_overflow(const DevState& st, int slot) {
+  const int o = atomicAdd(st.ovf_count, 1);
+  if (o < st.ovf_cap)
+    st.ovf_list[o] = slot;
+  else
+    atomicAdd(st.err + 1, 1);
+}
+
+// Pass 2: GJK, one thread per listed pair (dense warps, register simplex,
+// no EPA buffer). Overlapping pairs pass their terminal simplex to k_pairs_epa.
+#ifndef GDEV_PAIRS_MIN_BLOCKS
+#define GDEV_PAIRS_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHand H, DevObject O, DevState st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *st.pair_count) return;
+  const int slot = st.pair_list[i];
+  Hull A, B;
+  double scale;
+  slot_hulls(H, O, st, slot, A, B, scale);
+  PairResult r;
+  SP simp[4];
+  int ns;
+  const bool overlap = gjk_phase(A, B, scale, r, simp, ns);
+  if (st.ops) {
+    atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * (A.nv + B.nv));
+    atomicAdd(st.ops + kOpGjkIters, (unsigned long long)r.gjk_iters + 1);
+    atomicAdd(st.ops + kOpPairsNeeded, 1ull);
+  }
+  if (!overlap) {
+    store_pair(st.pairs + (size_t)slot * 12, r);
+    return;
+  }
+  const int job = atomicAdd(st.epa_count, 1);
+  if (job >= st.epa_cap) {
+    queue_overflow(st, slot);
+    return;
+  }
+  double* jb = st.epa_jobs + (size_t)job * kEpaJobStride;
+  jb[0] = slot;
+  jb[1] = ns;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    st3(jb + 2 + 9 * k, simp[k].w);
+    st3(jb + 5 + 9 * k, simp[k].a);
+    st3(jb + 8 + 9 * k, simp[k].b);
+  }
+}
+
+// Pass 3: EPA for the overlapping pairs (geometry.cpp:227-324).
+__global__ void __launch_bounds__(128) k_pairs_epa(DevHand H, DevObject O, DevState st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= min(*st.epa_count, st.epa_cap)) return;
+  const double* jb = st.epa_jobs + (size_t)i * kEpaJobStride;
+  const int slot = (int)jb[0], ns = (int)jb[1];
+  SP simp[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    simp[k].w = ld3(jb + 2 + 9 * k);
+    simp[k].a = ld3(jb + 5 + 9 * k);
+    simp[k].b = ld3(jb + 8 + 9 * k);
+  }
+  Hull A, B;
+  double scale;
+  slot_hulls(H, O, st, slot, A, B, scale);
+  PairResult r;
+  r.flags = 0;
+  r.n_support = 0;
+  r.gjk_iters = 0;
+  r.epa_iters = 0;
+  EpaScratch scratch;
+  epa(simp, ns, A, B, scale, scratch, r);
+  if (st.ops) {
+    atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * (A.nv + B.nv));
+    atomicAdd(st.ops + kOpEpaIters, (unsigned long long)r.epa_iters);
+    if (r.flags & kPairOverflow) atomicAdd(st.ops + kOpEpaOverflow, 1ull);
+  }
+  if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
+  if (r.flags & kPairOverflow) {
+    queue_overflow(st, slot);
+    return;
+  }
+  store_pair(st.pairs + (size_t)slot * 12, r);
 }
 
 // Warp-cooperative variant: each warp takes 32 consecutive pair slots, every

@@ -127,7 +127,14 @@ struct DevState {
   int ovf_cap;
   void* big_scratch;   // [big_slots] EpaScratchBig in global memory
   int big_slots;
+  int* pair_count;     // compacted list of pair slots that need GJK
+  int* pair_list;      // [G*NP]
+  int* epa_count;      // overlapping pairs handed from GJK to the EPA kernel
+  double* epa_jobs;    // [epa_cap * kEpaJobStride]: slot, ns, 4 x (w, a, b)
+  int epa_cap;
 };
+
+constexpr int kEpaJobStride = 40;
 
 // Op counters (profiling mode) for the roofline's algorithmic flop count
 // (SURVEY.md 8(d) constants are applied on the host).
@@ -140,7 +147,9 @@ enum OpCounter {
   kOpSupportVerts = 5,   // vertices scanned by support (GJK + EPA)
   kOpEpaIters = 6,
   kOpPointQueries = 7,
-  kNumOps = 8
+  kOpPairsNeeded = 8,    // (link, part) pairs that needed GJK (not culled)
+  kOpEpaOverflow = 9,    // pairs redone with the large EPA buffer
+  kNumOps = 10
 };
 
 }  // namespace gdev
