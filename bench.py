@@ -222,9 +222,9 @@ def run_ours(args):
     B, D, m = args.batch, hand.dims(), hand.n_tips
     n = m * cfg.contact.n_edges
 
-    # One global init_poses stream; this rank's contiguous shard.
-    x0_all = G.init_poses(hand, obj, B * world, SEED, cfg.init)
-    x0_host = np.ascontiguousarray(x0_all[rank * B:(rank + 1) * B])
+    # One global init_poses stream; this rank's contiguous shard (dist.py).
+    from paper_2412_16490_b200.dist import shard_start_states, synthesize_sharded
+    x0_host = shard_start_states(hand, obj, cfg, rank, world)
     import dataclasses
     shard_cfg = dataclasses.replace(cfg, batch=B)
 
@@ -286,22 +286,28 @@ def run_ours(args):
     ms_max = float(ms_t.item())
     value = B * world / (ms_max * 1e-3)
 
-    # ---- end-to-end through the C ABI with host buffers (value e2e)
+    # ---- end-to-end through the C ABI with host buffers (value e2e):
+    # init_poses (global stream, this rank's slice) + grasp_synthesize with
+    # host buffers + (N > 1) one all_gather of every record field.
+    import ctypes as C
     host_out = G.SynthesisOutput(B, D, m, cfg.contact.n_edges)
-    gather = [torch.empty(B, D, dtype=torch.float64, device=dev) for _ in range(world)] if world > 1 else None
+
+    def run_shard(x0_shard):
+        s = host_out.as_struct()
+        N.check(N.lib().grasp_synthesize(eng._ctx, C.byref(shard_cfg.to_params()), B,
+                                         np.ascontiguousarray(x0_shard).ctypes.data_as(C.POINTER(C.c_double)),
+                                         C.byref(s)))
+        return host_out
+
     e2e_times = []
     for _ in range(max(1, args.steps)):
         barrier()
         t0 = time.perf_counter()
-        x0_e2e = G.init_poses(hand, obj, B * world, SEED, cfg.init)[rank * B:(rank + 1) * B]
-        s = host_out.as_struct()
-        import ctypes as C
-        N.check(N.lib().grasp_synthesize(eng._ctx, C.byref(shard_cfg.to_params()), B,
-                                         np.ascontiguousarray(x0_e2e).ctypes.data_as(C.POINTER(C.c_double)),
-                                         C.byref(s)))
         if world > 1:
-            dist.all_gather(gather, torch.from_numpy(host_out.x).to(dev))
+            synthesize_sharded(hand, obj, cfg, rank, world, run_shard, device=dev)
             torch.cuda.synchronize(dev)
+        else:
+            run_shard(shard_start_states(hand, obj, cfg, rank, world))
         e2e_times.append(time.perf_counter() - t0)
     e2e_t = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -338,7 +344,7 @@ def run_ours(args):
             "e2e": {"value": round(e2e_value, 3), "unit": "grasps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": "init_poses + grasp_synthesize (C ABI, host buffers)" + (
-                        " + NCCL all_gather of x to every rank" if world > 1 else "")},
+                        " + NCCL all_gather of every record field" if world > 1 else "")},
             "gpu_launches": launches,
             "clocks": clk,
             "failed_grasps": failed,
