@@ -266,3 +266,88 @@ def test_synthesize_short_schedule_matches_oracle(G, O, trident, engine):
     # Mesh-stage energies are ~1e-2; the 1e-5-level pose differences above
     # move them by ~1e-5 absolute.
     np.testing.assert_allclose(gpu.stage_energy, cpu.stage_energy, rtol=1e-4, atol=1e-4)
+
+
+# ----------------------------------------------------------- KATs on device
+BOX_HAND = """{"format_version": 1, "name": "box", "links": [{"name": "box", "vertices":
+ [[-0.5,-0.5,-0.5],[-0.5,-0.5,0.5],[-0.5,0.5,-0.5],[-0.5,0.5,0.5],[0.5,-0.5,-0.5],[0.5,-0.5,0.5],[0.5,0.5,-0.5],
+  [0.5,0.5,0.5]], "proxies": [{"center": [0,0,0], "radius": 0.5}], "tip_proxy": 0}]}"""
+
+
+@pytest.mark.parametrize("p,d,pb", [((0.9, 0.1, 0.05), 0.4, (0.5, 0.1, 0.05)),
+                                    ((0.8, 0.7, 0.0), 0.42426406871192851, (0.5, 0.4, 0.0)),
+                                    ((1.5, 1.4, 1.3), 1.7320508075688772, (0.5, 0.4, 0.3)),
+                                    ((0.1, 0.0, 0.2), -0.1, (0.1, 0.0, 0.3))])
+def test_point_query_box_kats_on_device(G, trident, engine, p, d, pb):
+    # test_geometry.cpp:274-305 on the sm_100a kernel.
+    box = G.ObjectModel.from_points([np.array([(sx * 0.5, sy * 0.4, sz * 0.3) for sx in (-1, 1) for sy in (-1, 1)
+                                               for sz in (-1, 1)])])
+    use(engine, trident, box)
+    r = gpu_points(engine, [p])[0]
+    assert r[0] == pytest.approx(d, abs=1e-12)
+    np.testing.assert_allclose(r[1:4], pb, atol=1e-12)
+
+
+def test_gjk_epa_box_kats_on_device(G, engine):
+    # test_geometry.cpp:147-167, 215-247 (link = unit box, object = unit box).
+    hand = G.HandModel.from_json(BOX_HAND)
+    box = G.ObjectModel.from_points([np.array([(sx * 0.5, sy * 0.5, sz * 0.5) for sx in (-1, 1) for sy in (-1, 1)
+                                               for sz in (-1, 1)])])
+    use(engine, hand, box)
+    shifts = [1.0 + g for g in (1e-6, 0.01, 0.3, 2.0)] + [1.0 - d for d in (0.05, 0.2, 0.45)] + [0.0]
+    poses = np.zeros((len(shifts), 12))
+    poses[:, [0, 4, 8]] = 1.0
+    poses[:, 9] = -np.array(shifts)  # move the link so the object sits at +shift
+    r = gpu_pairs(engine, np.zeros(len(shifts)), np.zeros(len(shifts)), poses)
+    for i, g in enumerate((1e-6, 0.01, 0.3, 2.0)):
+        assert r[i, 0] == pytest.approx(g, rel=1e-10)
+    for i, dep in enumerate((0.05, 0.2, 0.45)):
+        assert r[4 + i, 0] == pytest.approx(-dep, rel=1e-9)
+        np.testing.assert_allclose(r[4 + i, 7:10], (-1, 0, 0), atol=1e-9)
+    assert r[7, 0] == pytest.approx(-1.0, rel=1e-9)  # concentric: depth 1, deterministic
+
+
+def test_energy_kats_on_device(G, engine):
+    # test_energy.cpp:152-217 through grasp_qp_batch.
+    def frame(p, n):
+        n = np.asarray(n, float)
+        seed = np.array([0.0, 1.0, 0.0]) if abs(n[0]) > 0.99 else np.array([1.0, 0.0, 0.0])
+        d = np.cross(n, seed)
+        d /= np.linalg.norm(d)
+        return np.concatenate([p, n, d, np.cross(n, d)])
+
+    def tight(beta, gamma):
+        cfg = G.RunConfig()
+        cfg.qp.eps_primal = cfg.qp.eps_dual = 1e-9
+        cfg.qp.max_iters = 200000
+        cfg.energy.beta, cfg.energy.gamma_per_contact = beta, gamma
+        return cfg
+
+    pair = np.array([[frame((1.0, 0, 0), (-1, 0, 0)), frame((-1.0, 0, 0), (1, 0, 0))]])
+    for gamma in (0.0, 0.1):
+        r = gpu_qp(engine, tight(0.8, gamma), pair, 2)
+        assert r["converged"].all() and r["per_direction"].sum() <= 1e-6
+    one = np.array([[frame((0.3, 0, 0), (-1, 0, 0))]])
+    r = gpu_qp(engine, tight(0.0, 0.1), one, 1)
+    np.testing.assert_allclose(r["per_direction"][0], 0.01, rtol=1e-4)
+
+
+# --------------------------------------------------- full schedule, statistics
+def test_full_schedule_matches_oracle_statistics(G, O, trident, engine):
+    """Default 300/100/100 schedule: per-grasp trajectories stay within
+    rounding of the oracle for most grasps; where ties or QP convergence
+    timing let them drift, the batch statistics (failure flags, final grasp
+    energy distribution, fine-stage energy) still agree."""
+    obj = G.make_primitive("sphere", 0.1)
+    use(engine, trident, obj)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 24, 17
+    x0 = G.init_poses(trident, obj, cfg.batch, cfg.seed, cfg.init)
+    gpu = engine.synthesize(cfg, x0)
+    cpu = O.synthesize(trident, obj, cfg, x0, workers=8)
+    assert (gpu.failed == cpu.failed).all()
+    close = np.abs(gpu.x - cpu.x).max(axis=1) <= 1e-4
+    assert close.mean() >= 0.75, close
+    ok = cpu.failed == 0
+    for a, b in ((gpu.energy_total[ok], cpu.energy_total[ok]), (gpu.stage_energy[ok, 1, 1], cpu.stage_energy[ok, 1, 1])):
+        assert abs(np.median(a) - np.median(b)) <= 0.05 * abs(np.median(b)) + 1e-3
