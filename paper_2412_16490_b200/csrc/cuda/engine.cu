@@ -121,7 +121,8 @@ struct grasp_ctx {
     if (v && std::string(v) == "thread") return 2;
     return 0;
   }();
-  DevBuf<int> pair_count, pair_list;
+  DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
+  DevBuf<unsigned char> pair_need;
   DevBuf<double> epa_jobs;
 
   // Instrumentation: launch counts always; per-class CUDA-event time and
@@ -448,6 +449,12 @@ struct grasp_ctx {
     pair_list.ensure(g * NP);
     st.pair_count = pair_count.p;
     st.pair_list = pair_list.p;
+    pair_need.ensure(g * NP);
+    seg_count.ensure(NP);
+    seg_offset.ensure(NP);
+    st.pair_need = pair_need.p;
+    st.seg_count = seg_count.p;
+    st.seg_offset = seg_offset.p;
     // EPA jobs: up to a quarter of all pair slots at once; beyond that the
     // pair is redone by k_pairs_big (never observed).
     const size_t epa_cap = std::max<size_t>(1024, g * NP / 4);
@@ -549,7 +556,10 @@ struct grasp_ctx {
         k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
       } else {
         ck(cudaMemsetAsync(pair_count.p, 0, 2 * sizeof(int), stream), "memset");  // pair_count, epa_count
+        ck(cudaMemsetAsync(seg_count.p, 0, sizeof(int) * nl * O.P, stream), "memset");
         k_pairs_cull<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
+        k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.P);
+        k_pairs_scatter<<<blocks(n, 128), 128, 0, stream>>>(st, lk, nl, O.P);
         k_pairs_list<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
         k_pairs_epa<<<blocks(std::min<long long>(n, st.epa_cap), 128), 128, 0, stream>>>(H, O, st);
       }

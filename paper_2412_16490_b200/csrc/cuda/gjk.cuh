@@ -38,8 +38,22 @@ GDEV_FN D3 support(const Hull& h, D3 dir) {
   const D3 dl = h.posed ? mulT(h.R, dir) : dir;
   double best = -INFINITY;
   int arg = 0;
-  for (int i = 0; i < h.nv; ++i) {
-    const double s = dl.x * GDEV_LDG(h.verts + 3 * i) + dl.y * GDEV_LDG(h.verts + 3 * i + 1) + dl.z * GDEV_LDG(h.verts + 3 * i + 2);
+  const double* __restrict__ V = h.verts;
+  int i = 0;
+  // Four independent dot products per step for ILP; the compares stay in
+  // index order, so the first maximum still wins (geometry.cpp:404-409).
+  for (; i + 4 <= h.nv; i += 4) {
+    const double s0 = dl.x * GDEV_LDG(V + 3 * i) + dl.y * GDEV_LDG(V + 3 * i + 1) + dl.z * GDEV_LDG(V + 3 * i + 2);
+    const double s1 = dl.x * GDEV_LDG(V + 3 * i + 3) + dl.y * GDEV_LDG(V + 3 * i + 4) + dl.z * GDEV_LDG(V + 3 * i + 5);
+    const double s2 = dl.x * GDEV_LDG(V + 3 * i + 6) + dl.y * GDEV_LDG(V + 3 * i + 7) + dl.z * GDEV_LDG(V + 3 * i + 8);
+    const double s3 = dl.x * GDEV_LDG(V + 3 * i + 9) + dl.y * GDEV_LDG(V + 3 * i + 10) + dl.z * GDEV_LDG(V + 3 * i + 11);
+    if (s0 > best) { best = s0; arg = i; }
+    if (s1 > best) { best = s1; arg = i + 1; }
+    if (s2 > best) { best = s2; arg = i + 2; }
+    if (s3 > best) { best = s3; arg = i + 3; }
+  }
+  for (; i < h.nv; ++i) {
+    const double s = dl.x * GDEV_LDG(V + 3 * i) + dl.y * GDEV_LDG(V + 3 * i + 1) + dl.z * GDEV_LDG(V + 3 * i + 2);
     if (s > best) {
       best = s;
       arg = i;
@@ -187,6 +201,94 @@ struct Simplex {
   bool contains;
 };
 
+// Cheap filter for one subset (K >= 2). Solves the same least-norm problem
+// in edge form (w0 + sum s_i e_i, normal equations by Cramer) and returns
+// true only when the exact FullPivLU path would certainly make no change to
+// `best`: some barycentric weight is below -1e-12 by more than a
+// conservative error bound E, or the subset is certainly accepted but its
+// squared distance certainly exceeds best * (1 + 1e-12). E grows with the
+// conditioning of both this solve and the reference's KKT system; poorly
+// conditioned subsets are never filtered. Skipping those subsets leaves
+// the enumeration's result bit-identical.
+template <int K>
+GDEV_FN bool subset_skippable(const SP* simp, const int (&idx)[K], const Simplex& best) {
+  constexpr int E_ = K - 1;
+  const D3 w0 = simp[idx[0]].w;
+  D3 e[E_];
+  double A[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, b[3] = {0, 0, 0};
+  double w2max = sqn(w0), emin = INFINITY;
+#pragma unroll
+  for (int i = 0; i < E_; ++i) {
+    e[i] = simp[idx[i + 1]].w - w0;
+    w2max = fmax(w2max, sqn(simp[idx[i + 1]].w));
+  }
+#pragma unroll
+  for (int i = 0; i < E_; ++i) {
+#pragma unroll
+    for (int j = 0; j < E_; ++j) A[i][j] = dot(e[i], e[j]);
+    b[i] = -dot(w0, e[i]);
+    emin = fmin(emin, A[i][i]);
+  }
+  if (!(emin > 0.0)) return false;
+  double s[3] = {0, 0, 0}, kappa;
+  if (E_ == 1) {
+    s[0] = b[0] / A[0][0];
+    kappa = 1.0;
+  } else if (E_ == 2) {
+    const double det = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+    if (!(det > 1e-6 * A[0][0] * A[1][1])) return false;
+    s[0] = (b[0] * A[1][1] - b[1] * A[0][1]) / det;
+    s[1] = (A[0][0] * b[1] - A[1][0] * b[0]) / det;
+    kappa = (A[0][0] + A[1][1]) * (A[0][0] + A[1][1]) / det;
+  } else {
+    const double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1];
+    const double c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2];
+    const double c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
+    const double det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
+    if (!(det > 1e-6 * A[0][0] * A[1][1] * A[2][2])) return false;
+    const double c11 = A[0][0] * A[2][2] - A[0][2] * A[2][0];
+    const double c12 = A[0][1] * A[2][0] - A[0][0] * A[2][1];
+    const double c22 = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+    const double c10 = A[0][2] * A[2][1] - A[0][1] * A[2][2];
+    const double c20 = A[0][1] * A[1][2] - A[0][2] * A[1][1];
+    const double c21 = A[0][2] * A[1][0] - A[0][0] * A[1][2];
+    s[0] = (c00 * b[0] + c10 * b[1] + c20 * b[2]) / det;
+    s[1] = (c01 * b[0] + c11 * b[1] + c21 * b[2]) / det;
+    s[2] = (c02 * b[0] + c12 * b[1] + c22 * b[2]) / det;
+    const double tr = A[0][0] + A[1][1] + A[2][2];
+    kappa = tr * tr * tr / det;
+  }
+  double lam[K];
+  double l0 = 1.0, lmax = 0.0;
+#pragma unroll
+  for (int i = 0; i < E_; ++i) {
+    lam[i + 1] = s[i];
+    l0 -= s[i];
+    lmax = fmax(lmax, fabs(s[i]));
+  }
+  lam[0] = l0;
+  lmax = fmax(lmax, fabs(l0));
+  // Error bound on |lam_cheap - lam_LU|: both solves carry ~eps * cond; the
+  // KKT form used by FullPivLU degrades with |w|^2 / |e|^2.
+  const double cond = kappa * fmax(1.0, w2max / emin);
+  if (!(cond < 1e6)) return false;
+  const double E = 1e-9 * (1.0 + lmax) * fmax(1.0, cond * 1e-3);
+  bool certainly_rejected = false, certainly_accepted = true;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    if (lam[i] < -1e-12 - E) certainly_rejected = true;
+    if (!(lam[i] >= -1e-12 + E)) certainly_accepted = false;
+  }
+  if (certainly_rejected) return true;
+  if (!certainly_accepted) return false;
+  D3 v = w0;
+#pragma unroll
+  for (int i = 0; i < E_; ++i) v += s[i] * e[i];
+  const double d2 = sqn(v);
+  const double Ed = 1e-9 * w2max * (1.0 + lmax) * fmax(1.0, cond * 1e-3);
+  return d2 - Ed > best.dist2 * (1.0 + 1e-6);
+}
+
 // One subset of closest_on_simplex (geometry.cpp:61-93): solve the
 // (K+1)x(K+1) affine least-norm KKT system and apply the acceptance and
 // tie rules against the running best.
@@ -200,6 +302,11 @@ GDEV_FN void simplex_subset(const SP* simp, const double (&gram)[4][4], Simplex&
     for (int i = 0; i < N; ++i)
       if (MASK & (1 << i)) idx[k++] = i;
   }
+#ifdef GDEV_SUBSET_FILTER  // exact but slower on sm_100a in mask order
+  if constexpr (K >= 2) {
+    if (subset_skippable<K>(simp, idx, best)) return;
+  }
+#endif
   double m[K + 1][K + 1];
   double rhs[K + 1];
 #pragma unroll

@@ -449,40 +449,94 @@ __global__ void __launch_bounds__(128) k_pairs(DevHand H, DevObject O, DevState 
   }
 }
 
-// Compacted pair evaluation, pass 1: one thread per (grasp, link, part)
-// slot runs the cull test; culled slots get their (+inf) result directly,
-// the rest are appended to st.pair_list with one atomic per warp (lane order
-// kept, so list neighbours share (link, part) and read the same vertices).
+// Compacted pair evaluation. The list is segmented by (link, part) so that a
+// GJK warp works on one hull pair: its vertex loads are warp-uniform
+// (broadcast) and its support loops have one trip count.
+//
+// Pass 1a: one thread per (grasp, link, part) launch index t (lp-major) runs
+// the cull test; culled slots get their (+inf) result directly, the others
+// set need[t] and are counted into their segment (one atomic per segment
+// present in the warp).
+__device__ __forceinline__ int warp_segment_add(int* counters, int seg, bool active) {
+  // Adds 1 per active lane to counters[seg] with one atomic per distinct seg;
+  // returns this lane's position (old value + rank among active lanes of seg).
+  const unsigned act = __ballot_sync(kFull, active);
+  const unsigned peers = __match_any_sync(kFull, seg) & act;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  const int leader = peers ? __ffs(peers) - 1 : lane;
+  if (active && lane == leader) base = atomicAdd(counters + seg, __popc(peers));
+  base = __shfl_sync(kFull, base, leader);
+  return base + __popc(peers & ((1u << lane) - 1));
+}
+
 __global__ void __launch_bounds__(128) k_pairs_cull(DevHand H, DevObject O, DevState st,
                                                     const int* __restrict__ links, int n_links) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
+  const long long n = (long long)st.G * n_links * O.P;
   bool need = false;
-  int slot = 0;
-  if (t < (long long)st.G * n_links * O.P) {
+  int lp = 0;
+  if (t < n) {
     const int g = (int)(t % st.G);
-    const int lp = (int)(t / st.G);
+    lp = (int)(t / st.G);
     const int link = links ? links[lp / O.P] : lp / O.P;
     const int part = lp % O.P;
-    slot = (int)((size_t)g * st.NP + link * O.P + part);
     if (!st.failed[g]) {
       const double* w = st.world + ((size_t)g * H.L + link) * 12;
       M33 Rw;
       for (int i = 0; i < 9; ++i) Rw.m[i] = w[i];
       need = pair_needed(H, O, st, g, link, part, Rw, ld3(w + 9));
       if (!need) {
-        double* o = st.pairs + (size_t)slot * 12;
+        double* o = st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12;
         o[0] = INFINITY;
         o[10] = kPairCulled;
       }
     }
+    st.pair_need[t] = need;
   }
-  const unsigned mask = __ballot_sync(kFull, need);
-  if (!mask) return;
-  int base = 0;
-  if (lane == 0) base = atomicAdd(st.pair_count, __popc(mask));
-  base = __shfl_sync(kFull, base, 0);
-  if (need) st.pair_list[base + __popc(mask & ((1u << lane) - 1))] = slot;
+  warp_segment_add(st.seg_count, lp, need);
+}
+
+// Pass 1b: exclusive scan of the segment counts (one block); seg_count turns
+// into the fill cursor of pass 1c, *pair_count into the list length.
+__global__ void __launch_bounds__(1024) k_pairs_scan(DevState st, int n_seg) {
+  __shared__ int part_sum[1024];
+  const int tid = threadIdx.x;
+  const int per = (n_seg + 1023) / 1024;
+  const int b = tid * per, e = min(n_seg, b + per);
+  int s = 0;
+  for (int i = b; i < e; ++i) s += st.seg_count[i];
+  part_sum[tid] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const int v = tid >= off ? part_sum[tid - off] : 0;
+    __syncthreads();
+    part_sum[tid] += v;
+    __syncthreads();
+  }
+  int run = part_sum[tid] - s;
+  for (int i = b; i < e; ++i) {
+    const int c = st.seg_count[i];
+    st.seg_offset[i] = run;
+    st.seg_count[i] = run;
+    run += c;
+  }
+  if (tid == 1023) *st.pair_count = part_sum[1023];
+}
+
+// Pass 1c: scatter the needed slots into their segments.
+__global__ void __launch_bounds__(128) k_pairs_scatter(DevState st, const int* __restrict__ links, int n_links,
+                                                       int P) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = (long long)st.G * n_links * P;
+  const bool need = t < n && st.pair_need[t];
+  const int lp = t < n ? (int)(t / st.G) : 0;
+  const int pos = warp_segment_add(st.seg_count, lp, need);
+  if (need) {
+    const int g = (int)(t % st.G);
+    const int link = links ? links[lp / P] : lp / P;
+    st.pair_list[pos] = (int)((size_t)g * st.NP + link * P + lp % P);
+  }
 }
 
 // Hulls and cloud_scale (geometry.cpp:17-23) of a pair slot.

@@ -129,6 +129,9 @@ struct DevState {
   int big_slots;
   int* pair_count;     // compacted list of pair slots that need GJK
   int* pair_list;      // [G*NP]
+  unsigned char* pair_need;  // [G*NP-slot order of the launch] 1 when the pair needs GJK
+  int* seg_count;      // [NP] needed pairs per (link, part) segment, then the fill cursor
+  int* seg_offset;     // [NP] exclusive scan of seg_count
   int* epa_count;      // overlapping pairs handed from GJK to the EPA kernel
   double* epa_jobs;    // [epa_cap * kEpaJobStride]: slot, ns, 4 x (w, a, b)
   int epa_cap;

@@ -56,8 +56,12 @@ struct QpSmem {
 // per-grasp scratch, envelope-gradient forces written when with_grad).
 // mode 1: final record (frames from st.frames, cold start).
 // mode 2: standalone batch (frames from st.frames, warm if qp_ready).
+#ifndef GDEV_QP_MIN_BLOCKS
+#define GDEV_QP_MIN_BLOCKS 3  // <= 170 registers, no spills (measured best)
+#endif
 template <int KT, int MT>
-__global__ void __launch_bounds__(128) k_qp_t(DevHand H, DevParams P, DevState st, int m_rt, int mode, int with_grad) {
+__global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
+    k_qp_t(DevHand H, DevParams P, DevState st, int m_rt, int mode, int with_grad) {
   __shared__ QpSmem smem_all[4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * 4 + warp;
