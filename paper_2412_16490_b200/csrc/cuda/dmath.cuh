@@ -19,6 +19,20 @@ struct D3 {
   double x, y, z;
 };
 
+// p ? a : b as one selp.f64. nvcc 12.9's optimiser miscompiles the
+// unrolled select chains of the pivoting swaps in fullpiv_solve_t (a swap
+// was applied with the pivot already in place; reproduced in isolation on
+// sm_100a at every ptxas level), so those selects are opaque to it.
+GDEV_FN double psel(bool p, double a, double b) {
+#if defined(__CUDA_ARCH__)
+  double r;
+  asm("{ .reg .pred q; setp.ne.u32 q, %1, 0; selp.f64 %0, %2, %3, q; }" : "=d"(r) : "r"((unsigned)p), "d"(a), "d"(b));
+  return r;
+#else
+  return p ? a : b;
+#endif
+}
+
 GDEV_FN D3 mk(double x, double y, double z) { return D3{x, y, z}; }
 GDEV_FN D3 operator+(D3 a, D3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
 GDEV_FN D3 operator-(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }

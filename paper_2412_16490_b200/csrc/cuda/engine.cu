@@ -119,10 +119,12 @@ struct grasp_ctx {
     const char* v = std::getenv("GRASP_PAIRS");
     if (v && std::string(v) == "warp") return 1;
     if (v && std::string(v) == "thread") return 2;
+    if (v && std::string(v) == "list1") return 3;
     return 0;
   }();
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
   DevBuf<unsigned char> pair_need;
+  long long list_grid = 148 * 4;  // persistent k_pairs_list blocks
   DevBuf<double> epa_jobs;
 
   // Instrumentation: launch counts always; per-class CUDA-event time and
@@ -445,7 +447,7 @@ struct grasp_ctx {
     st.ovf_cap = static_cast<int>(g * NP);
     st.big_scratch = big_scratch.p;
     st.big_slots = kBigSlots;
-    pair_count.ensure(2);
+    pair_count.ensure(3);  // list length, EPA jobs, list cursor
     pair_list.ensure(g * NP);
     st.pair_count = pair_count.p;
     st.pair_list = pair_list.p;
@@ -555,12 +557,15 @@ struct grasp_ctx {
       } else if (pairs_variant == 2) {
         k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
       } else {
-        ck(cudaMemsetAsync(pair_count.p, 0, 2 * sizeof(int), stream), "memset");  // pair_count, epa_count
+        ck(cudaMemsetAsync(pair_count.p, 0, 3 * sizeof(int), stream), "memset");
         ck(cudaMemsetAsync(seg_count.p, 0, sizeof(int) * nl * O.P, stream), "memset");
         k_pairs_cull<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
         k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.P);
         k_pairs_scatter<<<blocks(n, 128), 128, 0, stream>>>(st, lk, nl, O.P);
-        k_pairs_list<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
+        if (pairs_variant == 3)
+          k_pairs_list1<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
+        else
+          k_pairs_list<<<std::min<long long>(blocks(n, 128), list_grid), 128, 0, stream>>>(H, O, st);
         k_pairs_epa<<<blocks(std::min<long long>(n, st.epa_cap), 128), 128, 0, stream>>>(H, O, st);
       }
     });
@@ -753,6 +758,11 @@ int grasp_ctx_create(int device, grasp_ctx** out) {
       ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
       // Large per-thread stacks for the EPA scratch of k_pairs.
       ck(cudaDeviceSetLimit(cudaLimitStackSize, 32 * 1024), "stack limit");
+      // Persistent GJK grid: every resident block slot on every SM.
+      int sms = 0, per_sm = 0;
+      ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gdev::k_pairs_list, 128, 0), "occupancy");
+      ctx->list_grid = static_cast<long long>(sms) * std::max(per_sm, 1);
     } catch (...) {
       delete ctx;
       throw;

@@ -108,24 +108,28 @@ GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (
     maxpivot = fmax(maxpivot, biggest);
     rowt[k] = br;
     colt[k] = bc;
+    // Row and column swaps as select chains: the pivot position differs
+    // from lane to lane, and branches here would serialise the warp.
 #pragma unroll
-    for (int r = k + 1; r < S; ++r)
-      if (r == br)
+    for (int c = 0; c < S; ++c) {
+      const double old = m[k][c];
+      double pick = old;
 #pragma unroll
-        for (int c = 0; c < S; ++c) {
-          const double t = m[k][c];
-          m[k][c] = m[r][c];
-          m[r][c] = t;
-        }
+      for (int r = k + 1; r < S; ++r) pick = psel(br == r, m[r][c], pick);
 #pragma unroll
-    for (int c = k + 1; c < S; ++c)
-      if (c == bc)
+      for (int r = k + 1; r < S; ++r) m[r][c] = psel(br == r, old, m[r][c]);
+      m[k][c] = pick;
+    }
 #pragma unroll
-        for (int r = 0; r < S; ++r) {
-          const double t = m[r][k];
-          m[r][k] = m[r][c];
-          m[r][c] = t;
-        }
+    for (int r = 0; r < S; ++r) {
+      const double old = m[r][k];
+      double pick = old;
+#pragma unroll
+      for (int c = k + 1; c < S; ++c) pick = psel(bc == c, m[r][c], pick);
+#pragma unroll
+      for (int c = k + 1; c < S; ++c) m[r][c] = psel(bc == c, old, m[r][c]);
+      m[r][k] = pick;
+    }
     if (k < S - 1) {
       const double piv = m[k][k];
 #pragma unroll
@@ -151,44 +155,51 @@ GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (
 #pragma unroll
   for (int i = 0; i < S; ++i) c[i] = rhs[i];
 #pragma unroll
-  for (int k = 0; k < S; ++k)
+  for (int k = 0; k < S; ++k) {
+    const double old = c[k];
+    double pick = old;
 #pragma unroll
-    for (int r = k + 1; r < S; ++r)
-      if (r == rowt[k]) {
-        const double t = c[k];
-        c[k] = c[r];
-        c[r] = t;
-      }
+    for (int r = k + 1; r < S; ++r) pick = (rowt[k] == r) ? c[r] : pick;
 #pragma unroll
-  for (int i = 0; i < S; ++i)
-    if (c[i] != 0.0)
+    for (int r = k + 1; r < S; ++r) c[r] = (rowt[k] == r) ? old : c[r];
+    c[k] = pick;
+  }
+  // Substitutions with the reference's zero skips as selects (same
+  // operations on the taken path, no lane-dependent branches).
 #pragma unroll
-      for (int r = i + 1; r < S; ++r) c[r] -= c[i] * m[r][i];
+  for (int i = 0; i < S; ++i) {
+    const bool nz = c[i] != 0.0;
 #pragma unroll
-  for (int i = S - 1; i >= 0; --i)
-    if (i < rank && c[i] != 0.0) {
-      c[i] /= m[i][i];
+    for (int r = i + 1; r < S; ++r) c[r] = nz ? c[r] - c[i] * m[r][i] : c[r];
+  }
 #pragma unroll
-      for (int r = 0; r < i; ++r) c[r] -= c[i] * m[r][i];
-    }
+  for (int i = S - 1; i >= 0; --i) {
+    const bool act = i < rank && c[i] != 0.0;
+    const double ci = c[i] / (act ? m[i][i] : 1.0);
+    c[i] = act ? ci : c[i];
+#pragma unroll
+    for (int r = 0; r < i; ++r) c[r] = act ? c[r] - ci * m[r][i] : c[r];
+  }
   int perm[S];
 #pragma unroll
   for (int i = 0; i < S; ++i) perm[i] = i;
 #pragma unroll
-  for (int k = 0; k < S; ++k)
+  for (int k = 0; k < S; ++k) {
+    const int old = perm[k];
+    int pick = old;
 #pragma unroll
-    for (int r = k + 1; r < S; ++r)
-      if (r == colt[k]) {
-        const int t = perm[k];
-        perm[k] = perm[r];
-        perm[r] = t;
-      }
+    for (int r = k + 1; r < S; ++r) pick = (colt[k] == r) ? perm[r] : pick;
+#pragma unroll
+    for (int r = k + 1; r < S; ++r) perm[r] = (colt[k] == r) ? old : perm[r];
+    perm[k] = pick;
+  }
+#pragma unroll
+  for (int j = 0; j < S; ++j) sol[j] = 0.0;
 #pragma unroll
   for (int i = 0; i < S; ++i) {
     const double v = i < rank ? c[i] : 0.0;
 #pragma unroll
-    for (int j = 0; j < S; ++j)
-      if (perm[i] == j) sol[j] = v;
+    for (int j = 0; j < S; ++j) sol[j] = (perm[i] == j) ? v : sol[j];
   }
 }
 
@@ -201,118 +212,111 @@ struct Simplex {
   bool contains;
 };
 
-// Cheap filter for one subset (K >= 2). Solves the same least-norm problem
-// in edge form (w0 + sum s_i e_i, normal equations by Cramer) and returns
-// true only when the exact FullPivLU path would certainly make no change to
-// `best`: some barycentric weight is below -1e-12 by more than a
-// conservative error bound E, or the subset is certainly accepted but its
-// squared distance certainly exceeds best * (1 + 1e-12). E grows with the
-// conditioning of both this solve and the reference's KKT system; poorly
-// conditioned subsets are never filtered. Skipping those subsets leaves
-// the enumeration's result bit-identical.
+// Cheap classification of one subset (closest_fast's first pass). Solves
+// the same least-norm problem in edge form (w0 + sum s_i e_i, normal
+// equations by Cramer) and bounds its error against the reference's
+// FullPivLU solve of the KKT system: E grows with the conditioning of both
+// (poorly conditioned subsets are never classified). Returns
+//   0  certainly rejected (some weight < -1e-12 by more than E),
+//   1  certainly accepted, with d2 and an error bound err on it,
+//   2  ambiguous.
 template <int K>
-GDEV_FN bool subset_skippable(const SP* simp, const int (&idx)[K], const Simplex& best) {
-  constexpr int E_ = K - 1;
-  const D3 w0 = simp[idx[0]].w;
-  D3 e[E_];
-  double A[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, b[3] = {0, 0, 0};
-  double w2max = sqn(w0), emin = INFINITY;
-#pragma unroll
-  for (int i = 0; i < E_; ++i) {
-    e[i] = simp[idx[i + 1]].w - w0;
-    w2max = fmax(w2max, sqn(simp[idx[i + 1]].w));
-  }
-#pragma unroll
-  for (int i = 0; i < E_; ++i) {
-#pragma unroll
-    for (int j = 0; j < E_; ++j) A[i][j] = dot(e[i], e[j]);
-    b[i] = -dot(w0, e[i]);
-    emin = fmin(emin, A[i][i]);
-  }
-  if (!(emin > 0.0)) return false;
-  double s[3] = {0, 0, 0}, kappa;
-  if (E_ == 1) {
-    s[0] = b[0] / A[0][0];
-    kappa = 1.0;
-  } else if (E_ == 2) {
-    const double det = A[0][0] * A[1][1] - A[0][1] * A[1][0];
-    if (!(det > 1e-6 * A[0][0] * A[1][1])) return false;
-    s[0] = (b[0] * A[1][1] - b[1] * A[0][1]) / det;
-    s[1] = (A[0][0] * b[1] - A[1][0] * b[0]) / det;
-    kappa = (A[0][0] + A[1][1]) * (A[0][0] + A[1][1]) / det;
+GDEV_FN int cheap_subset(const SP* simp, const int (&idx)[K], double& d2, double& err) {
+  if constexpr (K == 1) {
+    d2 = sqn(simp[idx[0]].w);
+    err = 1e-9 * d2;
+    return 1;
   } else {
-    const double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1];
-    const double c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2];
-    const double c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
-    const double det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
-    if (!(det > 1e-6 * A[0][0] * A[1][1] * A[2][2])) return false;
-    const double c11 = A[0][0] * A[2][2] - A[0][2] * A[2][0];
-    const double c12 = A[0][1] * A[2][0] - A[0][0] * A[2][1];
-    const double c22 = A[0][0] * A[1][1] - A[0][1] * A[1][0];
-    const double c10 = A[0][2] * A[2][1] - A[0][1] * A[2][2];
-    const double c20 = A[0][1] * A[1][2] - A[0][2] * A[1][1];
-    const double c21 = A[0][2] * A[1][0] - A[0][0] * A[1][2];
-    s[0] = (c00 * b[0] + c10 * b[1] + c20 * b[2]) / det;
-    s[1] = (c01 * b[0] + c11 * b[1] + c21 * b[2]) / det;
-    s[2] = (c02 * b[0] + c12 * b[1] + c22 * b[2]) / det;
-    const double tr = A[0][0] + A[1][1] + A[2][2];
-    kappa = tr * tr * tr / det;
-  }
-  double lam[K];
-  double l0 = 1.0, lmax = 0.0;
+    constexpr int E_ = K - 1;
+    const D3 w0 = simp[idx[0]].w;
+    D3 e[E_];
+    double A[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, b[3] = {0, 0, 0};
+    double w2max = sqn(w0), emin = INFINITY;
 #pragma unroll
-  for (int i = 0; i < E_; ++i) {
-    lam[i + 1] = s[i];
-    l0 -= s[i];
-    lmax = fmax(lmax, fabs(s[i]));
-  }
-  lam[0] = l0;
-  lmax = fmax(lmax, fabs(l0));
-  // Error bound on |lam_cheap - lam_LU|: both solves carry ~eps * cond; the
-  // KKT form used by FullPivLU degrades with |w|^2 / |e|^2.
-  const double cond = kappa * fmax(1.0, w2max / emin);
-  if (!(cond < 1e6)) return false;
-  const double E = 1e-9 * (1.0 + lmax) * fmax(1.0, cond * 1e-3);
-  bool certainly_rejected = false, certainly_accepted = true;
+    for (int i = 0; i < E_; ++i) {
+      e[i] = simp[idx[i + 1]].w - w0;
+      w2max = fmax(w2max, sqn(simp[idx[i + 1]].w));
+    }
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    if (lam[i] < -1e-12 - E) certainly_rejected = true;
-    if (!(lam[i] >= -1e-12 + E)) certainly_accepted = false;
-  }
-  if (certainly_rejected) return true;
-  if (!certainly_accepted) return false;
-  D3 v = w0;
+    for (int i = 0; i < E_; ++i) {
 #pragma unroll
-  for (int i = 0; i < E_; ++i) v += s[i] * e[i];
-  const double d2 = sqn(v);
-  const double Ed = 1e-9 * w2max * (1.0 + lmax) * fmax(1.0, cond * 1e-3);
-  return d2 - Ed > best.dist2 * (1.0 + 1e-6);
+      for (int j = 0; j < E_; ++j) A[i][j] = dot(e[i], e[j]);
+      b[i] = -dot(w0, e[i]);
+      emin = fmin(emin, A[i][i]);
+    }
+    if (!(emin > 0.0)) return 2;
+    double s[3] = {0, 0, 0}, kappa;
+    if constexpr (E_ == 1) {
+      s[0] = b[0] / A[0][0];
+      kappa = 1.0;
+    } else if constexpr (E_ == 2) {
+      const double det = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+      if (!(det > 1e-6 * A[0][0] * A[1][1])) return 2;
+      const double inv = 1.0 / det;
+      s[0] = (b[0] * A[1][1] - b[1] * A[0][1]) * inv;
+      s[1] = (A[0][0] * b[1] - A[1][0] * b[0]) * inv;
+      kappa = (A[0][0] + A[1][1]) * (A[0][0] + A[1][1]) * inv;
+    } else {
+      const double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1];
+      const double c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2];
+      const double c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
+      const double det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
+      if (!(det > 1e-6 * A[0][0] * A[1][1] * A[2][2])) return 2;
+      const double c11 = A[0][0] * A[2][2] - A[0][2] * A[2][0];
+      const double c12 = A[0][1] * A[2][0] - A[0][0] * A[2][1];
+      const double c22 = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+      const double c10 = A[0][2] * A[2][1] - A[0][1] * A[2][2];
+      const double c20 = A[0][1] * A[1][2] - A[0][2] * A[1][1];
+      const double c21 = A[0][2] * A[1][0] - A[0][0] * A[1][2];
+      const double inv = 1.0 / det;
+      s[0] = (c00 * b[0] + c10 * b[1] + c20 * b[2]) * inv;
+      s[1] = (c01 * b[0] + c11 * b[1] + c21 * b[2]) * inv;
+      s[2] = (c02 * b[0] + c12 * b[1] + c22 * b[2]) * inv;
+      const double tr = A[0][0] + A[1][1] + A[2][2];
+      kappa = tr * tr * tr * inv;
+    }
+    double l0 = 1.0, lmax = 0.0, lmin = INFINITY;
+#pragma unroll
+    for (int i = 0; i < E_; ++i) {
+      l0 -= s[i];
+      lmax = fmax(lmax, fabs(s[i]));
+      lmin = fmin(lmin, s[i]);
+    }
+    lmax = fmax(lmax, fabs(l0));
+    lmin = fmin(lmin, l0);
+    // Error bound on |lam_cheap - lam_LU|: both solves carry ~eps * cond; the
+    // KKT form used by FullPivLU degrades with |w|^2 / |e|^2.
+    const double cond = kappa * fmax(1.0, w2max / emin);
+    if (!(cond < 1e6)) return 2;
+    const double E = 1e-9 * (1.0 + lmax) * fmax(1.0, cond * 1e-3);
+    if (lmin < -1e-12 - E) return 0;
+    if (!(lmin >= -1e-12 + E)) return 2;
+    D3 v = w0;
+#pragma unroll
+    for (int i = 0; i < E_; ++i) v += s[i] * e[i];
+    d2 = sqn(v);
+    err = 1e-9 * w2max * (1.0 + lmax) * fmax(1.0, cond * 1e-3);
+    return 1;
+  }
 }
 
 // One subset of closest_on_simplex (geometry.cpp:61-93): solve the
-// (K+1)x(K+1) affine least-norm KKT system and apply the acceptance and
-// tie rules against the running best.
-template <int N, int MASK>
-GDEV_FN void simplex_subset(const SP* simp, const double (&gram)[4][4], Simplex& best) {
-  constexpr int K = (MASK & 1) + ((MASK >> 1) & 1) + ((MASK >> 2) & 1) + ((MASK >> 3) & 1);
-  int idx[K];
-  {
-    int k = 0;
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-      if (MASK & (1 << i)) idx[k++] = i;
-  }
-#ifdef GDEV_SUBSET_FILTER  // exact but slower on sm_100a in mask order
-  if constexpr (K >= 2) {
-    if (subset_skippable<K>(simp, idx, best)) return;
-  }
-#endif
+// (K+1)x(K+1) affine least-norm KKT system for the gathered points P[0..K)
+// (original simplex indices id[0..K)) and apply the acceptance and tie rules
+// against the running best. Gram entries are dot(P_i, P_j), bit-identical
+// to the reference's gram(idx_i, idx_j) (products commute exactly, sums in
+// the same order, no contraction in this TU).
+template <int K>
+GDEV_FN void simplex_subset(const D3 (&P)[4], const int (&id)[4], Simplex& best) {
   double m[K + 1][K + 1];
   double rhs[K + 1];
 #pragma unroll
   for (int i = 0; i < K; ++i) {
 #pragma unroll
-    for (int j = 0; j < K; ++j) m[i][j] = gram[idx[i]][idx[j]];
+    for (int j = i; j < K; ++j) {
+      m[i][j] = dot(P[i], P[j]);
+      m[j][i] = m[i][j];
+    }
     m[i][K] = 1.0;
     m[K][i] = 1.0;
     rhs[i] = 0.0;
@@ -329,7 +333,7 @@ GDEV_FN void simplex_subset(const SP* simp, const double (&gram)[4][4], Simplex&
   if (!ok) return;
   D3 v = mk(0, 0, 0);
 #pragma unroll
-  for (int i = 0; i < K; ++i) v += sol[i] * simp[idx[i]].w;
+  for (int i = 0; i < K; ++i) v += sol[i] * P[i];
   const double d2 = sqn(v);
   if (d2 < best.dist2 - 1e-300 || (K < best.nkeep && d2 <= best.dist2 * (1.0 + 1e-12))) {
     best.dist2 = d2;
@@ -337,34 +341,39 @@ GDEV_FN void simplex_subset(const SP* simp, const double (&gram)[4][4], Simplex&
     best.nkeep = K;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      best.keep[i] = i < K ? idx[i < K ? i : 0] : 0;
+      best.keep[i] = i < K ? id[i] : 0;
       best.wts[i] = i < K ? sol[i < K ? i : 0] : 0.0;
     }
     best.contains = K == 4;
   }
 }
 
-template <int N, int MASK>
-struct SubsetLoop {
-  GDEV_FN static void run(const SP* simp, const double (&gram)[4][4], Simplex& best) {
-    simplex_subset<N, MASK>(simp, gram, best);
-    SubsetLoop<N, MASK + 1>::run(simp, gram, best);
+// Gathers the points of subset `mask` (ascending index order) into P/id.
+GDEV_FN int gather_subset(const SP* simp, int mask, D3 (&P)[4], int (&id)[4]) {
+  int k = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool bit = (mask >> i) & 1;
+#pragma unroll
+    for (int s = 0; s <= i; ++s) {
+      const bool put = bit && k == s;
+      P[s].x = psel(put, simp[i].w.x, P[s].x);
+      P[s].y = psel(put, simp[i].w.y, P[s].y);
+      P[s].z = psel(put, simp[i].w.z, P[s].z);
+      id[s] = put ? i : id[s];
+    }
+    k += bit ? 1 : 0;
   }
-};
-template <int N>
-struct SubsetLoop<N, (1 << N)> {
-  GDEV_FN static void run(const SP*, const double (&)[4][4], Simplex&) {}
-};
+  return k;
+}
 
-// Closest point of conv(simp) to the origin by subset enumeration in mask
-// order 1..2^n-1 (geometry.cpp:58-95).
-template <int N>
-GDEV_FN Simplex closest_on_simplex_t(const SP* simp) {
-  double gram[4][4];
-#pragma unroll
-  for (int i = 0; i < N; ++i)
-#pragma unroll
-    for (int j = 0; j < N; ++j) gram[i][j] = dot(simp[i].w, simp[j].w);
+// Closest point of conv(simp[0..n)) to the origin by subset enumeration in
+// mask order 1..2^n-1 (geometry.cpp:58-95). The mask loop is a runtime loop
+// over one solver body per subset size: every lane sees the same size at
+// the same mask, so lanes stay converged, and the code stays small enough
+// for the instruction cache (a fully unrolled enumeration is ~18k SASS
+// instructions and stalled on instruction fetch).
+GDEV_FN Simplex closest_on_simplex(const SP* simp, int n) {
   Simplex best;
   best.dist2 = INFINITY;
   best.v = mk(0, 0, 0);
@@ -375,18 +384,28 @@ GDEV_FN Simplex closest_on_simplex_t(const SP* simp) {
     best.keep[i] = 0;
     best.wts[i] = 0.0;
   }
-  SubsetLoop<N, 1>::run(simp, gram, best);
+  const int last = (1 << n) - 1;
+#pragma unroll 1
+  for (int mask = 1; mask <= last; ++mask) {
+    D3 P[4];
+    int id[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      P[i] = mk(0, 0, 0);
+      id[i] = 0;
+    }
+    const int K = gather_subset(simp, mask, P, id);
+    switch (K) {
+      case 1: simplex_subset<1>(P, id, best); break;
+      case 2: simplex_subset<2>(P, id, best); break;
+      case 3: simplex_subset<3>(P, id, best); break;
+      default: simplex_subset<4>(P, id, best); break;
+    }
+  }
   return best;
 }
 
-GDEV_INL Simplex closest_on_simplex(const SP* simp, int n) {
-  switch (n) {
-    case 1: return closest_on_simplex_t<1>(simp);
-    case 2: return closest_on_simplex_t<2>(simp);
-    case 3: return closest_on_simplex_t<3>(simp);
-    default: return closest_on_simplex_t<4>(simp);
-  }
-}
+GDEV_FN Simplex closest_on_simplex_var(const SP* simp, int n) { return closest_on_simplex(simp, n); }
 
 struct PairResult {
   double d;
@@ -624,11 +643,33 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
   ns = 1;
   simp[0] = support_pair(A, B, mk(1, 0, 0));
   simp[1] = simp[2] = simp[3] = simp[0];
-  bool done = false;
   bool overlap = false;
   Simplex sx;
-  for (int iter = 0; iter < kGjkMaxIters && !done; ++iter) {
+  // One closest_on_simplex call site (code size): call kGjkMaxIters is the
+  // iteration-cap estimate on the unreduced simplex (geometry.cpp:136-149).
+  for (int iter = 0;; ++iter) {
     sx = closest_on_simplex(simp, ns);
+    if (iter == kGjkMaxIters) {
+      D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i < sx.nkeep) {
+          const int src = sx.keep[i];
+          SP p = simp[0];
+          if (src == 1) p = simp[1];
+          if (src == 2) p = simp[2];
+          if (src == 3) p = simp[3];
+          wa += sx.wts[i] * p.a;
+          wb += sx.wts[i] * p.b;
+        }
+      }
+      const double d = sqrt(sx.dist2);
+      out.d = d;
+      out.pa = wa;
+      out.pb = wb;
+      out.n = d > 1e-14 ? (wa - wb) / d : mk(0, 0, 1);
+      return false;
+    }
     SP red[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -643,7 +684,6 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
     for (int i = 0; i < 4; ++i) simp[i] = red[i];
     if (sx.contains || sqrt(sx.dist2) < kTouchTol * scale) {
       overlap = true;
-      done = true;
       break;
     }
     const SP w = support_pair(A, B, -sx.v);
@@ -654,37 +694,11 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       if (i < ns && nrm(simp[i].w - w.w) < 1e-14 * scale) repeat = true;
-    if (gap <= kGjkRelTol * sx.dist2 + 1e-300 || repeat || ns == 4) {
-      done = true;
-      break;
-    }
+    if (gap <= kGjkRelTol * sx.dist2 + 1e-300 || repeat || ns == 4) break;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       if (i == ns) simp[i] = w;
     ++ns;
-  }
-  if (!done) {
-    // Iteration cap: current estimate from the unreduced simplex.
-    sx = closest_on_simplex(simp, ns);
-    D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (i < sx.nkeep) {
-        const int src = sx.keep[i];
-        SP p = simp[0];
-        if (src == 1) p = simp[1];
-        if (src == 2) p = simp[2];
-        if (src == 3) p = simp[3];
-        wa += sx.wts[i] * p.a;
-        wb += sx.wts[i] * p.b;
-      }
-    }
-    const double d = sqrt(sx.dist2);
-    out.d = d;
-    out.pa = wa;
-    out.pb = wb;
-    out.n = d > 1e-14 ? (wa - wb) / d : mk(0, 0, 1);
-    return false;
   }
   if (!overlap) {
     D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);

@@ -573,7 +573,167 @@ __device__ __forceinline__ void queue_overflow(const DevState& st, int slot) {
 #ifndef GDEV_PAIRS_MIN_BLOCKS
 #define GDEV_PAIRS_MIN_BLOCKS 4
 #endif
+__device__ __forceinline__ void write_epa_job(const DevState& st, int slot, const SP (&simp)[4], int ns) {
+  const int job = atomicAdd(st.epa_count, 1);
+  if (job >= st.epa_cap) {
+    queue_overflow(st, slot);
+    return;
+  }
+  double* jb = st.epa_jobs + (size_t)job * kEpaJobStride;
+  jb[0] = slot;
+  jb[1] = ns;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    st3(jb + 2 + 9 * k, simp[k].w);
+    st3(jb + 5 + 9 * k, simp[k].a);
+    st3(jb + 8 + 9 * k, simp[k].b);
+  }
+}
+
+// Separated-pair result (geometry.cpp:136-164): weights sx.wts over
+// simp[i] when simp is already reduced to sx's keep set, else over
+// simp[sx.keep[i]] (iteration cap).
+__device__ __forceinline__ void store_separated(double* o, const Simplex& sx, const SP (&simp)[4], bool reduced) {
+  D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < sx.nkeep) {
+      const int src = reduced ? i : sx.keep[i];
+      SP p = simp[0];
+      if (src == 1) p = simp[1];
+      if (src == 2) p = simp[2];
+      if (src == 3) p = simp[3];
+      wa += sx.wts[i] * p.a;
+      wb += sx.wts[i] * p.b;
+    }
+  }
+  const double d = sqrt(sx.dist2);
+  o[0] = d;
+  st3(o + 1, wa);
+  st3(o + 4, wb);
+  st3(o + 7, d > 1e-14 ? (wa - wb) / d : mk(0, 0, 1));
+  o[10] = 0;
+}
+
+// Pass 2: GJK over the pair list, persistent and iteration-interleaved. A
+// lane owns one pair at a time and runs one GJK iteration (geometry.cpp:
+// 105-164) per trip of the warp loop; a lane whose pair finished takes the
+// next list entry at the top of the following trip. Lanes therefore stay
+// busy regardless of how many iterations their pairs need (the per-pair
+// iteration counts are heavy-tailed), all lanes share one support_pair call
+// per trip, and closest_on_simplex_var keeps mixed simplex sizes converged.
+// Results are those of gjk_phase: the same operations run per pair, only
+// interleaved with other pairs. Overlapping pairs pass their terminal
+// simplex to k_pairs_epa.
 __global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHand H, DevObject O, DevState st) {
+  const int lane = threadIdx.x & 31;
+  const int total = *(volatile int*)st.pair_count;
+  int* cursor = st.pair_count + 2;
+  int slot = -1, ns = 0, iter = 0;
+  bool fresh = false, exhausted = false;
+  unsigned nsup = 0;
+  SP simp[4];
+  double scale = 1.0;
+  Hull A, B;
+  Simplex sx;
+  while (true) {
+    D3 dir = mk(1, 0, 0);
+    if (slot >= 0) {
+      // closest point, reduce, overlap test (geometry.cpp:112-120)
+      sx = closest_on_simplex(simp, ns);
+      if (iter >= kGjkMaxIters) {
+        // iteration cap: estimate from the unreduced simplex (geometry.cpp:136-149)
+        store_separated(st.pairs + (size_t)slot * 12, sx, simp, false);
+        slot = -1;
+      }
+    }
+    if (slot >= 0) {
+      SP red[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int src = sx.keep[i];
+        red[i] = simp[0];
+        if (src == 1) red[i] = simp[1];
+        if (src == 2) red[i] = simp[2];
+        if (src == 3) red[i] = simp[3];
+      }
+      ns = sx.nkeep;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) simp[i] = red[i];
+      if (sx.contains || sqrt(sx.dist2) < kTouchTol * scale) {
+        if (st.ops) {
+          atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)nsup * (A.nv + B.nv));
+          atomicAdd(st.ops + kOpGjkIters, (unsigned long long)iter + 1);
+          atomicAdd(st.ops + kOpPairsNeeded, 1ull);
+        }
+        write_epa_job(st, slot, simp, ns);
+        slot = -1;
+      } else {
+        dir = -sx.v;
+      }
+    }
+    // refill idle lanes from the list
+    const unsigned want = __ballot_sync(kFull, slot < 0 && !exhausted);
+    if (want) {
+      const int leader = __ffs(want) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(cursor, __popc(want));
+      base = __shfl_sync(kFull, base, leader);
+      if (slot < 0 && !exhausted) {
+        const int i = base + __popc(want & ((1u << lane) - 1));
+        if (i < total) {
+          slot = st.pair_list[i];
+          slot_hulls(H, O, st, slot, A, B, scale);
+          fresh = true;
+          dir = mk(1, 0, 0);
+        } else {
+          exhausted = true;
+        }
+      }
+    }
+    if (!__any_sync(kFull, slot >= 0)) break;
+    if (slot < 0) continue;
+    const SP w = support_pair(A, B, dir);
+    if (fresh) {
+      simp[0] = simp[1] = simp[2] = simp[3] = w;
+      ns = 1;
+      iter = 0;
+      nsup = 1;
+      fresh = false;
+      continue;
+    }
+    ++nsup;
+    ++iter;
+    // termination tests, then grow the simplex (geometry.cpp:122-135)
+    const double gap = sx.dist2 - dot(sx.v, w.w);
+    bool repeat = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < ns && nrm(simp[i].w - w.w) < 1e-14 * scale) repeat = true;
+    const bool done = gap <= kGjkRelTol * sx.dist2 + 1e-300 || repeat || ns == 4;
+    if (!done) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i == ns) simp[i] = w;
+      ++ns;
+    }
+    if (done || iter >= kGjkMaxIters) {
+      if (st.ops) {
+        atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)nsup * (A.nv + B.nv));
+        atomicAdd(st.ops + kOpGjkIters, (unsigned long long)iter + 1);
+        atomicAdd(st.ops + kOpPairsNeeded, 1ull);
+      }
+      if (done) {
+        store_separated(st.pairs + (size_t)slot * 12, sx, simp, true);
+        slot = -1;
+      }  // else: capped, the next trip's closest_on_simplex gives the estimate
+    }
+  }
+}
+
+// Non-interleaved variant (one pair per thread start to end; A/B reference
+// for the kernel above, GRASP_PAIRS=list1).
+__global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list1(DevHand H, DevObject O, DevState st) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *st.pair_count) return;
   const int slot = st.pair_list[i];

@@ -1,5 +1,5 @@
 """Short synthesis run for ncu captures (dev tool): Shadow-like + drill,
-batch 1024, 20/10/10 iterations."""
+batch 1024, 20/10/10 iterations (argv: batch [coarse fine final])."""
 import sys
 from pathlib import Path
 
@@ -13,7 +13,8 @@ cfg = G.RunConfig()
 cfg.seed = 17
 batch = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 cfg.batch = batch
-cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 20, 10, 10
+sched = [int(a) for a in sys.argv[2:5]] if len(sys.argv) > 4 else [20, 10, 10]
+cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = sched
 eng = G.Engine(0)
 eng.set_hand(hand)
 eng.set_object(obj)
