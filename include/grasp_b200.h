@@ -222,7 +222,7 @@ void* grasp_ctx_stream(grasp_ctx* ctx);
  * not culled, 9 EPA overflows. */
 int grasp_ctx_set_profiling(grasp_ctx* ctx, int on);
 int grasp_ctx_profile(grasp_ctx* ctx, double* ms /*[8]*/, long long* launches /*[8]*/,
-                      unsigned long long* ops /*[10]*/);
+                      unsigned long long* ops /*[20]*/);
 /* Kernels launched by this context so far. */
 long long grasp_ctx_launch_count(grasp_ctx* ctx);
 /* Measured dense fp64 FMA throughput of the device (TFLOP/s). */

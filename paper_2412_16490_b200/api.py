@@ -462,12 +462,14 @@ class Engine:
 
     KERNEL_CLASSES = ("point_query", "qp", "step_coarse", "pairs", "step_mesh", "fk", "finalize", "pairs_big")
     OP_NAMES = ("plane_tests", "triangle_tests", "qp_column_sweeps", "qp_solves", "gjk_iters", "support_verts",
-                "epa_iters", "point_queries", "pairs_needed", "epa_overflow")
+                "epa_iters", "point_queries", "pairs_needed", "epa_overflow",
+                "gjk_pairs_le4", "gjk_pairs_le8", "gjk_pairs_le16", "gjk_pairs_le32", "gjk_pairs_le64",
+                "gjk_pairs_gt64", "gjk_cycle_jumps", "gjk_iters_skipped", "reserved18", "reserved19")
 
     def profile(self) -> dict:
         ms = (C.c_double * 8)()
         launches = (C.c_longlong * 8)()
-        ops = (C.c_ulonglong * 10)()
+        ops = (C.c_ulonglong * 20)()
         N.check(N.lib().grasp_ctx_profile(self._ctx, ms, launches, ops))
         return {"ms": dict(zip(self.KERNEL_CLASSES, list(ms))),
                 "launches": dict(zip(self.KERNEL_CLASSES, list(launches))),

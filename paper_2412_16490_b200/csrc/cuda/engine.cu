@@ -119,7 +119,7 @@ struct grasp_ctx {
     const char* v = std::getenv("GRASP_PAIRS");
     if (v && std::string(v) == "warp") return 1;
     if (v && std::string(v) == "thread") return 2;
-    if (v && std::string(v) == "list1") return 3;
+    if (v && std::string(v) == "interleaved") return 3;
     return 0;
   }();
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
@@ -563,9 +563,9 @@ struct grasp_ctx {
         k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.P);
         k_pairs_scatter<<<blocks(n, 128), 128, 0, stream>>>(st, lk, nl, O.P);
         if (pairs_variant == 3)
-          k_pairs_list1<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
+          k_pairs_list_il<<<std::min<long long>(blocks(n, 128), list_grid), 128, 0, stream>>>(H, O, st);
         else
-          k_pairs_list<<<std::min<long long>(blocks(n, 128), list_grid), 128, 0, stream>>>(H, O, st);
+          k_pairs_list<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
         k_pairs_epa<<<blocks(std::min<long long>(n, st.epa_cap), 128), 128, 0, stream>>>(H, O, st);
       }
     });
@@ -761,7 +761,7 @@ int grasp_ctx_create(int device, grasp_ctx** out) {
       // Persistent GJK grid: every resident block slot on every SM.
       int sms = 0, per_sm = 0;
       ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
-      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gdev::k_pairs_list, 128, 0), "occupancy");
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gdev::k_pairs_list_il, 128, 0), "occupancy");
       ctx->list_grid = static_cast<long long>(sms) * std::max(per_sm, 1);
     } catch (...) {
       delete ctx;

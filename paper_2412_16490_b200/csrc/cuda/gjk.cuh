@@ -34,7 +34,7 @@ struct SP {
   D3 w, a, b;
 };
 
-GDEV_FN D3 support(const Hull& h, D3 dir) {
+GDEV_FN D3 support(const Hull& h, D3 dir, int& arg_out) {
   const D3 dl = h.posed ? mulT(h.R, dir) : dir;
   double best = -INFINITY;
   int arg = 0;
@@ -60,7 +60,13 @@ GDEV_FN D3 support(const Hull& h, D3 dir) {
     }
   }
   const D3 v = ldg3(h.verts + 3 * arg);
+  arg_out = arg;
   return h.posed ? mul(h.R, v) + h.t : v;
+}
+
+GDEV_FN D3 support(const Hull& h, D3 dir) {
+  int arg;
+  return support(h, dir, arg);
 }
 
 GDEV_FN SP support_pair(const Hull& A, const Hull& B, D3 dir) {
@@ -69,6 +75,60 @@ GDEV_FN SP support_pair(const Hull& A, const Hull& B, D3 dir) {
   s.b = support(B, -dir);
   s.w = s.a - s.b;
   return s;
+}
+
+// Same, also returning the support vertices as a key (ia | ib << 16).
+GDEV_FN SP support_pair(const Hull& A, const Hull& B, D3 dir, unsigned& key) {
+  SP s;
+  int ia, ib;
+  s.a = support(A, dir, ia);
+  s.b = support(B, -dir, ib);
+  s.w = s.a - s.b;
+  key = (unsigned)ia | ((unsigned)ib << 16);
+  return s;
+}
+
+// Exact cycle detection for GJK (Brent). The loop state at the top of an
+// iteration is the ordered simplex, and every simplex point is a function
+// of its support-vertex pair, so the state is fully described by the keys
+// of its points. Once the state at iteration i equals the one at i - p, the
+// run is periodic, and the state at the iteration cap (geometry.cpp:111,
+// 136-149) is the current one after jumping a multiple of p: the output is
+// unchanged, bit for bit, and the cycling iterations are not executed.
+// (Pairs of hulls with >= 65535 vertices run without detection.)
+struct GjkCycle {
+  unsigned long long s0, s1;
+  int power, lam;
+  bool on;
+};
+
+GDEV_FN void cycle_init(GjkCycle& c, int nva, int nvb) {
+  c.s0 = c.s1 = ~0ull;
+  c.power = 1;
+  c.lam = 0;
+  c.on = nva < 65535 && nvb < 65535;
+}
+
+// Returns the number of iterations to jump (0 when no cycle was closed).
+GDEV_FN int cycle_step(GjkCycle& c, const unsigned (&key)[4], int ns, int iter) {
+  if (!c.on) return 0;
+  unsigned k[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) k[i] = i < ns ? key[i] : ~0u;
+  const unsigned long long a = (unsigned long long)k[0] | ((unsigned long long)k[1] << 32);
+  const unsigned long long b = (unsigned long long)k[2] | ((unsigned long long)k[3] << 32);
+  if (a == c.s0 && b == c.s1) {
+    c.on = false;
+    return ((kGjkMaxIters - iter) / c.lam) * c.lam;
+  }
+  if (c.lam == c.power) {
+    c.s0 = a;
+    c.s1 = b;
+    c.power <<= 1;
+    c.lam = 0;
+  }
+  ++c.lam;
+  return 0;
 }
 
 // Eigen::FullPivLU::solve restated for a compile-time size S (complete
@@ -411,7 +471,7 @@ struct PairResult {
   double d;
   D3 pa, pb, n;
   int flags;
-  unsigned n_support, gjk_iters, epa_iters;  // op counters
+  unsigned n_support, gjk_iters, epa_iters, gjk_skipped;  // op counters
 };
 
 struct EpaFace {
@@ -640,14 +700,22 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
   out.epa_iters = 0;
   // The simplex is only ever indexed by compile-time constants (unrolled
   // loops with predicates) so it stays in registers.
+  out.gjk_skipped = 0;
   ns = 1;
-  simp[0] = support_pair(A, B, mk(1, 0, 0));
+  unsigned key[4];
+  simp[0] = support_pair(A, B, mk(1, 0, 0), key[0]);
   simp[1] = simp[2] = simp[3] = simp[0];
+  key[1] = key[2] = key[3] = key[0];
+  GjkCycle cyc;
+  cycle_init(cyc, A.nv, B.nv);
   bool overlap = false;
   Simplex sx;
   // One closest_on_simplex call site (code size): call kGjkMaxIters is the
   // iteration-cap estimate on the unreduced simplex (geometry.cpp:136-149).
   for (int iter = 0;; ++iter) {
+    const int jump = cycle_step(cyc, key, ns, iter);
+    iter += jump;
+    out.gjk_skipped += jump;
     sx = closest_on_simplex(simp, ns);
     if (iter == kGjkMaxIters) {
       D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
@@ -671,22 +739,25 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
       return false;
     }
     SP red[4];
+    unsigned rkey[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int src = sx.keep[i];
       red[i] = simp[0];
-      if (src == 1) red[i] = simp[1];
-      if (src == 2) red[i] = simp[2];
-      if (src == 3) red[i] = simp[3];
+      rkey[i] = key[0];
+      if (src == 1) red[i] = simp[1], rkey[i] = key[1];
+      if (src == 2) red[i] = simp[2], rkey[i] = key[2];
+      if (src == 3) red[i] = simp[3], rkey[i] = key[3];
     }
     ns = sx.nkeep;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) simp[i] = red[i];
+    for (int i = 0; i < 4; ++i) simp[i] = red[i], key[i] = rkey[i];
     if (sx.contains || sqrt(sx.dist2) < kTouchTol * scale) {
       overlap = true;
       break;
     }
-    const SP w = support_pair(A, B, -sx.v);
+    unsigned wkey;
+    const SP w = support_pair(A, B, -sx.v, wkey);
     ++out.n_support;
     ++out.gjk_iters;
     const double gap = sx.dist2 - dot(sx.v, w.w);
@@ -697,7 +768,7 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
     if (gap <= kGjkRelTol * sx.dist2 + 1e-300 || repeat || ns == 4) break;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (i == ns) simp[i] = w;
+      if (i == ns) simp[i] = w, key[i] = wkey;
     ++ns;
   }
   if (!overlap) {

@@ -363,6 +363,17 @@ __device__ inline PairResult link_part_distance(const DevHand& H, const DevObjec
   return signed_distance(A, B, scale, scratch);
 }
 
+// Profiling: GJK closest-point calls of one pair, total and histogram.
+__device__ __forceinline__ void count_gjk(unsigned long long* ops, unsigned calls, unsigned skipped) {
+  atomicAdd(ops + kOpGjkIters, (unsigned long long)calls);
+  if (skipped) {
+    atomicAdd(ops + kOpGjkCycleJumps, 1ull);
+    atomicAdd(ops + kOpGjkItersSkipped, (unsigned long long)skipped);
+  }
+  const int b = calls <= 4 ? 0 : calls <= 8 ? 1 : calls <= 16 ? 2 : calls <= 32 ? 3 : calls <= 64 ? 4 : 5;
+  atomicAdd(ops + kOpGjkHist + b, 1ull);
+}
+
 __device__ __forceinline__ void store_pair(double* o, const PairResult& r) {
   o[0] = r.d;
   st3(o + 1, r.pa);
@@ -433,7 +444,7 @@ __global__ void __launch_bounds__(128) k_pairs(DevHand H, DevObject O, DevState 
   if (st.ops) {
     const unsigned nv = (H.link_vbeg[link + 1] - H.link_vbeg[link]) + (O.part_vbeg[part + 1] - O.part_vbeg[part]);
     atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * nv);
-    atomicAdd(st.ops + kOpGjkIters, (unsigned long long)r.gjk_iters + 1);
+    count_gjk(st.ops, r.gjk_iters + 1, r.gjk_skipped);
     atomicAdd(st.ops + kOpEpaIters, (unsigned long long)r.epa_iters);
     atomicAdd(st.ops + kOpPairsNeeded, 1ull);
     if (r.flags & kPairOverflow) atomicAdd(st.ops + kOpEpaOverflow, 1ull);
@@ -615,7 +626,8 @@ __device__ __forceinline__ void store_separated(double* o, const Simplex& sx, co
   o[10] = 0;
 }
 
-// Pass 2: GJK over the pair list, persistent and iteration-interleaved. A
+// Pass 2 variant (GRASP_PAIRS=interleaved): GJK over the pair list,
+// persistent and iteration-interleaved. A
 // lane owns one pair at a time and runs one GJK iteration (geometry.cpp:
 // 105-164) per trip of the warp loop; a lane whose pair finished takes the
 // next list entry at the top of the following trip. Lanes therefore stay
@@ -625,47 +637,58 @@ __device__ __forceinline__ void store_separated(double* o, const Simplex& sx, co
 // Results are those of gjk_phase: the same operations run per pair, only
 // interleaved with other pairs. Overlapping pairs pass their terminal
 // simplex to k_pairs_epa.
-__global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHand H, DevObject O, DevState st) {
+__global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list_il(DevHand H, DevObject O, DevState st) {
   const int lane = threadIdx.x & 31;
   const int total = *(volatile int*)st.pair_count;
   int* cursor = st.pair_count + 2;
   int slot = -1, ns = 0, iter = 0;
   bool fresh = false, exhausted = false;
-  unsigned nsup = 0;
+  unsigned nsup = 0, skipped = 0;
   SP simp[4];
+  unsigned key[4];
+  GjkCycle cyc;
   double scale = 1.0;
   Hull A, B;
   Simplex sx;
+  auto finish_stats = [&]() {
+    if (st.ops) {
+      atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)nsup * (A.nv + B.nv));
+      count_gjk(st.ops, iter + 1 - skipped, skipped);
+      atomicAdd(st.ops + kOpPairsNeeded, 1ull);
+    }
+  };
   while (true) {
     D3 dir = mk(1, 0, 0);
     if (slot >= 0) {
+      const int jump = cycle_step(cyc, key, ns, iter);
+      iter += jump;
+      skipped += jump;
       // closest point, reduce, overlap test (geometry.cpp:112-120)
       sx = closest_on_simplex(simp, ns);
       if (iter >= kGjkMaxIters) {
         // iteration cap: estimate from the unreduced simplex (geometry.cpp:136-149)
+        finish_stats();
         store_separated(st.pairs + (size_t)slot * 12, sx, simp, false);
         slot = -1;
       }
     }
     if (slot >= 0) {
       SP red[4];
+      unsigned rkey[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int src = sx.keep[i];
         red[i] = simp[0];
-        if (src == 1) red[i] = simp[1];
-        if (src == 2) red[i] = simp[2];
-        if (src == 3) red[i] = simp[3];
+        rkey[i] = key[0];
+        if (src == 1) red[i] = simp[1], rkey[i] = key[1];
+        if (src == 2) red[i] = simp[2], rkey[i] = key[2];
+        if (src == 3) red[i] = simp[3], rkey[i] = key[3];
       }
       ns = sx.nkeep;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) simp[i] = red[i];
+      for (int i = 0; i < 4; ++i) simp[i] = red[i], key[i] = rkey[i];
       if (sx.contains || sqrt(sx.dist2) < kTouchTol * scale) {
-        if (st.ops) {
-          atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)nsup * (A.nv + B.nv));
-          atomicAdd(st.ops + kOpGjkIters, (unsigned long long)iter + 1);
-          atomicAdd(st.ops + kOpPairsNeeded, 1ull);
-        }
+        finish_stats();
         write_epa_job(st, slot, simp, ns);
         slot = -1;
       } else {
@@ -693,12 +716,16 @@ __global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHa
     }
     if (!__any_sync(kFull, slot >= 0)) break;
     if (slot < 0) continue;
-    const SP w = support_pair(A, B, dir);
+    unsigned wkey;
+    const SP w = support_pair(A, B, dir, wkey);
     if (fresh) {
       simp[0] = simp[1] = simp[2] = simp[3] = w;
+      key[0] = key[1] = key[2] = key[3] = wkey;
       ns = 1;
       iter = 0;
       nsup = 1;
+      skipped = 0;
+      cycle_init(cyc, A.nv, B.nv);
       fresh = false;
       continue;
     }
@@ -711,29 +738,21 @@ __global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHa
     for (int i = 0; i < 4; ++i)
       if (i < ns && nrm(simp[i].w - w.w) < 1e-14 * scale) repeat = true;
     const bool done = gap <= kGjkRelTol * sx.dist2 + 1e-300 || repeat || ns == 4;
-    if (!done) {
+    if (done) {
+      finish_stats();
+      store_separated(st.pairs + (size_t)slot * 12, sx, simp, true);
+      slot = -1;
+    } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (i == ns) simp[i] = w;
+        if (i == ns) simp[i] = w, key[i] = wkey;
       ++ns;
-    }
-    if (done || iter >= kGjkMaxIters) {
-      if (st.ops) {
-        atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)nsup * (A.nv + B.nv));
-        atomicAdd(st.ops + kOpGjkIters, (unsigned long long)iter + 1);
-        atomicAdd(st.ops + kOpPairsNeeded, 1ull);
-      }
-      if (done) {
-        store_separated(st.pairs + (size_t)slot * 12, sx, simp, true);
-        slot = -1;
-      }  // else: capped, the next trip's closest_on_simplex gives the estimate
     }
   }
 }
 
-// Non-interleaved variant (one pair per thread start to end; A/B reference
-// for the kernel above, GRASP_PAIRS=list1).
-__global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list1(DevHand H, DevObject O, DevState st) {
+// Pass 2 (default): GJK, one thread per listed pair from start to end.
+__global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHand H, DevObject O, DevState st) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *st.pair_count) return;
   const int slot = st.pair_list[i];
@@ -746,7 +765,7 @@ __global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list1(DevH
   const bool overlap = gjk_phase(A, B, scale, r, simp, ns);
   if (st.ops) {
     atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * (A.nv + B.nv));
-    atomicAdd(st.ops + kOpGjkIters, (unsigned long long)r.gjk_iters + 1);
+    count_gjk(st.ops, r.gjk_iters + 1, r.gjk_skipped);
     atomicAdd(st.ops + kOpPairsNeeded, 1ull);
   }
   if (!overlap) {
@@ -864,7 +883,7 @@ __global__ void __launch_bounds__(128) k_pairs_warp(DevHand H, DevObject O, DevS
       store_pair(st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12, r);
       if (st.ops) {
         atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * (A.nv + B.nv));
-        atomicAdd(st.ops + kOpGjkIters, (unsigned long long)r.gjk_iters + 1);
+        count_gjk(st.ops, r.gjk_iters + 1, r.gjk_skipped);
         atomicAdd(st.ops + kOpEpaIters, (unsigned long long)r.epa_iters);
       }
       if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);

@@ -152,7 +152,10 @@ enum OpCounter {
   kOpPointQueries = 7,
   kOpPairsNeeded = 8,    // (link, part) pairs that needed GJK (not culled)
   kOpEpaOverflow = 9,    // pairs redone with the large EPA buffer
-  kNumOps = 10
+  kOpGjkHist = 10,       // 10..15: pairs by GJK iterations <=4, <=8, <=16, <=32, <=64, >64
+  kOpGjkCycleJumps = 16, // pairs whose GJK state cycle was fast-forwarded to the iteration cap
+  kOpGjkItersSkipped = 17,
+  kNumOps = 20
 };
 
 }  // namespace gdev
