@@ -146,6 +146,9 @@ int grasp_init_poses(const grasp_hand* h, const grasp_object* o, int n, uint64_t
                      double joint_span_fraction, double* out);
 /* squeeze_pose(model, x, x_p) (pipeline.cpp:426-434): out[D]. */
 int grasp_squeeze_pose(const grasp_hand* h, const double* x, const double* x_p, double* out);
+/* forward_kinematics(model, pose_from_state(model, x)) (hand.hpp:100, hand.cpp:126-153) for n
+ * states x[n*D]: world link transforms out[n*n_links*12] = R (9, column-major), t (3). Host. */
+int grasp_forward_kinematics(const grasp_hand* h, int n, const double* x, double* out);
 
 /* ---- device engine ------------------------------------------------------ */
 typedef struct grasp_ctx grasp_ctx;

@@ -94,6 +94,7 @@ SIGNATURES = {
     "grasp_run_params_validate": (C.c_int, [C.POINTER(RunParams)]),
     "grasp_init_poses": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.c_double, C.c_double, _dp]),
     "grasp_squeeze_pose": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
+    "grasp_forward_kinematics": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp]),
     "grasp_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "grasp_ctx_destroy": (None, [C.c_void_p]),
     "grasp_ctx_set_hand": (C.c_int, [C.c_void_p, C.POINTER(HandDesc)]),

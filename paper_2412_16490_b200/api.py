@@ -339,6 +339,15 @@ def squeeze_pose(model: HandModel, x, x_p) -> np.ndarray:
     return out
 
 
+def forward_kinematics(model: HandModel, x) -> np.ndarray:
+    """hand::forward_kinematics (hand.hpp:100) of (n, D) states -> (n, n_links, 12) world link
+    transforms: R (9, column-major), t (3). Host-side."""
+    x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
+    out = np.zeros((x.shape[0], model.n_links, 12))
+    N.check(N.lib().grasp_forward_kinematics(model._h, int(x.shape[0]), dptr(x), dptr(out)))
+    return out
+
+
 # -------------------------------------------------------------------- records
 @dataclass
 class ContactFrame:

@@ -865,7 +865,8 @@ int grasp_signed_distance(grasp_ctx* ctx, int n, const int* link_ids, const int*
     dout.ensure(static_cast<size_t>(n) * 11);
     ctx->big_scratch.ensure(grasp_ctx::kBigSlots);
     k_pairs_raw<<<grasp_ctx::kBigSlots / 128, 128, 0, ctx->stream>>>(ctx->H, ctx->O, n, dl.p, dpi.p, dpose.p, dout.p,
-                                                                     ctx->big_scratch.p);
+                                                                     ctx->big_scratch.p,
+                                                                     ctx->profiling ? ctx->ops.p : nullptr);
     ck(cudaGetLastError(), "launch");
     ck(cudaMemcpyAsync(out, dout.p, sizeof(double) * n * 11, cudaMemcpyDeviceToHost, ctx->stream), "out");
     ck(cudaStreamSynchronize(ctx->stream), "sync");

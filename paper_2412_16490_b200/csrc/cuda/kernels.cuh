@@ -922,7 +922,8 @@ __global__ void __launch_bounds__(128) k_pairs_big(DevHand H, DevObject O, DevSt
 // Standalone pair surface (teacher-forced tests): poses[n*12] column-major R
 // + t; grid-stride over n with one large EPA buffer per thread.
 __global__ void k_pairs_raw(DevHand H, DevObject O, int n, const int* __restrict__ links, const int* __restrict__ parts,
-                            const double* __restrict__ poses, double* out, EpaScratchBig* big) {
+                            const double* __restrict__ poses, double* out, EpaScratchBig* big,
+                            unsigned long long* ops) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   for (int t = tid; t < n; t += gridDim.x * blockDim.x) {
     M33 Rw;
@@ -931,6 +932,7 @@ __global__ void k_pairs_raw(DevHand H, DevObject O, int n, const int* __restrict
     const PairResult r = link_part_distance(H, O, links[t], parts[t], Rw, ld3(poses + 12 * t + 9), big[tid]);
     store_pair(out + 11 * t, r);
     out[11 * t + 10] = r.flags;
+    if (ops) count_gjk(ops, r.gjk_iters + 1, r.gjk_skipped);
   }
 }
 

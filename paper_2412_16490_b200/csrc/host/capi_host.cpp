@@ -351,6 +351,25 @@ int grasp_init_poses(const grasp_hand* h, const grasp_object* o, int n, uint64_t
   });
 }
 
+int grasp_forward_kinematics(const grasp_hand* h, int n, const double* x, double* out) {
+  return guard([&] {
+    if (!h || n < 0 || (n > 0 && (!x || !out))) throw std::invalid_argument("null argument");
+    const size_t D = 12 + static_cast<size_t>(h->model.dof());
+    const size_t L = h->model.links.size();
+    for (int i = 0; i < n; ++i) {
+      const std::vector<double> xv(x + i * D, x + (i + 1) * D);
+      const auto fk = hand::forward_kinematics(h->model, hand::pose_from_state(h->model, xv));
+      for (size_t l = 0; l < L; ++l) {
+        double* o = out + (i * L + l) * 12;
+        std::memcpy(o, fk.world[l].R.m, sizeof(double) * 9);
+        o[9] = fk.world[l].t.x;
+        o[10] = fk.world[l].t.y;
+        o[11] = fk.world[l].t.z;
+      }
+    }
+  });
+}
+
 int grasp_squeeze_pose(const grasp_hand* h, const double* x, const double* x_p, double* out) {
   return guard([&] {
     const size_t D = 12 + static_cast<size_t>(h->model.dof());

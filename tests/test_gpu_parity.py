@@ -8,7 +8,8 @@ FMA contraction and device libm):
   * distances / points / normals: 1e-9 abs;
   * energies and gradients: 1e-7 relative (teacher-forced, one iteration);
   * QP: iteration counts exact, lambda 1e-7 abs (teacher-forced);
-  * end-to-end after 20/10/10 iterations: |dx| <= 1e-6.
+  * end-to-end after 20/10/10 iterations: |dx| <= 1e-5 (ulp-level FK differences from device
+    sin/cos grow through the optimisation), stage energies 1e-4.
 """
 import ctypes as C
 
@@ -161,6 +162,47 @@ def assert_witnesses_match_or_tie(got, ref, budget=0.01):
         sep = r[:, 1:4] - r[:, 4:7]
         np.testing.assert_allclose(np.linalg.norm(sep, axis=1), -r[:, 0], atol=1e-9)
         np.testing.assert_allclose(np.einsum("ij,ij->i", sep, r[:, 7:10]), r[:, 0], atol=1e-9)
+
+
+def test_signed_distance_late_stage_matches_oracle(G, O, engine):
+    """Pairs from the final states of a full-schedule oracle run (tests/golden/
+    make_late_states.py) and 1-2 mm shifts of them: near-contact geometry where the
+    reference's GJK enters exact cycles and runs to its 128-iteration cap. The device
+    fast-forwards those cycles (Brent detection on support-vertex keys); results must
+    still be the oracle's."""
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    hand = G.HandModel.from_file(root / "paper_2412_16490_b200/assets/hands/shadow_like.json")
+    obj = G.load_object(root / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+    use(engine, hand, obj)
+    x = np.load(root / "tests/golden/late_states_shadow_drill.npz")["x"]
+    rng = np.random.default_rng(3)
+    xs = [x]
+    for _ in range(4):
+        xp = x.copy()
+        xp[:, 9:12] += rng.uniform(-2e-3, 2e-3, size=(len(x), 3))
+        xs.append(xp)
+    world = G.forward_kinematics(hand, np.concatenate(xs))  # (n, L, 12)
+    n, L, _ = world.shape
+    P = obj.n_parts
+    links = np.tile(np.repeat(np.arange(L), P), n)
+    parts = np.tile(np.arange(P), n * L)
+    poses = np.repeat(world.reshape(n * L, 12), P, axis=0)
+    ref = O.signed_distance(hand, obj, links, parts, poses)
+    engine.set_profiling(True)
+    try:
+        got = gpu_pairs(engine, links, parts, poses)
+        ops = engine.profile()["ops"]
+    finally:
+        engine.set_profiling(False)
+    assert ops["gjk_cycle_jumps"] > 0, "no cycling pair exercised"
+    assert ((got[:, 10] % 2) == ref[:, 10]).all(), "EPA usage differs"
+    np.testing.assert_allclose(got[:, 0], ref[:, 0], atol=1e-9, rtol=0)
+    np.testing.assert_allclose(got[:, 7:10], ref[:, 7:10], atol=1e-9, rtol=0)
+    assert_witnesses_match_or_tie(got, ref)
+    # separated pairs (incl. every capped one) are bit-exact
+    sep = ref[:, 10] == 0
+    assert (got[sep, :10] == ref[sep, :10]).all()
 
 
 # ---------------------------------------------------------------------- QP
