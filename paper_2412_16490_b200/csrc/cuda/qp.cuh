@@ -44,11 +44,16 @@ __device__ __forceinline__ double qp_group_max(double v, int base, int cnt) {
   return s;
 }
 
+// Per-contact blocks are padded to an odd number of doubles so that the
+// m contacts a warp reads at once (lanes of one contact broadcast) fall in
+// distinct shared-memory bank pairs.
+constexpr int kQpWStride = kMaxEdges | 1;        // W: [6][m][ws] with ws = k | 1
+constexpr int kQpGStride = (7 * kMaxEdges) | 1;  // G, Z: [m][gs] with gs = 7k | 1, rows of 7
 struct QpSmem {
   double frame[kMaxTips * 12];
-  double W[6 * kMaxTips * kMaxEdges];   // row-major 6 x n
-  double Gm[kMaxTips * kMaxEdges * 7];  // B^-1 U, n x 7
-  double Zm[kMaxTips * kMaxEdges * 7];  // G (I + U^T G)^-1, n x 7
+  double W[6 * kMaxTips * kQpWStride];  // W(r, c, e) = W[r * m * ws + c * ws + e]
+  double Gm[kMaxTips * kQpGStride];     // B^-1 U: G(c, e, p) = Gm[c * gs + e * 7 + p]
+  double Zm[kMaxTips * kQpGStride];     // G (I + U^T G)^-1, same layout
   double C[49];
 };
 
@@ -72,6 +77,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
   const int k = KT > 0 ? KT : P.k;
   const int m = MT > 0 ? MT : m_rt;
   const int n = m * k, M = m + 1 + n;
+  const int ws = k | 1, wn = m * ws, gs = (7 * k) | 1;
 
   // Frames.
   if (lane < m) {
@@ -95,20 +101,20 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     for (int j = 0; j < k; ++j) {
       const D3 edge = nn + P.mu * (P.cos_t[j] * d + P.sin_t[j] * e);
       const D3 tq = cross(p, edge);
-      const int col = c * k + j;
-      s.W[0 * n + col] = edge.x;
-      s.W[1 * n + col] = edge.y;
-      s.W[2 * n + col] = edge.z;
-      s.W[3 * n + col] = tq.x;
-      s.W[4 * n + col] = tq.y;
-      s.W[5 * n + col] = tq.z;
+      const int col = c * ws + j;
+      s.W[0 * wn + col] = edge.x;
+      s.W[1 * wn + col] = edge.y;
+      s.W[2 * wn + col] = edge.z;
+      s.W[3 * wn + col] = tq.x;
+      s.W[4 * wn + col] = tq.y;
+      s.W[5 * wn + col] = tq.z;
     }
     for (int q = 0; q < 7; ++q) {
       double bs = 0.0;
-      for (int j = 0; j < k; ++j) bs += q < 6 ? sqrt2 * s.W[q * n + c * k + j] : sqrt_rho;
+      for (int j = 0; j < k; ++j) bs += q < 6 ? sqrt2 * s.W[q * wn + c * ws + j] : sqrt_rho;
       for (int j = 0; j < k; ++j) {
-        const double u = q < 6 ? sqrt2 * s.W[q * n + c * k + j] : sqrt_rho;
-        s.Gm[(c * k + j) * 7 + q] = (u - betap * bs) / a_diag;
+        const double u = q < 6 ? sqrt2 * s.W[q * wn + c * ws + j] : sqrt_rho;
+        s.Gm[c * gs + j * 7 + q] = (u - betap * bs) / a_diag;
       }
     }
   }
@@ -123,8 +129,9 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     q += p;
     double acc = 0.0;
     for (int i = 0; i < n; ++i) {
-      const double u = p < 6 ? sqrt2 * s.W[p * n + i] : sqrt_rho;
-      acc += u * s.Gm[i * 7 + q];
+      const int ci = i / k, ei = i - ci * k;
+      const double u = p < 6 ? sqrt2 * s.W[p * wn + ci * ws + ei] : sqrt_rho;
+      acc += u * s.Gm[ci * gs + ei * 7 + q];
     }
     const double v = acc + (p == q ? 1.0 : 0.0);
     s.C[p * 7 + q] = v;
@@ -151,10 +158,11 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     }
     // Z^T = C^-1 G^T: solve C z = g for each of this lane's rows of G.
     for (int i = lane; i < n; i += 32) {
+      const int gi = (i / k) * gs + (i % k) * 7;
       double y[7];
 #pragma unroll
       for (int r = 0; r < 7; ++r) {
-        double v = s.Gm[i * 7 + r];
+        double v = s.Gm[gi + r];
 #pragma unroll
         for (int q = 0; q < r; ++q) v -= L[r][q] * y[q];
         y[r] = v / L[r][r];
@@ -167,7 +175,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
         y[r] = v / L[r][r];
       }
 #pragma unroll
-      for (int r = 0; r < 7; ++r) s.Zm[i * 7 + r] = y[r];
+      for (int r = 0; r < 7; ++r) s.Zm[gi + r] = y[r];
     }
   }
   __syncwarp();
@@ -181,8 +189,8 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
   const double rho = P.rho, sigma = P.sigma, alpha = P.alpha;
   const double inv_a = 1.0 / a_diag;
   const double inv_rho = 1.0 / rho;
-  const double* Gl = s.Gm + c * k * 7;
-  const double* Zl = s.Zm + c * k * 7;
+  const double* Gl = s.Gm + c * gs;
+  const double* Zl = s.Zm + c * gs;
 
   double x[KMAX], zid[KMAX], yid[KMAX], q[KMAX], xs[KMAX];
   double zc, yc, ztot, ytot;
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
       const int i = c * k + e;
       x[e] = warm ? wx[j * n + i] : 0.0;
       yid[e] = warm ? wy[j * M + m + 1 + i] : 0.0;
-      q[e] = (-2.0 * P.beta) * (tsign * s.W[axis * n + i]);
+      q[e] = (-2.0 * P.beta) * (tsign * s.W[axis * wn + c * ws + e]);
     } else {
       x[e] = yid[e] = q[e] = 0.0;
     }
@@ -301,7 +309,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
         double acc = 0.0;
 #pragma unroll
         for (int e = 0; e < KMAX; ++e)
-          if (e < k) acc += s.W[r * n + c * k + e] * x[e];
+          if (e < k) acc += s.W[r * wn + c * ws + e] * x[e];
         wx6[r] = qp_group_sum<MT>(acc, base, m);
       }
       double rd = 0.0;
@@ -310,7 +318,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
         if (e < k) {
           double px = 0.0;
 #pragma unroll
-          for (int r = 0; r < 6; ++r) px += s.W[r * n + c * k + e] * wx6[r];
+          for (int r = 0; r < 6; ++r) px += s.W[r * wn + c * ws + e] * wx6[r];
           const double dual = (2.0 * px + ((yc + ytot) + yid[e])) + q[e];
           rd = fmax(rd, fabs(dual));
         }
@@ -358,7 +366,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     double acc = 0.0;
 #pragma unroll
     for (int e = 0; e < KMAX; ++e)
-      if (e < k) acc += s.W[r * n + c * k + e] * xs[e];
+      if (e < k) acc += s.W[r * wn + c * ws + e] * xs[e];
     const double wl = qp_group_sum<MT>(acc, base, m);
     res[r] = P.beta * (r == axis ? tsign : 0.0) - wl;
   }
