@@ -80,7 +80,9 @@ struct grasp_ctx {
   DevObject O{};
   DevBuf<int> o_fbeg, o_vbeg;
   DevBuf<double> o_faces, o_verts, o_centroid, o_half, o_obb, o_part_sphere, o_face_sphere;
-  DevBuf<float4> o_face_sphere32;
+  DevBuf<float4> o_face_sphere32, o_cluster_sphere32, o_face_box32;
+  DevBuf<double4> o_face_plane;
+  DevBuf<int> o_part_cbeg, o_cluster_fbeg;
 
   // Bounding sphere (AABB center, max vertex distance, relative slack) of
   // each vertex range [begin[i], begin[i+1]).
@@ -385,10 +387,114 @@ struct grasp_ctx {
                               std::nextafter(std::nextafter(r, 1e30f), 1e30f) * (1.0f + 1e-6f));
     }
     o_face_sphere32.upload(face32, s);
+    // Thin box per face (point-query culling): axes from the longest edge
+    // and the normal, rounded to fp32; extents measured in double along the
+    // rounded axes (+ relative and absolute pad), so the box contains the
+    // triangle exactly in the rounded frame.
+    std::vector<float4> box32(4 * static_cast<size_t>(d->n_faces));
+    for (int f = 0; f < d->n_faces; ++f) {
+      const double* F = faces.data() + static_cast<size_t>(f) * kFaceStride;
+      const double* V[3] = {F, F + 3, F + 6};
+      int e0 = 0;
+      double best = -1.0;
+      for (int e = 0; e < 3; ++e) {
+        const double* a = V[e];
+        const double* b = V[(e + 1) % 3];
+        const double l2 = (b[0] - a[0]) * (b[0] - a[0]) + (b[1] - a[1]) * (b[1] - a[1]) + (b[2] - a[2]) * (b[2] - a[2]);
+        if (l2 > best) {
+          best = l2;
+          e0 = e;
+        }
+      }
+      double u[3], n[3], v[3];
+      const double* a = V[e0];
+      const double* b = V[(e0 + 1) % 3];
+      for (int k = 0; k < 3; ++k) u[k] = b[k] - a[k];
+      double lu = std::sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+      if (!(lu > 1e-30)) {
+        u[0] = 1, u[1] = u[2] = 0;
+        lu = 1;
+      }
+      for (double& x : u) x /= lu;
+      if (F[13] != 0.0) {
+        n[0] = F[9], n[1] = F[10], n[2] = F[11];
+      } else {
+        // degenerate face: any unit vector orthogonal to u
+        const double t[3] = {std::fabs(u[0]) < 0.9 ? 1.0 : 0.0, std::fabs(u[0]) < 0.9 ? 0.0 : 1.0, 0.0};
+        n[0] = u[1] * t[2] - u[2] * t[1], n[1] = u[2] * t[0] - u[0] * t[2], n[2] = u[0] * t[1] - u[1] * t[0];
+        const double ln = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+        for (double& x : n) x /= ln;
+      }
+      v[0] = n[1] * u[2] - n[2] * u[1], v[1] = n[2] * u[0] - n[0] * u[2], v[2] = n[0] * u[1] - n[1] * u[0];
+      float uf[3], vf[3], nf[3], of[3];
+      double o[3];
+      for (int k = 0; k < 3; ++k) {
+        uf[k] = static_cast<float>(u[k]);
+        vf[k] = static_cast<float>(v[k]);
+        nf[k] = static_cast<float>(n[k]);
+        o[k] = (V[0][k] + V[1][k] + V[2][k]) / 3.0;
+        of[k] = static_cast<float>(o[k]);
+      }
+      double h[3] = {0, 0, 0};
+      for (int q = 0; q < 3; ++q) {
+        const double r[3] = {V[q][0] - of[0], V[q][1] - of[1], V[q][2] - of[2]};
+        h[0] = std::max(h[0], std::fabs(r[0] * uf[0] + r[1] * uf[1] + r[2] * uf[2]));
+        h[1] = std::max(h[1], std::fabs(r[0] * vf[0] + r[1] * vf[1] + r[2] * vf[2]));
+        h[2] = std::max(h[2], std::fabs(r[0] * nf[0] + r[1] * nf[1] + r[2] * nf[2]));
+      }
+      float hf[3];
+      for (int k = 0; k < 3; ++k)
+        hf[k] = std::nextafter(static_cast<float>(h[k] * (1.0 + 1e-6) + 1e-9), 1e30f);
+      float4* B = box32.data() + 4 * static_cast<size_t>(f);
+      B[0] = make_float4(of[0], of[1], of[2], hf[0]);
+      B[1] = make_float4(uf[0], uf[1], uf[2], hf[1]);
+      B[2] = make_float4(vf[0], vf[1], vf[2], hf[2]);
+      B[3] = make_float4(nf[0], nf[1], nf[2], 0.0f);
+    }
+    o_face_box32.upload(box32, s);
+    std::vector<double4> planes(d->n_faces);
+    for (int f = 0; f < d->n_faces; ++f) {
+      const double* F = faces.data() + static_cast<size_t>(f) * kFaceStride;
+      planes[f] = F[13] != 0.0 ? make_double4(F[9], F[10], F[11], F[12]) : make_double4(0.0, 0.0, 0.0, INFINITY);
+    }
+    o_face_plane.upload(planes, s);
+    // Face clusters: runs of kFaceCluster consecutive faces inside a part,
+    // each with a sphere containing its faces' spheres (fp32 centre, radius
+    // from the rounded centre in fp64, rounded up).
+    std::vector<int> part_cbeg(P + 1, 0), cluster_fbeg;
+    std::vector<float4> cluster32;
+    for (int p = 0; p < P; ++p) {
+      part_cbeg[p] = static_cast<int>(cluster32.size());
+      for (int a = fbeg[p]; a < fbeg[p + 1]; a += kFaceCluster) {
+        const int b = std::min(fbeg[p + 1], a + kFaceCluster);
+        double c[3] = {0, 0, 0};
+        for (int f = a; f < b; ++f)
+          for (int k = 0; k < 3; ++k) c[k] += face_sphere[4 * f + k] / (b - a);
+        const float cx = static_cast<float>(c[0]), cy = static_cast<float>(c[1]), cz = static_cast<float>(c[2]);
+        double r = 0.0;
+        for (int f = a; f < b; ++f) {
+          const double dx = face_sphere[4 * f] - cx, dy = face_sphere[4 * f + 1] - cy, dz = face_sphere[4 * f + 2] - cz;
+          r = std::max(r, std::sqrt(dx * dx + dy * dy + dz * dz) + face_sphere[4 * f + 3]);
+        }
+        const float r32 = std::nextafter(std::nextafter(static_cast<float>(r * (1.0 + 1e-12)), 1e30f), 1e30f);
+        cluster32.push_back(make_float4(cx, cy, cz, r32 * (1.0f + 1e-6f)));
+        cluster_fbeg.push_back(a);
+      }
+    }
+    part_cbeg[P] = static_cast<int>(cluster32.size());
+    cluster_fbeg.push_back(fbeg[P]);
+    o_part_cbeg.upload(part_cbeg, s);
+    o_cluster_fbeg.upload(cluster_fbeg, s);
+    o_cluster_sphere32.upload(cluster32, s);
     ck(cudaStreamSynchronize(s), "object upload");
     O.part_sphere = o_part_sphere.p;
     O.face_sphere = o_face_sphere.p;
     O.face_sphere32 = o_face_sphere32.p;
+    O.face_box32 = o_face_box32.p;
+    O.face_plane = o_face_plane.p;
+    O.part_cbeg = o_part_cbeg.p;
+    O.cluster_fbeg = o_cluster_fbeg.p;
+    O.cluster_sphere32 = o_cluster_sphere32.p;
     O.P = P;
     O.F = d->n_faces;
     O.part_fbeg = o_fbeg.p;

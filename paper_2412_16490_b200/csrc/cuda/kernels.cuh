@@ -211,6 +211,12 @@ struct PointHit {
 // point_to_mesh (geometry.cpp:527-542) with query_part (:355-395): inside
 // test breaking at the first plane with depth < -1e-12, else the brute-force
 // closest point with strict '<' over faces and parts.
+__device__ __forceinline__ double4 ld_plane(const DevObject& O, int f) {
+  const double2* q = reinterpret_cast<const double2*>(O.face_plane + f);
+  const double2 a = __ldg(q), b = __ldg(q + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
 __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* plane_tests = nullptr,
                                          unsigned* tri_tests = nullptr) {
   PointHit best;
@@ -219,6 +225,7 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
   best.n = mk(0, 0, 1);
   best.part = -1;
   unsigned planes = 0, tris = 0;
+  const float px = (float)p.x, py = (float)p.y, pz = (float)p.z;
   for (int part = 0; part < O.P; ++part) {
     const int f0 = __ldg(O.part_fbeg + part), f1 = __ldg(O.part_fbeg + part + 1);
     // Part-level cull: every point of the part is at least |p - c| - r
@@ -229,22 +236,82 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
       const double lb = nrm(p - ldg3(S)) - __ldg(S + 3) - kCullSlack;
       if (lb > best.d) continue;
     }
-    bool inside = true;
+    // Face clusters (runs of consecutive faces with fp32 bounding spheres):
+    // an upper bound on the part distance (min |p-C| + R) and a seed face,
+    // the smallest sphere lower bound in the nearest cluster.
+    const int c0 = __ldg(O.part_cbeg + part), c1 = __ldg(O.part_cbeg + part + 1);
+    float ubA = INFINITY;
+    int seed_f;
+    {
+      float lb_seed = INFINITY;
+      int seed_c = c0;
+      for (int c = c0; c < c1; ++c) {
+        const float4 S = __ldg(O.cluster_sphere32 + c);
+        const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
+        const float dist = sqrtf(dx * dx + dy * dy + dz * dz);
+        ubA = fminf(ubA, dist + S.w);
+        if (dist - S.w < lb_seed) {
+          lb_seed = dist - S.w;
+          seed_c = c;
+        }
+      }
+      seed_f = __ldg(O.cluster_fbeg + seed_c);
+      const int e = __ldg(O.cluster_fbeg + seed_c + 1);
+      float lbf = INFINITY;
+      for (int f = seed_f; f < e; ++f) {
+        const float4 S = __ldg(O.face_sphere32 + f);
+        const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
+        const float lb = sqrtf(dx * dx + dy * dy + dz * dz) - S.w;
+        if (lb < lbf) {
+          lbf = lb;
+          seed_f = f;
+        }
+      }
+    }
+    // Inside test (query_part, geometry.cpp:369-383): inside iff no face
+    // plane has depth < -1e-12; then the shallowest face in index order
+    // (strict '<'). Whether some plane separates does not depend on the
+    // order the planes are tried, so the seed face's plane (usually a
+    // separating one for outside points) is tried first. Plane records are
+    // (n, n.a) with degenerate faces stored as (0, +inf), which neither
+    // separates nor wins the minimum, i.e. is skipped as in the reference.
+    bool inside;
     double min_depth = INFINITY;
     D3 best_n = mk(0, 0, 1);
-    for (int f = f0; f < f1; ++f) {
-      const double* F = O.faces + (size_t)f * kFaceStride;
+    {
+      const double4 Q = ld_plane(O, seed_f);
       ++planes;
-      if (__ldg(F + 13) == 0.0) continue;  // degenerate face (len < 1e-30)
-      const D3 n = ldg3(F + 9);
-      const double depth = __ldg(F + 12) - dot(n, p);
-      if (depth < -1e-12) {
-        inside = false;
-        break;
+      inside = !((Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z)) < -1e-12);
+    }
+    if (inside) {
+      int f = f0;
+      for (; f + 4 <= f1 && inside; f += 4) {
+        double4 Q[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) Q[i] = ld_plane(O, f + i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (!inside) break;
+          ++planes;
+          const double depth = Q[i].w - (Q[i].x * p.x + Q[i].y * p.y + Q[i].z * p.z);
+          if (depth < -1e-12) {
+            inside = false;
+          } else if (depth < min_depth) {
+            min_depth = depth;
+            best_n = mk(Q[i].x, Q[i].y, Q[i].z);
+          }
+        }
       }
-      if (depth < min_depth) {
-        min_depth = depth;
-        best_n = n;
+      for (; f < f1 && inside; ++f) {
+        const double4 Q = ld_plane(O, f);
+        ++planes;
+        const double depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
+        if (depth < -1e-12) {
+          inside = false;
+        } else if (depth < min_depth) {
+          min_depth = depth;
+          best_n = mk(Q.x, Q.y, Q.z);
+        }
       }
     }
     double sd;
@@ -256,35 +323,62 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
     } else {
       // Brute-force closest point over the faces in index order with strict
       // '<' (geometry.cpp:384-392), evaluated exactly only where it can
-      // matter: a cheap pass over per-face bounding spheres gives an upper
-      // bound ub >= min_f d_f; a face whose lower bound |p-c_f| - r_f exceeds
-      // min(ub, running best) is strictly worse than the final minimum and
-      // is skipped. The argmin and its value are therefore unchanged.
-      // Bounds in fp32 with kCullSlack32 (conservative); exact work in fp64.
-      const float px = (float)p.x, py = (float)p.y, pz = (float)p.z;
-      float ub32 = INFINITY;
-      for (int f = f0; f < f1; ++f) {
-        const float4 S = __ldg(O.face_sphere32 + f);
-        const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
-        ub32 = fminf(ub32, sqrtf(dx * dx + dy * dy + dz * dz) + S.w);
+      // matter. The seed face's exact distance bounds the minimum from
+      // above; faces are then visited in index order (cluster by cluster)
+      // and evaluated exactly only when their lower bounds (cluster sphere,
+      // face sphere, face thin box) do not exceed min(bound, running best):
+      // every skipped face is strictly worse than the final minimum, so the
+      // argmin and its value are unchanged. Bounds in fp32 with
+      // kCullSlack32 (conservative).
+      float bound;
+      {
+        ++tris;
+        const double* F = O.faces + (size_t)seed_f * kFaceStride;
+        const double d_seed = nrm(p - closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6)));
+        bound = fminf(ubA, __double2float_ru(d_seed)) + kCullSlack32;
       }
-      ub32 += kCullSlack32;
       sd = INFINITY;
       float sd32 = INFINITY;
       pt = mk(0, 0, 0);
-      for (int f = f0; f < f1; ++f) {
-        const float4 S = __ldg(O.face_sphere32 + f);
-        const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
-        const float lb = sqrtf(dx * dx + dy * dy + dz * dz) - S.w - kCullSlack32;
-        if (lb > ub32 || lb > sd32) continue;
-        ++tris;
-        const double* F = O.faces + (size_t)f * kFaceStride;
-        const D3 c = closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6));
-        const double d = nrm(p - c);
-        if (d < sd) {
-          sd = d;
-          sd32 = __double2float_ru(d) + kCullSlack32;
-          pt = c;
+      for (int c = c0; c < c1; ++c) {
+        {
+          const float4 S = __ldg(O.cluster_sphere32 + c);
+          const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
+          const float lb = sqrtf(dx * dx + dy * dy + dz * dz) - S.w - kCullSlack32;
+          if (lb > bound || lb > sd32) continue;
+        }
+        const int e = __ldg(O.cluster_fbeg + c + 1);
+        for (int f = __ldg(O.cluster_fbeg + c); f < e; ++f) {
+          const float cut = fminf(bound, sd32);
+          {
+            const float4 S = __ldg(O.face_sphere32 + f);
+            const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
+            if (sqrtf(dx * dx + dy * dy + dz * dz) - S.w - kCullSlack32 > cut) continue;
+          }
+          // Thin-box bound: the triangle lies in a box (centre o, fp32 axes
+          // u, v, n, half extents hu, hv, hn; built on the host from the
+          // rounded axes), so |p - q| for any triangle point q is at least
+          // the distance from p to the box (axes orthonormal to ~1e-7,
+          // covered by the slack). Tight for the long thin faces that
+          // sphere bounds cannot separate.
+          {
+            const float4 B0 = __ldg(O.face_box32 + 4 * f), B1 = __ldg(O.face_box32 + 4 * f + 1);
+            const float4 B2 = __ldg(O.face_box32 + 4 * f + 2), B3 = __ldg(O.face_box32 + 4 * f + 3);
+            const float rx = px - B0.x, ry = py - B0.y, rz = pz - B0.z;
+            const float eu = fmaxf(fabsf(rx * B1.x + ry * B1.y + rz * B1.z) - B0.w, 0.0f);
+            const float ev = fmaxf(fabsf(rx * B2.x + ry * B2.y + rz * B2.z) - B1.w, 0.0f);
+            const float en = fmaxf(fabsf(rx * B3.x + ry * B3.y + rz * B3.z) - B2.w, 0.0f);
+            if (sqrtf(eu * eu + ev * ev + en * en) - kCullSlack32 > cut) continue;
+          }
+          ++tris;
+          const double* F = O.faces + (size_t)f * kFaceStride;
+          const D3 cp = closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6));
+          const double d = nrm(p - cp);
+          if (d < sd) {
+            sd = d;
+            sd32 = __double2float_ru(d) + kCullSlack32;
+            pt = cp;
+          }
         }
       }
       nn = sd > 1e-14 ? (p - pt) / sd : mk(0, 0, 1);

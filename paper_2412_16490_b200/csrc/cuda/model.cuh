@@ -62,7 +62,14 @@ struct DevObject {
   const double* part_sphere;    // [P*4] bounding sphere of the part: center, radius
   const double* face_sphere;    // [F*4] bounding sphere of each triangle: center, radius
   const float4* face_sphere32;  // [F] same in fp32, radius rounded up (culling bounds only)
+  const double4* face_plane;    // [F] (n, n.a) in fp64; degenerate faces (0, 0, 0, +inf)
+  const float4* face_box32;     // [4F] thin box per face: (o, hu), (u, hv), (v, hn), (n, 0); fp32, bounds only
+  const int* part_cbeg;         // [P+1] face clusters of each part
+  const int* cluster_fbeg;      // [NC+1] first face of each cluster (consecutive indices)
+  const float4* cluster_sphere32;  // [NC] fp32 sphere bounding the cluster's face spheres
 };
+
+constexpr int kFaceCluster = 16;  // faces per point-query cluster
 
 // Slack on the fp32 culling bounds: fp32 distances of <= 1 m carry < 1e-7 m
 // rounding error, so 1e-5 m keeps every bound conservative.
