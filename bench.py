@@ -142,6 +142,13 @@ def roofline(prof, hand, cfg, peak_tflops):
     if f is None or ms[dom] <= 0:
         return dom, None
     achieved = f / (ms[dom] * 1e-3) / 1e12
+    # DRAM traffic per launch of the dominant kernel from the committed
+    # `ncu --set full` capture (profiles/), when one exists for it.
+    traffic, traffic_src = None, None
+    cap = {"qp": "profiles/r01_ncu_qp_full_v2.json"}.get(dom)
+    if cap and (ROOT / cap).exists():
+        traffic = json.loads((ROOT / cap).read_text()).get("traffic_bytes_per_launch")
+        traffic_src = cap + " (dram__bytes_read.sum + dram__bytes_write.sum, bytes per launch)"
     return dom, {
         "bound": "fp64",
         "kernel": dom,
@@ -149,7 +156,8 @@ def roofline(prof, hand, cfg, peak_tflops):
         "peak": round(peak_tflops, 3),
         "unit": "TFLOP/s",
         "frac": round(achieved / peak_tflops, 4),
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_source": traffic_src,
         "share_of_step": round(ms[dom] / total_ms, 3),
         "peak_source": "measured fp64 FMA micro-benchmark on this GPU (MEASURED_PEAKS.json has no fp64 entry)",
         "flop_model": "SURVEY 8(d): plane test 7, closest-on-triangle 64, ADMM column-sweep 45n+6M+100+3n, "
