@@ -53,8 +53,8 @@ struct QpSmem {
   double frame[kMaxTips * 12];
   double W[6 * kMaxTips * kQpWStride];  // W(r, c, e) = W[r * m * ws + c * ws + e]
   double Gm[kMaxTips * kQpGStride];     // B^-1 U: G(c, e, p) = Gm[c * gs + e * 7 + p]
-  double Zm[kMaxTips * kQpGStride];     // G (I + U^T G)^-1, same layout
-  double C[49];
+  double C[49];                         // I + U^T G
+  double Cinv[49];
 };
 
 // mode 0: coarse (frames from the tip point queries, warm start from the
@@ -138,7 +138,8 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     s.C[q * 7 + p] = v;
   }
   __syncwarp();
-  // Each lane inverts C redundantly (Cholesky, 7x7) and forms its Z rows.
+  // C^-1 (7x7): every lane factors C (Cholesky) redundantly; lane q < 7
+  // solves for column q.
   {
     double L[7][7];
 #pragma unroll
@@ -156,13 +157,12 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
         L[i][j] = v / ljj;
       }
     }
-    // Z^T = C^-1 G^T: solve C z = g for each of this lane's rows of G.
-    for (int i = lane; i < n; i += 32) {
-      const int gi = (i / k) * gs + (i % k) * 7;
+    __syncwarp();
+    if (lane < 7) {
       double y[7];
 #pragma unroll
       for (int r = 0; r < 7; ++r) {
-        double v = s.Gm[gi + r];
+        double v = r == lane ? 1.0 : 0.0;
 #pragma unroll
         for (int q = 0; q < r; ++q) v -= L[r][q] * y[q];
         y[r] = v / L[r][r];
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
         y[r] = v / L[r][r];
       }
 #pragma unroll
-      for (int r = 0; r < 7; ++r) s.Zm[gi + r] = y[r];
+      for (int r = 0; r < 7; ++r) s.Cinv[r * 7 + lane] = y[r];
     }
   }
   __syncwarp();
@@ -186,11 +186,32 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
   const int base = j * m;
   const int axis = j >> 1;
   const double tsign = (j & 1) ? -1.0 : 1.0;
-  const double rho = P.rho, sigma = P.sigma, alpha = P.alpha;
+  const double rho = P.rho, sigma = P.sigma, alpha = P.alpha, mu = P.mu;
   const double inv_a = 1.0 / a_diag;
   const double inv_rho = 1.0 / rho;
-  const double* Gl = s.Gm + c * gs;
-  const double* Zl = s.Zm + c * gs;
+  // This lane's contact frame (contact.cpp:47-53): edge_e = n + mu (cos_e d +
+  // sin_e e), torque_e = p x edge_e. Every product with W or W^T is formed
+  // from it: W v = (f, p x f) with f = n S0 + mu (d S1 + e S2), S0 = sum v_e,
+  // S1 = sum cos_e v_e, S2 = sum sin_e v_e; (W^T u)_e = edge_e . (u_f + u_t x p).
+  const D3 fp = ld3(s.frame + 12 * c), fn = ld3(s.frame + 12 * c + 3);
+  const D3 fd = ld3(s.frame + 12 * c + 6), fe = ld3(s.frame + 12 * c + 9);
+  double ccos = 0.0, csin = 0.0;
+#pragma unroll
+  for (int e = 0; e < KMAX; ++e)
+    if (e < k) ccos += P.cos_t[e], csin += P.sin_t[e];
+  auto w_times = [&](const double (&v)[KMAX], D3& f, D3& t) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int e = 0; e < KMAX; ++e) {
+      if (e < k) {
+        s0 += v[e];
+        s1 += P.cos_t[e] * v[e];
+        s2 += P.sin_t[e] * v[e];
+      }
+    }
+    f = s0 * fn + mu * (s1 * fd + s2 * fe);
+    t = cross(fp, f);
+  };
 
   double x[KMAX], zid[KMAX], yid[KMAX], q[KMAX], xs[KMAX];
   double zc, yc, ztot, ytot;
@@ -229,40 +250,55 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
   int sweeps = 0;
   for (int iter = 1; iter <= P.max_iters; ++iter) {
     sweeps = iter;
-    // rhs = A'(rho z - y) + sigma x - q
+    // rhs = A'(rho z - y) + sigma x - q ; r' = B^-1 rhs
     const double vc = rho * zc - yc, vt = rho * ztot - ytot;
-    double rhs[KMAX];
+    double rp[KMAX];
     double bsum = 0.0;
 #pragma unroll
     for (int e = 0; e < KMAX; ++e) {
       if (e < k) {
         const double vi = rho * zid[e] - yid[e];
-        rhs[e] = ((vc + vt) + vi) + (sigma * x[e] - q[e]);
-        bsum += rhs[e];
+        rp[e] = ((vc + vt) + vi) + (sigma * x[e] - q[e]);
+        bsum += rp[e];
       } else {
-        rhs[e] = 0.0;
+        rp[e] = 0.0;
       }
     }
-    // t = G^T rhs over the column
-    double tv[7];
 #pragma unroll
-    for (int p = 0; p < 7; ++p) {
-      double acc = 0.0;
+    for (int e = 0; e < KMAX; ++e) rp[e] = e < k ? (rp[e] - betap * bsum) * inv_a : 0.0;
+    // t = U^T r' over the column: (sqrt2 W r', sqrt(rho) sum r')
+    double tv[7];
+    {
+      D3 f, t;
+      w_times(rp, f, t);
+      double s0 = 0.0;
 #pragma unroll
       for (int e = 0; e < KMAX; ++e)
-        if (e < k) acc += Gl[e * 7 + p] * rhs[e];
-      tv[p] = qp_group_sum<MT>(acc, base, m);
+        if (e < k) s0 += rp[e];
+      const double tl[7] = {sqrt2 * f.x, sqrt2 * f.y, sqrt2 * f.z, sqrt2 * t.x, sqrt2 * t.y, sqrt2 * t.z,
+                            sqrt_rho * s0};
+#pragma unroll
+      for (int p = 0; p < 7; ++p) tv[p] = qp_group_sum<MT>(tl[p], base, m);
     }
-    // xt = B^-1 rhs - Z t ; zt = A xt
+    // s = C^-1 t (smem broadcast) ; G s = B^-1 U s ; xt = r' - G s
+    double sv[7];
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int p = 0; p < 7; ++p) acc += s.Cinv[r * 7 + p] * tv[p];
+      sv[r] = acc;
+    }
+    const D3 wv = mk(sv[0], sv[1], sv[2]) + cross(mk(sv[3], sv[4], sv[5]), fp);
+    const double nw = dot(fn, wv), dw = dot(fd, wv), ew = dot(fe, wv);
+    const double us_sum = sqrt2 * (k * nw + mu * (ccos * dw + csin * ew)) + (k * sqrt_rho) * sv[6];
     double xt[KMAX];
     double ztc = 0.0;
 #pragma unroll
     for (int e = 0; e < KMAX; ++e) {
       if (e < k) {
-        double zs = 0.0;
-#pragma unroll
-        for (int p = 0; p < 7; ++p) zs += Zl[e * 7 + p] * tv[p];
-        xt[e] = (rhs[e] - betap * bsum) * inv_a - zs;
+        const double us = sqrt2 * (nw + mu * (P.cos_t[e] * dw + P.sin_t[e] * ew)) + sqrt_rho * sv[6];
+        xt[e] = rp[e] - (us - betap * us_sum) * inv_a;
         ztc += xt[e];
       } else {
         xt[e] = 0.0;
@@ -298,34 +334,30 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
       for (int e = 0; e < KMAX; ++e)
         if (e < k) axc += x[e];
       const double axt = qp_group_sum<MT>(axc, base, m);
-      double rp = fmax(fabs(axc - zc), fabs(axt - ztot));
+      double rp_ = fmax(fabs(axc - zc), fabs(axt - ztot));
 #pragma unroll
       for (int e = 0; e < KMAX; ++e)
-        if (e < k) rp = fmax(rp, fabs(x[e] - zid[e]));
-      rp = qp_group_max<MT>(rp, base, m);
-      double wx6[6];
-#pragma unroll
-      for (int r = 0; r < 6; ++r) {
-        double acc = 0.0;
-#pragma unroll
-        for (int e = 0; e < KMAX; ++e)
-          if (e < k) acc += s.W[r * wn + c * ws + e] * x[e];
-        wx6[r] = qp_group_sum<MT>(acc, base, m);
-      }
+        if (e < k) rp_ = fmax(rp_, fabs(x[e] - zid[e]));
+      rp_ = qp_group_max<MT>(rp_, base, m);
+      // W x over the column, then (W^T W x)_e = edge_e . (wf + wt x p)
+      D3 wf, wt;
+      w_times(x, wf, wt);
+      wf = mk(qp_group_sum<MT>(wf.x, base, m), qp_group_sum<MT>(wf.y, base, m), qp_group_sum<MT>(wf.z, base, m));
+      wt = mk(qp_group_sum<MT>(wt.x, base, m), qp_group_sum<MT>(wt.y, base, m), qp_group_sum<MT>(wt.z, base, m));
+      const D3 u = wf + cross(wt, fp);
+      const double nu = dot(fn, u), du = dot(fd, u), eu = dot(fe, u);
       double rd = 0.0;
 #pragma unroll
       for (int e = 0; e < KMAX; ++e) {
         if (e < k) {
-          double px = 0.0;
-#pragma unroll
-          for (int r = 0; r < 6; ++r) px += s.W[r * wn + c * ws + e] * wx6[r];
+          const double px = nu + mu * (P.cos_t[e] * du + P.sin_t[e] * eu);
           const double dual = (2.0 * px + ((yc + ytot) + yid[e])) + q[e];
           rd = fmax(rd, fabs(dual));
         }
       }
       rd = qp_group_max<MT>(rd, base, m);
       if (!frozen) {
-        const bool ok = rp <= P.eps_primal && rd <= P.eps_dual;
+        const bool ok = rp_ <= P.eps_primal && rd <= P.eps_dual;
         if (ok || iter == P.max_iters) {
           frozen = true;
 #pragma unroll
