@@ -62,7 +62,7 @@ struct QpSmem {
 // mode 1: final record (frames from st.frames, cold start).
 // mode 2: standalone batch (frames from st.frames, warm if qp_ready).
 #ifndef GDEV_QP_MIN_BLOCKS
-#define GDEV_QP_MIN_BLOCKS 3  // <= 170 registers, no spills (measured best)
+#define GDEV_QP_MIN_BLOCKS 4  // 128 registers, small spills (measured best)
 #endif
 template <int KT, int MT>
 __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
@@ -199,8 +199,9 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
 #pragma unroll
   for (int e = 0; e < KMAX; ++e)
     if (e < k) ccos += P.cos_t[e], csin += P.sin_t[e];
-  auto w_times = [&](const double (&v)[KMAX], D3& f, D3& t) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  auto w_times = [&](const double (&v)[KMAX], D3& f, D3& t, double& s0) {
+    double s1 = 0.0, s2 = 0.0;
+    s0 = 0.0;
 #pragma unroll
     for (int e = 0; e < KMAX; ++e) {
       if (e < k) {
@@ -270,11 +271,8 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     double tv[7];
     {
       D3 f, t;
-      w_times(rp, f, t);
-      double s0 = 0.0;
-#pragma unroll
-      for (int e = 0; e < KMAX; ++e)
-        if (e < k) s0 += rp[e];
+      double s0;
+      w_times(rp, f, t, s0);
       const double tl[7] = {sqrt2 * f.x, sqrt2 * f.y, sqrt2 * f.z, sqrt2 * t.x, sqrt2 * t.y, sqrt2 * t.z,
                             sqrt_rho * s0};
 #pragma unroll
@@ -291,14 +289,17 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     }
     const D3 wv = mk(sv[0], sv[1], sv[2]) + cross(mk(sv[3], sv[4], sv[5]), fp);
     const double nw = dot(fn, wv), dw = dot(fd, wv), ew = dot(fe, wv);
-    const double us_sum = sqrt2 * (k * nw + mu * (ccos * dw + csin * ew)) + (k * sqrt_rho) * sv[6];
+    // (U s)_e = ua + ub cos_e + uc sin_e, so (G s)_e = (U s - betap sum U s)_e / a
+    // is ga + gb cos_e + gc sin_e.
+    const double ua = sqrt2 * nw + sqrt_rho * sv[6], ub = sqrt2 * mu * dw, uc = sqrt2 * mu * ew;
+    const double us_sum = k * ua + ccos * ub + csin * uc;
+    const double ga = (ua - betap * us_sum) * inv_a, gb = ub * inv_a, gc = uc * inv_a;
     double xt[KMAX];
     double ztc = 0.0;
 #pragma unroll
     for (int e = 0; e < KMAX; ++e) {
       if (e < k) {
-        const double us = sqrt2 * (nw + mu * (P.cos_t[e] * dw + P.sin_t[e] * ew)) + sqrt_rho * sv[6];
-        xt[e] = rp[e] - (us - betap * us_sum) * inv_a;
+        xt[e] = ((rp[e] - ga) - gb * P.cos_t[e]) - gc * P.sin_t[e];
         ztc += xt[e];
       } else {
         xt[e] = 0.0;
@@ -341,7 +342,8 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
       rp_ = qp_group_max<MT>(rp_, base, m);
       // W x over the column, then (W^T W x)_e = edge_e . (wf + wt x p)
       D3 wf, wt;
-      w_times(x, wf, wt);
+      double sx_;
+      w_times(x, wf, wt, sx_);
       wf = mk(qp_group_sum<MT>(wf.x, base, m), qp_group_sum<MT>(wf.y, base, m), qp_group_sum<MT>(wf.z, base, m));
       wt = mk(qp_group_sum<MT>(wt.x, base, m), qp_group_sum<MT>(wt.y, base, m), qp_group_sum<MT>(wt.z, base, m));
       const D3 u = wf + cross(wt, fp);
