@@ -211,6 +211,14 @@ struct PointHit {
 // point_to_mesh (geometry.cpp:527-542) with query_part (:355-395): inside
 // test breaking at the first plane with depth < -1e-12, else the brute-force
 // closest point with strict '<' over faces and parts.
+// Single-instruction fp32 square root (relative error ~1e-7, far inside the
+// culling slack); used only for culling bounds.
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ double4 ld_plane(const DevObject& O, int f) {
   const double2* q = reinterpret_cast<const double2*>(O.face_plane + f);
   const double2 a = __ldg(q), b = __ldg(q + 1);
@@ -248,7 +256,7 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
       for (int c = c0; c < c1; ++c) {
         const float4 S = __ldg(O.cluster_sphere32 + c);
         const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
-        const float dist = sqrtf(dx * dx + dy * dy + dz * dz);
+        const float dist = sqrt_approx(dx * dx + dy * dy + dz * dz);
         ubA = fminf(ubA, dist + S.w);
         if (dist - S.w < lb_seed) {
           lb_seed = dist - S.w;
@@ -261,7 +269,7 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
       for (int f = seed_f; f < e; ++f) {
         const float4 S = __ldg(O.face_sphere32 + f);
         const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
-        const float lb = sqrtf(dx * dx + dy * dy + dz * dz) - S.w;
+        const float lb = sqrt_approx(dx * dx + dy * dy + dz * dz) - S.w;
         if (lb < lbf) {
           lbf = lb;
           seed_f = f;
@@ -342,10 +350,11 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
       pt = mk(0, 0, 0);
       for (int c = c0; c < c1; ++c) {
         {
+          // |p - C| - R - slack > min(bound, best), squared (both sides >= 0)
           const float4 S = __ldg(O.cluster_sphere32 + c);
           const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
-          const float lb = sqrtf(dx * dx + dy * dy + dz * dz) - S.w - kCullSlack32;
-          if (lb > bound || lb > sd32) continue;
+          const float reach = fminf(bound, sd32) + S.w + kCullSlack32;
+          if (dx * dx + dy * dy + dz * dz > reach * reach) continue;
         }
         const int e = __ldg(O.cluster_fbeg + c + 1);
         for (int f = __ldg(O.cluster_fbeg + c); f < e; ++f) {
@@ -353,7 +362,8 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
           {
             const float4 S = __ldg(O.face_sphere32 + f);
             const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
-            if (sqrtf(dx * dx + dy * dy + dz * dz) - S.w - kCullSlack32 > cut) continue;
+            const float reach = cut + S.w + kCullSlack32;
+            if (dx * dx + dy * dy + dz * dz > reach * reach) continue;
           }
           // Thin-box bound: the triangle lies in a box (centre o, fp32 axes
           // u, v, n, half extents hu, hv, hn; built on the host from the
@@ -368,7 +378,8 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
             const float eu = fmaxf(fabsf(rx * B1.x + ry * B1.y + rz * B1.z) - B0.w, 0.0f);
             const float ev = fmaxf(fabsf(rx * B2.x + ry * B2.y + rz * B2.z) - B1.w, 0.0f);
             const float en = fmaxf(fabsf(rx * B3.x + ry * B3.y + rz * B3.z) - B2.w, 0.0f);
-            if (sqrtf(eu * eu + ev * ev + en * en) - kCullSlack32 > cut) continue;
+            const float reach = cut + kCullSlack32;
+            if (eu * eu + ev * ev + en * en > reach * reach) continue;
           }
           ++tris;
           const double* F = O.faces + (size_t)f * kFaceStride;
