@@ -113,7 +113,7 @@ struct grasp_ctx {
   DevState st{};
   DevBuf<double> x, pose, world, joints, qpts, qres, pairs, warm_x, warm_y, out_z, qp_force, qp_energy, qp_perdir,
       frames, anchors, energy, grad, stage_energy, x_p, x_s, witness;
-  DevBuf<int> qp_iters, qp_conv, qp_ready, failed, have_pregrasp, err, ovf_count, ovf_list;
+  DevBuf<int> qp_iters, qp_conv, qp_ready, failed, have_pregrasp, err, ovf_count, ovf_list, qface;
   DevBuf<EpaScratchBig> big_scratch;
   static constexpr int kBigSlots = 1024;
   // Pair kernel variant (GRASP_PAIRS=list|warp|thread, default list).
@@ -540,6 +540,9 @@ struct grasp_ctx {
     qp_iters.ensure(g * 6);
     qp_conv.ensure(g * 6);
     qp_ready.ensure(g);
+    qface.ensure(g * NQ);
+    ck(cudaMemsetAsync(qface.p, 0xff, sizeof(int) * g * NQ, stream), "memset");
+    st.qface = qface.p;
     failed.ensure(g);
     have_pregrasp.ensure(g);
     err.ensure(4);
@@ -1122,6 +1125,26 @@ __global__ void k_cos_debug(int n, const double* w, double* out) {
   }
 }
 }  // namespace
+
+// Debug surface: point_to_mesh with caller-chosen warm-start faces (tests the
+// warm-start culling for exactness; not part of the public ABI).
+extern "C" int grasp_debug_point_to_mesh_warm(grasp_ctx* ctx, int n, const double* points, const int* warm,
+                                              double* out) {
+  return guard([&] {
+    if (!ctx || !ctx->has_object) throw std::invalid_argument("no object uploaded");
+    ctx->set_device();
+    DevBuf<double> dp, dout;
+    DevBuf<int> dw;
+    dp.ensure(static_cast<size_t>(n) * 3);
+    dout.ensure(static_cast<size_t>(n) * 8);
+    dw.upload(std::vector<int>(warm, warm + n), ctx->stream);
+    ck(cudaMemcpyAsync(dp.p, points, sizeof(double) * n * 3, cudaMemcpyHostToDevice, ctx->stream), "pts");
+    k_points_raw<<<grasp_ctx::blocks(n, 128), 128, 0, ctx->stream>>>(ctx->O, n, dp.p, dout.p, dw.p);
+    ck(cudaGetLastError(), "launch");
+    ck(cudaMemcpyAsync(out, dout.p, sizeof(double) * n * 8, cudaMemcpyDeviceToHost, ctx->stream), "out");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
 
 extern "C" int grasp_debug_cos(int n, const double* w, double* out) {
   return guard([&] {

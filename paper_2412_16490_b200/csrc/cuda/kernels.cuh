@@ -206,6 +206,7 @@ struct PointHit {
   double d;
   D3 pb, n;
   int part;
+  int face;  // closest face when the winning part was outside, else -1
 };
 
 // point_to_mesh (geometry.cpp:527-542) with query_part (:355-395): inside
@@ -225,15 +226,26 @@ __device__ __forceinline__ double4 ld_plane(const DevObject& O, int f) {
   return make_double4(a.x, a.y, b.x, b.y);
 }
 
-__device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* plane_tests = nullptr,
-                                         unsigned* tri_tests = nullptr) {
+__device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int warm_face = -1,
+                                         unsigned* plane_tests = nullptr, unsigned* tri_tests = nullptr) {
   PointHit best;
   best.d = INFINITY;
   best.pb = mk(0, 0, 0);
   best.n = mk(0, 0, 1);
   best.part = -1;
+  best.face = -1;
   unsigned planes = 0, tris = 0;
   const float px = (float)p.x, py = (float)p.y, pz = (float)p.z;
+  // Warm start: the exact distance to any face (here the slot's closest face
+  // of the previous query) bounds the minimum over all outside parts from
+  // above; parts and faces whose lower bounds exceed it cannot be the
+  // argmin (inside parts have lower bound <= 0 and are never skipped).
+  double ub_warm = INFINITY;
+  if (warm_face >= 0 && warm_face < O.F) {
+    ++tris;
+    const double* F = O.faces + (size_t)warm_face * kFaceStride;
+    ub_warm = nrm(p - closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6)));
+  }
   for (int part = 0; part < O.P; ++part) {
     const int f0 = __ldg(O.part_fbeg + part), f1 = __ldg(O.part_fbeg + part + 1);
     // Part-level cull: every point of the part is at least |p - c| - r
@@ -242,7 +254,7 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
     {
       const double* S = O.part_sphere + 4 * part;
       const double lb = nrm(p - ldg3(S)) - __ldg(S + 3) - kCullSlack;
-      if (lb > best.d) continue;
+      if (lb > best.d || lb > ub_warm) continue;
     }
     // Face clusters (runs of consecutive faces with fp32 bounding spheres):
     // an upper bound on the part distance (min |p-C| + R) and a seed face,
@@ -324,6 +336,7 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
     }
     double sd;
     D3 pt, nn;
+    int sf = -1;
     if (inside && isfinite(min_depth)) {
       sd = -min_depth;
       nn = best_n;
@@ -343,11 +356,12 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
         ++tris;
         const double* F = O.faces + (size_t)seed_f * kFaceStride;
         const double d_seed = nrm(p - closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6)));
-        bound = fminf(ubA, __double2float_ru(d_seed)) + kCullSlack32;
+        bound = fminf(fminf(ubA, __double2float_ru(d_seed)), __double2float_ru(ub_warm)) + kCullSlack32;
       }
       sd = INFINITY;
       float sd32 = INFINITY;
       pt = mk(0, 0, 0);
+      sf = -1;
       for (int c = c0; c < c1; ++c) {
         {
           // |p - C| - R - slack > min(bound, best), squared (both sides >= 0)
@@ -389,6 +403,7 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
             sd = d;
             sd32 = __double2float_ru(d) + kCullSlack32;
             pt = cp;
+            sf = f;
           }
         }
       }
@@ -399,6 +414,7 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, unsigned* pla
       best.pb = pt;
       best.n = nn;
       best.part = part;
+      best.face = sf;
     }
   }
   if (plane_tests) *plane_tests = planes;
@@ -416,7 +432,9 @@ __global__ void k_point_query(DevObject O, DevState st, const int* __restrict__ 
   if (st.failed[g]) return;
   const D3 p = ld3(st.qpts + ((size_t)g * st.NQ + slot) * 3);
   unsigned planes, tris;
-  const PointHit h = point_to_mesh(O, p, &planes, &tris);
+  int* qf = st.qface + (size_t)g * st.NQ + slot;
+  const PointHit h = point_to_mesh(O, p, *qf, &planes, &tris);
+  *qf = h.face;
   if (st.ops) {
     atomicAdd(st.ops + kOpPlaneTests, (unsigned long long)planes);
     atomicAdd(st.ops + kOpTriangleTests, (unsigned long long)tris);
@@ -430,10 +448,11 @@ __global__ void k_point_query(DevObject O, DevState st, const int* __restrict__ 
 }
 
 // Standalone query surface (teacher-forced tests).
-__global__ void k_points_raw(DevObject O, int n, const double* __restrict__ pts, double* out) {
+__global__ void k_points_raw(DevObject O, int n, const double* __restrict__ pts, double* out,
+                             const int* __restrict__ warm = nullptr) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  const PointHit h = point_to_mesh(O, ld3(pts + 3 * t));
+  const PointHit h = point_to_mesh(O, ld3(pts + 3 * t), warm ? warm[t] : -1);
   double* o = out + 8 * t;
   o[0] = h.d;
   st3(o + 1, h.pb);

@@ -109,6 +109,7 @@ struct DevState {
   double* joints;   // [G*dof*6]: chain-frame origin(3), axis(3)
   double* qpts;     // [G*NQ*3]
   double* qres;     // [G*NQ*8]: d, pb(3), n(3), part
+  int* qface;       // [G*NQ] closest face of the slot's last query (warm-start seed), -1 if none
   double* pairs;    // [G*NP*12]: d, pa(3), pb(3), n(3), flags, pad
   double* warm_x;   // [G*n*6] column-major n x 6
   double* warm_y;   // [G*M*6]

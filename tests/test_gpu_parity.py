@@ -122,6 +122,47 @@ def test_point_queries_multipart(G, O, trident, engine):
     np.testing.assert_allclose(got[:, :7], ref[:, :7], atol=1e-9, rtol=0)
 
 
+def test_point_queries_warm_start_exact(G, O, engine, trident):
+    """Warm-start seeds (the slot's previous closest face, used as an exact upper
+    bound) must not change any result: random and nearest-face seeds vs no seed,
+    bitwise, and vs the oracle, on the multi-part drill mesh."""
+    from pathlib import Path
+    from paper_2412_16490_b200 import _native as N
+    from paper_2412_16490_b200.api import dptr, iptr
+    root = Path(__file__).resolve().parents[1]
+    obj = G.load_object(root / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+    use(engine, trident, obj)
+    rng = np.random.default_rng(11)
+    lo, hi = obj.desc.verts[0:1], None
+    pts = rng.normal(size=(6000, 3)) * 0.06 + np.array([0.02, 0.0, 0.0])
+    nf = int(obj.desc.n_faces)
+    cold = gpu_points(engine, pts)
+    ref = O.point_to_mesh(obj, pts)
+    assert (cold[:, 7] == ref[:, 7]).all()
+    np.testing.assert_allclose(cold[:, :7], ref[:, :7], atol=1e-9, rtol=0)
+    lib = N.lib()
+    fn = getattr(lib, "grasp_debug_point_to_mesh_warm")
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_double)]
+    for warm in (rng.integers(0, nf, size=len(pts)).astype(np.int32),
+                 np.full(len(pts), -1, np.int32), np.full(len(pts), nf + 5, np.int32)):
+        out = np.zeros((len(pts), 8))
+        N.check(fn(engine._ctx, len(pts), dptr(pts), iptr(warm), dptr(out)))
+        assert np.array_equal(out, cold), "warm start changed a point query"
+    # seeds from the neighbours' answers (the solver's real use): shifted points
+    pts2 = pts + rng.normal(size=pts.shape) * 1e-3
+    cold2 = gpu_points(engine, pts2)
+    out = np.zeros((len(pts), 8))
+    seeds = np.full(len(pts), -1, np.int32)
+    N.check(fn(engine._ctx, len(pts), dptr(pts), iptr(seeds), dptr(out)))
+    # no face output on this surface; use random faces of the winning part instead
+    fb = np.asarray(obj.part_face_begin)
+    part = cold[:, 7].astype(int)
+    seeds = (fb[part] + rng.integers(0, 1 << 30, size=len(pts)) % (fb[part + 1] - fb[part])).astype(np.int32)
+    N.check(fn(engine._ctx, len(pts2), dptr(pts2), iptr(seeds), dptr(out)))
+    assert np.array_equal(out, cold2)
+
+
 # ---------------------------------------------------------------- GJK / EPA
 def random_link_poses(rng, n, span):
     from scipy.spatial.transform import Rotation
