@@ -278,14 +278,33 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
 #pragma unroll
       for (int p = 0; p < 7; ++p) tv[p] = qp_group_sum<MT>(tl[p], base, m);
     }
-    // s = C^-1 t (smem broadcast) ; G s = B^-1 U s ; xt = r' - G s
+    // s = C^-1 t ; G s = B^-1 U s ; xt = r' - G s. With the contact count
+    // known at compile time the 7 rows of C^-1 t are split over the m lanes
+    // of the column (lane c takes rows c, c + m, ...) and shared by shuffles.
     double sv[7];
+    if constexpr (MT > 0) {
+      constexpr int RPL = (7 + MT - 1) / MT;  // rows per lane
+      double mine[RPL];
 #pragma unroll
-    for (int r = 0; r < 7; ++r) {
-      double acc = 0.0;
+      for (int i = 0; i < RPL; ++i) {
+        const int r = c + i * MT;
+        double acc = 0.0;
+        if (r < 7) {
 #pragma unroll
-      for (int p = 0; p < 7; ++p) acc += s.Cinv[r * 7 + p] * tv[p];
-      sv[r] = acc;
+          for (int p = 0; p < 7; ++p) acc += s.Cinv[r * 7 + p] * tv[p];
+        }
+        mine[i] = acc;
+      }
+#pragma unroll
+      for (int r = 0; r < 7; ++r) sv[r] = __shfl_sync(kFull, mine[r / MT], base + r % MT);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 7; ++r) {
+        double acc = 0.0;
+#pragma unroll
+        for (int p = 0; p < 7; ++p) acc += s.Cinv[r * 7 + p] * tv[p];
+        sv[r] = acc;
+      }
     }
     const D3 wv = mk(sv[0], sv[1], sv[2]) + cross(mk(sv[3], sv[4], sv[5]), fp);
     const double nw = dot(fn, wv), dw = dot(fd, wv), ew = dot(fe, wv);
