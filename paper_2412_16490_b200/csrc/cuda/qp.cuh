@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     t = cross(fp, f);
   };
 
-  double x[KMAX], zid[KMAX], yid[KMAX], q[KMAX], xs[KMAX];
+  double x[KMAX], zid[KMAX], yid[KMAX], q[KMAX];
   double zc, yc, ztot, ytot;
   const bool warm = (mode == 0 || mode == 2) && st.qp_ready[g];
   const double* wx = st.warm_x + (size_t)g * n * 6;
@@ -230,7 +230,6 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
       x[e] = yid[e] = q[e] = 0.0;
     }
     zid[e] = x[e];
-    xs[e] = x[e];
   }
   yc = warm ? wy[j * M + c] : 0.0;
   ytot = warm ? wy[j * M + m] : 0.0;
@@ -385,7 +384,6 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
           for (int e = 0; e < KMAX; ++e) {
             if (e < k) {
               const int i = c * k + e;
-              xs[e] = x[e];
               ox[j * n + i] = x[e];
               oy[j * M + m + 1 + i] = yid[e];
               oz[j * M + m + 1 + i] = zid[e];
@@ -412,7 +410,11 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     }
   }
 
-  // Energy report from the snapshot (energy.cpp:78-90).
+  // Energy report from the snapshot (energy.cpp:78-90), read back from the
+  // warm-start copy this lane wrote when its column froze.
+  double xs[KMAX];
+#pragma unroll
+  for (int e = 0; e < KMAX; ++e) xs[e] = (active && e < k) ? ox[j * n + c * k + e] : 0.0;
   double res[6];
 #pragma unroll
   for (int r = 0; r < 6; ++r) {
