@@ -127,6 +127,11 @@ struct grasp_ctx {
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
   DevBuf<unsigned char> pair_need;
   long long list_grid = 148 * 4;  // persistent k_pairs_list blocks
+  long long epa_grid = 148 * 4;   // grid-stride k_pairs_epa_warp blocks
+  bool epa_thread = [] {  // the warp-per-job EPA measured slower (lane-0 polytope updates)
+    const char* v = std::getenv("GRASP_EPA");
+    return !(v && std::string(v) == "warp");
+  }();
   DevBuf<double> epa_jobs;
 
   // Instrumentation: launch counts always; per-class CUDA-event time and
@@ -675,7 +680,11 @@ struct grasp_ctx {
           k_pairs_list_il<<<std::min<long long>(blocks(n, 128), list_grid), 128, 0, stream>>>(H, O, st);
         else
           k_pairs_list<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
-        k_pairs_epa<<<blocks(std::min<long long>(n, st.epa_cap), 128), 128, 0, stream>>>(H, O, st);
+        if (epa_thread)
+          k_pairs_epa<<<blocks(std::min<long long>(n, st.epa_cap), 128), 128, 0, stream>>>(H, O, st);
+        else
+          k_pairs_epa_warp<<<std::min<long long>(blocks(std::min<long long>(n, st.epa_cap), 4), epa_grid), 128, 0,
+                             stream>>>(H, O, st);
       }
     });
     launch(7, [&] { k_pairs_big<<<kBigSlots / 128, 128, 0, stream>>>(H, O, st); });
@@ -872,6 +881,8 @@ int grasp_ctx_create(int device, grasp_ctx** out) {
       ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
       ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gdev::k_pairs_list_il, 128, 0), "occupancy");
       ctx->list_grid = static_cast<long long>(sms) * std::max(per_sm, 1);
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gdev::k_pairs_epa_warp, 128, 0), "occupancy");
+      ctx->epa_grid = static_cast<long long>(sms) * std::max(per_sm, 1);
     } catch (...) {
       delete ctx;
       throw;

@@ -913,6 +913,54 @@ __global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHa
 }
 
 // Pass 3: EPA for the overlapping pairs (geometry.cpp:227-324).
+// Pass 3 variant (GRASP_EPA=warp; measured slower than the per-thread
+// kernel): EPA for the overlapping pairs, one warp per job
+// (warp_epa: support scans split over the lanes, polytope in shared memory,
+// its order-dependent updates on lane 0 - same faces, order and tie rules
+// as the per-thread epa(); geometry.cpp:168-205, 227-324). Grid-stride over
+// the job list so the grid can be sized without reading the job count.
+__global__ void __launch_bounds__(128) k_pairs_epa_warp(DevHand H, DevObject O, DevState st) {
+  __shared__ WarpEpa epa_smem[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int njobs = min(*(volatile int*)st.epa_count, st.epa_cap);
+  for (int i = blockIdx.x * 4 + warp; i < njobs; i += gridDim.x * 4) {
+    const double* jb = st.epa_jobs + (size_t)i * kEpaJobStride;
+    const int slot = (int)jb[0], ns = (int)jb[1];
+    SP simp[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      simp[k].w = ld3(jb + 2 + 9 * k);
+      simp[k].a = ld3(jb + 5 + 9 * k);
+      simp[k].b = ld3(jb + 8 + 9 * k);
+    }
+    Hull A, B;
+    double scale;
+    slot_hulls(H, O, st, slot, A, B, scale);
+    PairResult r;
+    r.flags = 0;
+    r.n_support = 0;
+    r.gjk_iters = 0;
+    r.epa_iters = 0;
+    r.gjk_skipped = 0;
+    warp_epa(simp, ns, A, B, scale, epa_smem[warp], lane, r);
+    if (lane == 0) {
+      if (st.ops) {
+        atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * (A.nv + B.nv));
+        atomicAdd(st.ops + kOpEpaIters, (unsigned long long)r.epa_iters);
+        if (r.flags & kPairOverflow) atomicAdd(st.ops + kOpEpaOverflow, 1ull);
+      }
+      if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
+      if (r.flags & kPairOverflow)
+        queue_overflow(st, slot);
+      else
+        store_pair(st.pairs + (size_t)slot * 12, r);
+    }
+    __syncwarp();
+  }
+}
+
+// Pass 3 (default): EPA for the overlapping pairs, one thread per job,
+// polytope in local memory.
 __global__ void __launch_bounds__(128) k_pairs_epa(DevHand H, DevObject O, DevState st) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= min(*st.epa_count, st.epa_cap)) return;
