@@ -13,6 +13,8 @@
 #define GDEV_FN __host__ __device__ __forceinline__
 #define GDEV_INL __host__ __device__ inline
 
+#include "crmath.cuh"
+
 namespace gdev {
 
 struct D3 {
@@ -108,7 +110,7 @@ GDEV_FN void set_col(M33& a, int c, D3 v) { a.m[c] = v.x; a.m[3 + c] = v.y; a.m[
 GDEV_FN M33 angle_axis(double angle, D3 axis) {
   double s, c;
 #if defined(__CUDA_ARCH__)
-  sincos(angle, &s, &c);
+  cr_sincos(angle, &s, &c);  // correctly rounded: matches glibc except near midpoints (crmath.cuh)
 #else
   s = ::sin(angle);
   c = ::cos(angle);

@@ -64,6 +64,24 @@ struct DevBuf {
 
 }  // namespace
 
+// Boxes for the pair cull's separating-axis test: the OBB axes and centre of
+// the descriptor, half extents re-measured from the hull vertices along those
+// axes and padded, so the box provably contains the hull.
+std::vector<double> containing_boxes(const double* obb, const double* verts, const int* vbeg, int n) {
+  std::vector<double> out(obb, obb + 15 * static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    double* b = out.data() + 15 * static_cast<size_t>(i);
+    double h[3] = {0, 0, 0};
+    for (int v = vbeg[i]; v < vbeg[i + 1]; ++v) {
+      const double r[3] = {verts[3 * v] - b[0], verts[3 * v + 1] - b[1], verts[3 * v + 2] - b[2]};
+      for (int k = 0; k < 3; ++k)
+        h[k] = std::max(h[k], std::fabs(r[0] * b[6 + 3 * k] + r[1] * b[7 + 3 * k] + r[2] * b[8 + 3 * k]));
+    }
+    for (int k = 0; k < 3; ++k) b[3 + k] = h[k] * (1.0 + 1e-12) + 1e-12;
+  }
+  return out;
+}
+
 struct grasp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -75,11 +93,11 @@ struct grasp_ctx {
       h_tip_slots, h_tip_links_sorted, h_link_tip;
   DevBuf<unsigned> h_subtree;
   DevBuf<double> h_jorigin, h_jaxis, h_jlo, h_jhi, h_proxy, h_envelope, h_lverts, h_lcentroid, h_lhalf,
-      h_link_bsphere;
+      h_link_bsphere, h_link_box;
   // object
   DevObject O{};
   DevBuf<int> o_fbeg, o_vbeg;
-  DevBuf<double> o_faces, o_verts, o_centroid, o_half, o_obb, o_part_sphere, o_face_sphere;
+  DevBuf<double> o_faces, o_verts, o_centroid, o_half, o_obb, o_part_sphere, o_face_sphere, o_part_box;
   DevBuf<float4> o_face_sphere32, o_cluster_sphere32, o_face_box32;
   DevBuf<double4> o_face_plane;
   DevBuf<int> o_part_cbeg, o_cluster_fbeg;
@@ -283,9 +301,12 @@ struct grasp_ctx {
     h_tip_links_sorted.upload(tip_link, s);
     h_link_tip.upload(link_tip, s);
     h_link_bsphere.upload(bsphere, s);
+    h_link_box.upload(containing_boxes(d->link_obb, d->verts, d->link_vert_begin, L), s);
     ck(cudaStreamSynchronize(s), "hand upload");
     H.link_tip = h_link_tip.p;
     H.link_bsphere = h_link_bsphere.p;
+    H.link_box = (std::getenv("GRASP_SAT") && std::string(std::getenv("GRASP_SAT")) == "0") ? nullptr : h_link_box.p;
+    H.cull = std::getenv("GRASP_CULL") && std::string(std::getenv("GRASP_CULL")) == "1";
     H.L = L;
     H.dof = dof;
     H.m = m;
@@ -383,6 +404,7 @@ struct grasp_ctx {
     o_half.upload(half, s);
     o_obb.upload(std::vector<double>(d->part_obb, d->part_obb + 15 * P), s);
     o_part_sphere.upload(part_sphere, s);
+    o_part_box.upload(containing_boxes(d->part_obb, d->verts, d->part_vert_begin, P), s);
     o_face_sphere.upload(face_sphere, s);
     std::vector<float4> face32(d->n_faces);
     for (int f = 0; f < d->n_faces; ++f) {
@@ -493,6 +515,7 @@ struct grasp_ctx {
     o_cluster_sphere32.upload(cluster32, s);
     ck(cudaStreamSynchronize(s), "object upload");
     O.part_sphere = o_part_sphere.p;
+    O.part_box = o_part_box.p;
     O.face_sphere = o_face_sphere.p;
     O.face_sphere32 = o_face_sphere32.p;
     O.face_box32 = o_face_box32.p;

@@ -717,6 +717,12 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
     iter += jump;
     out.gjk_skipped += jump;
     sx = closest_on_simplex(simp, ns);
+#ifdef GJK_TRACE
+    printf("iter %d ns %d -> nkeep %d contains %d dist2 %.17g keep %d %d %d %d wts %.3g %.3g %.3g %.3g\n", iter, ns,
+           sx.nkeep, (int)sx.contains, sx.dist2, sx.keep[0], sx.keep[1], sx.keep[2], sx.keep[3], sx.wts[0], sx.wts[1],
+           sx.wts[2], sx.wts[3]);
+    for (int i = 0; i < ns; ++i) printf("   w%d %.17g %.17g %.17g\n", i, simp[i].w.x, simp[i].w.y, simp[i].w.z);
+#endif
     if (iter == kGjkMaxIters) {
       D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
 #pragma unroll

@@ -523,23 +523,81 @@ __device__ __forceinline__ double obb_sphere(const double* obb, D3 center, doubl
   return dist - radius;
 }
 
-// True when the exact signed distance of (link, part) is needed: the pair
-// is in a fingertip's witness keep-set (the same OBB test select_witness
-// applies, pipeline.cpp:332-334), or it may penetrate. Everything else has
-// d > 0 by the link-sphere vs part-OBB lower bound, and the reference only
-// reads d < 0 from it (hinge, pipeline.cpp:182), so it is stored as +inf.
+// True when the signed distance of (link, part) must be computed. By default
+// every pair is: the reference runs GJK on every pair (pipeline.cpp:176-188)
+// and its GJK reports a spurious overlap for some provably separated pairs
+// (a coplanar 4-point simplex whose rank-deficient KKT solve wins the
+// subset enumeration by an ulp, so contains = true; about 1 in 6e4 late-stage
+// pairs, gaps up to mm measured), which then enters the penetration hinge.
+// Reproducing those needs the GJK. With the opt-in cull (GRASP_CULL=1) a
+// pair is skipped (+inf) unless it is in a fingertip's witness keep-set (the
+// OBB test select_witness applies, pipeline.cpp:332-334) or it may
+// penetrate by the link-sphere vs part-OBB and link-box vs part-box (SAT)
+// lower bounds: exact for the true geometry, not for those spurious overlaps.
+// Separating-axis test between the link box (posed by Rw, tw) and the part
+// box (object frame), 15 axes (Gottschalk's OBB test). true only if the
+// projections on some axis are disjoint with a gap > margin, which proves
+// the hulls inside are separated (d > 0). |R| is padded by 1e-12, and the
+// unnormalised cross axes only make the margin test stricter.
+__device__ __forceinline__ bool boxes_separated(const double* la, const M33& Rw, D3 tw, const double* pb,
+                                                double margin) {
+  D3 A[3], B[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    A[i] = mul(Rw, ld3(la + 6 + 3 * i));
+    B[i] = ld3(pb + 6 + 3 * i);
+  }
+  const double ah[3] = {la[3], la[4], la[5]}, bh[3] = {pb[3], pb[4], pb[5]};
+  const D3 T = ld3(pb) - (mul(Rw, ld3(la)) + tw);
+  double R[3][3], AR[3][3], t[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    t[i] = dot(T, A[i]);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      R[i][j] = dot(A[i], B[j]);
+      AR[i][j] = fabs(R[i][j]) + 1e-12;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (fabs(t[i]) > ah[i] + bh[0] * AR[i][0] + bh[1] * AR[i][1] + bh[2] * AR[i][2] + margin) return true;
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+    if (fabs(t[0] * R[0][j] + t[1] * R[1][j] + t[2] * R[2][j]) >
+        ah[0] * AR[0][j] + ah[1] * AR[1][j] + ah[2] * AR[2][j] + bh[j] + margin)
+      return true;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+      const double ra = ah[i1] * AR[i2][j] + ah[i2] * AR[i1][j];
+      const double rb = bh[j1] * AR[i][j2] + bh[j2] * AR[i][j1];
+      if (fabs(t[i2] * R[i1][j] - t[i1] * R[i2][j]) > ra + rb + margin) return true;
+    }
+  }
+  return false;
+}
+
 __device__ __forceinline__ bool pair_needed(const DevHand& H, const DevObject& O, const DevState& st, int g,
                                             int link, int part, const M33& Rw, D3 tw) {
+  if (!H.cull) return true;
   const int f = H.link_tip[link];
   if (f >= 0) {
     const int tp = H.tip_proxy[f];
     const D3 center = mul(Rw, ld3(H.proxy + 4 * tp)) + tw;
     const double reference = st.qres[((size_t)g * st.NQ + tp) * 8] - H.proxy[4 * tp + 3];
-    if (obb_sphere(O.part_obb + 15 * part, center, H.tip_envelope[f]) < reference + 1e-9) return true;
+    // Superset of select_witness's keep test (reference + 1e-9 there): the
+    // tip centre here comes from st.world, the step kernel's from its own FK
+    // copy, so a wider margin keeps every pair it may read exact.
+    if (obb_sphere(O.part_obb + 15 * part, center, H.tip_envelope[f]) < reference + 1e-6) return true;
   }
   const double* bs = H.link_bsphere + 4 * link;
   const D3 c = mul(Rw, ld3(bs)) + tw;
-  return !(obb_sphere(O.part_obb + 15 * part, c, bs[3]) > kCullSlack);
+  if (obb_sphere(O.part_obb + 15 * part, c, bs[3]) > kCullSlack) return false;
+  return !(H.link_box && boxes_separated(H.link_box + 15 * link, Rw, tw, O.part_box + 15 * part, kCullSlack));
 }
 
 // One thread per (grasp, link, part); consecutive threads share (link, part)

@@ -26,6 +26,7 @@ constexpr double kCullSlack = 1e-9;
 
 struct DevHand {
   int L, dof, m, S, nsp, D;
+  int cull;                         // opt-in (GRASP_CULL=1) separation cull of (link, part) pairs, see pair_needed
   const int* link_parent_joint;     // [L]
   const int* link_depth;            // [L] path length root..l
   const int* link_path;             // [L*kMaxDepth] links from root to l
@@ -48,6 +49,7 @@ struct DevHand {
   const double* link_halfnorm;      // [L] |obb.half_extents|
   const int* link_tip;              // [L] fingertip index of the link, -1 if none
   const double* link_bsphere;       // [L*4] bounding sphere of the link hull (link frame): center, radius
+  const double* link_box;           // [L*15] box containing the link hull (link frame): center, half, axes (col-major)
 };
 
 struct DevObject {
@@ -60,6 +62,7 @@ struct DevObject {
   const double* part_halfnorm;  // [P]
   const double* part_obb;       // [P*15] center, half, rotation (column-major)
   const double* part_sphere;    // [P*4] bounding sphere of the part: center, radius
+  const double* part_box;       // [P*15] box containing the part hull: center, half, axes (col-major)
   const double* face_sphere;    // [F*4] bounding sphere of each triangle: center, radius
   const float4* face_sphere32;  // [F] same in fp32, radius rounded up (culling bounds only)
   const double4* face_plane;    // [F] (n, n.a) in fp64; degenerate faces (0, 0, 0, +inf)

@@ -318,6 +318,32 @@ def test_mesh_energy_and_gradient_match_oracle(G, O, trident, engine):
         assert row_err[sel].max() <= 1e-2
 
 
+def test_mesh_energy_late_stage_matches_oracle(G, O, engine):
+    """Teacher-forced mesh-stage energies on late-stage Shadow/drill states
+    (tests/golden/make_late_states.py + 3 mm shifts). The batch includes a pair the
+    reference's GJK reports as overlapping although the hulls are 0.4 mm apart
+    (coplanar 4-point simplex); the default engine computes every pair
+    like the reference, so the spurious hinge term is reproduced."""
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    hand = G.HandModel.from_file(root / "paper_2412_16490_b200/assets/hands/shadow_like.json")
+    obj = G.load_object(root / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+    use(engine, hand, obj)
+    x = np.load(root / "tests/golden/late_states_shadow_drill.npz")["x"]
+    rng = np.random.default_rng(0)
+    xs = np.concatenate([x] + [x + np.concatenate([np.zeros((len(x), 9)), rng.normal(size=(len(x), 3)) * 0.003,
+                                                   np.zeros((len(x), x.shape[1] - 12))], 1) for _ in range(30)])
+    xs = xs[256:320]  # includes state 278 (link 6 / part 3 spurious overlap)
+    anchors = np.random.default_rng(1).normal(size=(len(xs), hand.n_tips, 3)) * 0.05
+    cfg = G.RunConfig()
+    ties = witness_ties(gpu_fcq(engine, hand, xs), O.fine_contact_query(hand, obj, xs)).any(axis=1)
+    e_ref, _ = O.total_energy(hand, obj, cfg, 1, xs, anchors=anchors)
+    e_got, _ = gpu_energy(engine, cfg, 1, xs, anchors=anchors)
+    ok = np.abs(e_got - e_ref) <= 1e-7 * np.abs(e_ref)
+    assert ok[278 - 256], "spurious-overlap state differs from the reference"
+    assert (ok | ties).all(), np.where(~(ok | ties))[0]
+
+
 def test_fine_contact_query_matches_oracle(G, O, trident, engine):
     obj = G.make_primitive("box", 0.1)
     use(engine, trident, obj)
