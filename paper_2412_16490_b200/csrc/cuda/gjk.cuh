@@ -136,8 +136,15 @@ GDEV_FN int cycle_step(GjkCycle& c, const unsigned (&key)[4], int ns, int iter) 
 // rank = #{|u_ii| > max_pivot * S * eps}; unit-lower then upper substitution
 // on the rank block; free unknowns 0). Every index is compile-time or a
 // predicated select, so the matrix stays in registers.
+//
+// Zero padding is exact: a system of size s_real < S embedded in the top-left
+// corner with zeros elsewhere gets the same pivots (padded entries are 0 and
+// never beat a nonzero one; the column-major scan keeps the real entries'
+// order), the same eliminations (padded entries stay +0), stops at the same
+// step, and the rank threshold uses s_real. So one body of size S serves all
+// smaller systems (instruction-cache footprint).
 template <int S>
-GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (&sol)[S]) {
+GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (&sol)[S], int s_real = S) {
   int rowt[S], colt[S];
   int nonzero = S;
   double maxpivot = 0.0;
@@ -202,7 +209,7 @@ GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (
       }
     }
   }
-  const double thresh = maxpivot * (S * 2.220446049250313e-16);
+  const double thresh = maxpivot * (s_real * 2.220446049250313e-16);
   int rank = 0;
 #pragma unroll
   for (int i = 0; i < S; ++i) rank += (i < nonzero && fabs(m[i][i]) > thresh) ? 1 : 0;
@@ -365,7 +372,9 @@ GDEV_FN int cheap_subset(const SP* simp, const int (&idx)[K], double& d2, double
 // (original simplex indices id[0..K)) and apply the acceptance and tie rules
 // against the running best. Gram entries are dot(P_i, P_j), bit-identical
 // to the reference's gram(idx_i, idx_j) (products commute exactly, sums in
-// the same order, no contraction in this TU).
+// the same order, no contraction in this TU). (A single zero-padded size-5
+// body for every K cuts the kernel's code by a fifth but costs more than
+// the instruction-cache stalls it removes; measured.)
 template <int K>
 GDEV_FN void simplex_subset(const D3 (&P)[4], const int (&id)[4], Simplex& best) {
   double m[K + 1][K + 1];
@@ -384,7 +393,18 @@ GDEV_FN void simplex_subset(const D3 (&P)[4], const int (&id)[4], Simplex& best)
   m[K][K] = 0.0;
   rhs[K] = 1.0;
   double sol[K + 1];
-  fullpiv_solve_t<K + 1>(m, rhs, sol);
+  if constexpr (K == 1) {
+    // [[g, 1], [1, 0]] with |g| < 1: FullPivLU pivots on the (1, 0) one,
+    // and its solve gives exactly (1, -g) (every step is exact).
+    if (fabs(m[0][0]) < 1.0) {
+      sol[0] = 1.0;
+      sol[1] = -m[0][0];
+    } else {
+      fullpiv_solve_t<K + 1>(m, rhs, sol);
+    }
+  } else {
+    fullpiv_solve_t<K + 1>(m, rhs, sol);
+  }
   bool ok = true;
 #pragma unroll
   for (int i = 0; i <= K; ++i) ok = ok && isfinite(sol[i]);
