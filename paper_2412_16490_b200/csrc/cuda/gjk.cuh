@@ -270,6 +270,41 @@ GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (
   }
 }
 
+// FullPivLU on the 2-point KKT system [[a, b, 1], [b, c, 1], [1, 1, 0]],
+// rhs e_2, along its pivot path when |a|, |b| < 1 and |c| <= 1 (first pivot:
+// the 1 at (2, 0), the first entry of largest magnitude in column-major
+// order) and |c - b|, |b - a| < 1 (second: the 1 at (1, 2), columns 1 and 2
+// swapped): the same operations on the same operands as fullpiv_solve_t,
+// so the result is bit-identical; returns false off that path.
+GDEV_FN bool kkt2_fast(double a, double b, double c, double (&sol)[3]) {
+  if (!(fabs(a) < 1.0 && fabs(b) < 1.0 && fabs(c) <= 1.0)) return false;
+  const double cb = c - b * 1.0, ba = b - a * 1.0;
+  if (!(fabs(cb) < 1.0 && fabs(ba) < 1.0)) return false;
+  const double e = ba - 1.0 * cb;
+  const double maxpivot = e != 0.0 ? fmax(1.0, fabs(e)) : 1.0;
+  const double thresh = maxpivot * (3 * 2.220446049250313e-16);
+  const bool rank3 = e != 0.0 && fabs(e) > thresh;
+  // forward substitution (unit lower) on the permuted rhs (1, 0, 0)
+  double c0 = 1.0, c1 = 0.0 - 1.0 * b, c2 = 0.0 - 1.0 * a;
+  if (c1 != 0.0) c2 = c2 - c1 * 1.0;
+  // back substitution on the rank block
+  if (rank3 && c2 != 0.0) {
+    c2 = c2 / e;
+    c1 = c1 - c2 * cb;
+    c0 = c0 - c2 * 1.0;
+  }
+  if (c1 != 0.0) {
+    c1 = c1 / 1.0;
+    c0 = c0 - c1 * 0.0;
+  }
+  if (c0 != 0.0) c0 = c0 / 1.0;
+  // column permutation (0, 2, 1)
+  sol[0] = c0;
+  sol[2] = c1;
+  sol[1] = rank3 ? c2 : 0.0;
+  return true;
+}
+
 struct Simplex {
   double dist2;
   D3 v;
@@ -402,6 +437,8 @@ GDEV_FN void simplex_subset(const D3 (&P)[4], const int (&id)[4], Simplex& best)
     } else {
       fullpiv_solve_t<K + 1>(m, rhs, sol);
     }
+  } else if constexpr (K == 2) {
+    if (!kkt2_fast(m[0][0], m[0][1], m[1][1], sol)) fullpiv_solve_t<K + 1>(m, rhs, sol);
   } else {
     fullpiv_solve_t<K + 1>(m, rhs, sol);
   }
