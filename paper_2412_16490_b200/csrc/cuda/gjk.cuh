@@ -143,17 +143,73 @@ GDEV_FN int cycle_step(GjkCycle& c, const unsigned (&key)[4], int ns, int iter) 
 // order), the same eliminations (padded entries stay +0), stops at the same
 // step, and the rank threshold uses s_real. So one body of size S serves all
 // smaller systems (instruction-cache footprint).
-template <int S>
+//
+// KKT = true: m is a subset KKT matrix [[G, 1], [1^T, 0]]. When every |G_r0|
+// < 1 and every other |G_rc| <= 1, the first pivot is the 1 at (S-1, 0) (the
+// first entry of largest magnitude in column-major order); after that
+// elimination the step-1 block's last column is exactly 1, so when its other
+// columns are all below 1 in magnitude the second pivot is the 1 at
+// (1, S-1). On that path the two searches and the select-chain swaps are
+// replaced by the known fixed swaps; every arithmetic operation is the same.
+template <int S, bool KKT = false>
 GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (&sol)[S], int s_real = S) {
   int rowt[S], colt[S];
   int nonzero = S;
   double maxpivot = 0.0;
   bool stopped = false;
+  bool fast = false;
+  if constexpr (KKT) {
+    fast = true;
+#pragma unroll
+    for (int r = 0; r < S - 1; ++r) {
+      fast = fast && fabs(m[r][0]) < 1.0;
+#pragma unroll
+      for (int c = 1; c < S - 1; ++c) fast = fast && fabs(m[r][c]) <= 1.0;
+    }
+  }
 #pragma unroll
   for (int k = 0; k < S; ++k) {
     rowt[k] = k;
     colt[k] = k;
     if (stopped) continue;
+    if constexpr (KKT) {
+      if (k == 1 && fast) {
+#pragma unroll
+        for (int r = 1; r < S; ++r)
+#pragma unroll
+          for (int c = 1; c < S - 1; ++c) fast = fast && fabs(m[r][c]) < 1.0;
+      }
+      if (k < 2 && fast) {
+        maxpivot = fmax(maxpivot, 1.0);
+        if (k == 0) {
+          rowt[0] = S - 1;
+#pragma unroll
+          for (int c = 0; c < S; ++c) {
+            const double t = m[0][c];
+            m[0][c] = m[S - 1][c];
+            m[S - 1][c] = t;
+          }
+        } else {
+          colt[1] = S - 1;
+#pragma unroll
+          for (int r = 0; r < S; ++r) {
+            const double t = m[r][1];
+            m[r][1] = m[r][S - 1];
+            m[r][S - 1] = t;
+          }
+        }
+        const double piv = m[k][k];
+#pragma unroll
+        for (int r = k + 1; r < S; ++r) m[r][k] /= piv;
+#pragma unroll
+        for (int c = k + 1; c < S; ++c) {
+          const double mkc = m[k][c];
+#pragma unroll
+          for (int r = k + 1; r < S; ++r) m[r][c] -= m[r][k] * mkc;
+        }
+        continue;
+      }
+    }
     double biggest = -1.0;
     int br = k, bc = k;
 #pragma unroll
@@ -440,7 +496,7 @@ GDEV_FN void simplex_subset(const D3 (&P)[4], const int (&id)[4], Simplex& best)
   } else if constexpr (K == 2) {
     if (!kkt2_fast(m[0][0], m[0][1], m[1][1], sol)) fullpiv_solve_t<K + 1>(m, rhs, sol);
   } else {
-    fullpiv_solve_t<K + 1>(m, rhs, sol);
+    fullpiv_solve_t<K + 1, true>(m, rhs, sol);
   }
   bool ok = true;
 #pragma unroll

@@ -47,6 +47,40 @@ int main() {
       if (std::memcmp(s1, sp, sizeof s1) || sp[3] != 0.0 || sp[4] != 0.0) ++badpad;
     }
   }
+  // 3- and 4-point KKT systems: fixed-pivot fast path == generic FullPivLU
+  long bad34 = 0;
+  for (long t = 0; t < 300000; ++t) {
+    const int K = 3 + (int)(t & 1);
+    D3 P[4];
+    const double sc = std::ldexp(1.0, -(int)(rng() % 10));
+    for (int i = 0; i < 4; ++i) P[i] = sc * mk(U(rng), U(rng), U(rng));
+    if (t % 5 == 0) P[2] = P[0] + 0.5 * (P[1] - P[0]);  // collinear
+    if (t % 7 == 0) P[3] = P[0] + 0.3 * (P[1] - P[0]) + 0.2 * (P[2] - P[0]);  // coplanar
+    if (t % 9 == 0) P[1] = P[0];
+    if (t % 11 == 0) for (int i = 0; i < 4; ++i) P[i] = mk(P[i].x, P[i].y, 0.0);
+    double g[4][4];
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) g[i][j] = dot(P[i], P[j]);
+    if (K == 3) {
+      double m1[4][4], m2[4][4], r[4] = {0, 0, 0, 1}, s1[4], s2[4];
+      for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) m1[i][j] = (i < 3 && j < 3) ? g[i][j] : ((i == 3) != (j == 3) ? 1.0 : 0.0);
+      std::memcpy(m2, m1, sizeof m1);
+      fullpiv_solve_t<4>(m1, r, s1);
+      fullpiv_solve_t<4, true>(m2, r, s2);
+      if (std::memcmp(s1, s2, sizeof s1)) ++bad34;
+    } else {
+      double m1[5][5], m2[5][5], r[5] = {0, 0, 0, 0, 1}, s1[5], s2[5];
+      for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) m1[i][j] = (i < 4 && j < 4) ? g[i][j] : ((i == 4) != (j == 4) ? 1.0 : 0.0);
+      std::memcpy(m2, m1, sizeof m1);
+      fullpiv_solve_t<5>(m1, r, s1);
+      fullpiv_solve_t<5, true>(m2, r, s2);
+      if (std::memcmp(s1, s2, sizeof s1)) ++bad34;
+    }
+  }
+  std::printf("bad34 %ld\n", bad34);
+  if (bad34) return 1;
   long cr_bad = 0, n_cr = 2000000;
   std::uniform_real_distribution<double> A(-4.0, 4.0);
   for (long i = 0; i < n_cr; ++i) {
