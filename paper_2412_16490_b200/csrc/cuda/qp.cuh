@@ -264,14 +264,23 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
         rp[e] = 0.0;
       }
     }
-#pragma unroll
-    for (int e = 0; e < KMAX; ++e) rp[e] = e < k ? (rp[e] - betap * bsum) * inv_a : 0.0;
-    // t = U^T r' over the column: (sqrt2 W r', sqrt(rho) sum r')
+    // r' = B^-1 rhs = (rhs - betap sum rhs) / a is never formed: its sums
+    // over the edges follow from those of rhs, and xt below folds 1/a in.
+    const double bb = betap * bsum;
     double tv[7];
     {
-      D3 f, t;
-      double s0;
-      w_times(rp, f, t, s0);
+      double s1r = 0.0, s2r = 0.0;
+#pragma unroll
+      for (int e = 0; e < KMAX; ++e) {
+        if (e < k) {
+          s1r += P.cos_t[e] * rp[e];
+          s2r += P.sin_t[e] * rp[e];
+        }
+      }
+      const double s0 = (bsum - k * bb) * inv_a;
+      const double s1 = (s1r - ccos * bb) * inv_a, s2 = (s2r - csin * bb) * inv_a;
+      const D3 f = s0 * fn + mu * (s1 * fd + s2 * fe);
+      const D3 t = cross(fp, f);
       const double tl[7] = {sqrt2 * f.x, sqrt2 * f.y, sqrt2 * f.z, sqrt2 * t.x, sqrt2 * t.y, sqrt2 * t.z,
                             sqrt_rho * s0};
 #pragma unroll
@@ -312,12 +321,13 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     const double ua = sqrt2 * nw + sqrt_rho * sv[6], ub = sqrt2 * mu * dw, uc = sqrt2 * mu * ew;
     const double us_sum = k * ua + ccos * ub + csin * uc;
     const double ga = (ua - betap * us_sum) * inv_a, gb = ub * inv_a, gc = uc * inv_a;
+    const double h0 = bb * inv_a + ga;
     double xt[KMAX];
     double ztc = 0.0;
 #pragma unroll
     for (int e = 0; e < KMAX; ++e) {
       if (e < k) {
-        xt[e] = ((rp[e] - ga) - gb * P.cos_t[e]) - gc * P.sin_t[e];
+        xt[e] = ((inv_a * rp[e] - h0) - gb * P.cos_t[e]) - gc * P.sin_t[e];
         ztc += xt[e];
       } else {
         xt[e] = 0.0;
