@@ -195,6 +195,22 @@ int grasp_qp_batch(grasp_ctx* ctx, const grasp_run_params* p, int n_grasps, int 
                    const double* warm_x, const double* warm_y, double* X, double* Y, double* Z, int* iters,
                    int* converged, double* per_direction, int device_ptrs);
 
+/* ---- evaluation (eval.cpp:51-158) ------------------ */
+typedef struct grasp_eval_params {
+  double mass, gravity, residual_rel_tol, force_budget_factor, contact_tol, penetration_tol, qp_eps;
+} grasp_eval_params;
+/* EvalParams{} defaults (config.hpp:66-74). */
+void grasp_eval_params_default(grasp_eval_params* e);
+/* quasi_static_check(model, {x, x_s}, object, cfg) (eval.cpp:91-158) for n grasps on the
+ * device: penetration_depth over every (link, part) pair, self_penetration_depth over the
+ * collision pairs, contact_distance_consistency of the fingertip witnesses at x, and the six
+ * gravity-resistance QPs on the witnesses within contact_tol at x_s. out_real[n*9] = pd_mm,
+ * spd_mm, cdc_mm, per_direction_residuals[6]; out_int[n*3] = contact_count, success,
+ * note flags (1 no contacts, 2 resistance qp unconverged, 4 gravity residual above
+ * tolerance, 8 fewer than two contacts, 16 penetration above tolerance). */
+int grasp_eval(grasp_ctx* ctx, const grasp_run_params* p, const grasp_eval_params* e, int n, const double* x,
+               const double* x_s, double* out_real, int* out_int);
+
 /* ---- teacher-forced surfaces (parity tests call the kernels piecewise) -- */
 /* point_to_mesh(p, object.parts) for n points: out[n*8] = distance, point_b(3),
  * normal(3), part_index (geometry.cpp:527-542). */

@@ -52,6 +52,7 @@ def lib():
             "oracle_qp_batch": (C.c_int, [_vp, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _ip, _ip, _dp,
                                           C.c_int]),
             "oracle_synthesize": (C.c_int, [_vp, _vp, _vp, C.c_int, _dp, C.c_int, _vp, _lp]),
+            "oracle_eval": (C.c_int, [_vp, _vp, _vp, _dp, C.c_int, _dp, _dp, _dp, _ip]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -160,6 +161,23 @@ def qp_batch(cfg, frames, m, warm_x=None, warm_y=None, threads=1):
     _check(lib().oracle_qp_batch(ref(p), g, m, _d(frames), _d(warm_x), _d(warm_y), _d(X), _d(Y), _d(Z), _i(iters),
                                  _i(conv), _d(per), int(threads)))
     return dict(X=X, Y=Y, Z=Z, iters=iters, converged=conv, per_direction=per)
+
+
+def evaluate(hand, obj, cfg, x, x_s):
+    """quasi_static_check per grasp (eval.cpp:91-158) -> dict of arrays; notes as flags
+    (1 no contacts, 2 qp unconverged, 4 residual above tol, 8 < 2 contacts, 16 penetration)."""
+    x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
+    x_s = np.ascontiguousarray(np.atleast_2d(x_s), dtype=np.float64)
+    n = len(x)
+    e = cfg.eval
+    ev = np.array([e.mass, e.gravity, e.residual_rel_tol, e.force_budget_factor, e.contact_tol, e.penetration_tol,
+                   e.qp_eps])
+    real = np.zeros((n, 9))
+    ints = np.zeros((n, 3), dtype=np.int32)
+    p = cfg.to_params()
+    _check(lib().oracle_eval(ref(hand.desc), ref(obj.desc), ref(p), _d(ev), n, _d(x), _d(x_s), _d(real), _i(ints)))
+    return dict(pd_mm=real[:, 0], spd_mm=real[:, 1], cdc_mm=real[:, 2], residuals=real[:, 3:9],
+                contact_count=ints[:, 0], success=ints[:, 1].astype(bool), note_flags=ints[:, 2])
 
 
 def synthesize(hand, obj, cfg, x0, workers=1, with_stats=False):

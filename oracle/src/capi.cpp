@@ -323,6 +323,37 @@ int oracle_fine_contact_query(const grasp_hand_desc* hd, const grasp_object_desc
   });
 }
 
+// Grasp evaluation (eval.cpp:51-158). ev = {mass, gravity, residual_rel_tol,
+// force_budget_factor, contact_tol, penetration_tol, qp_eps}. Per grasp:
+// out_real[9] = pd_mm, spd_mm, cdc_mm, residuals[6]; out_int[3] =
+// contact_count, success, note_flags.
+int oracle_eval(const grasp_hand_desc* hd, const grasp_object_desc* od, const grasp_run_params* p, const double* ev,
+                int n, const double* x, const double* x_s, double* out_real, int* out_int) {
+  return guarded([&] {
+    const Hand h = make_hand(hd);
+    const Object obj = make_object(od);
+    const Config cfg = make_config(p);
+    EvalParams e;
+    e.mass = ev[0], e.gravity = ev[1], e.residual_rel_tol = ev[2], e.force_budget_factor = ev[3];
+    e.contact_tol = ev[4], e.penetration_tol = ev[5], e.qp_eps = ev[6];
+    const int D = h.dims();
+    for (int g = 0; g < n; ++g) {
+      const VecX xv(x + static_cast<size_t>(g) * D, x + static_cast<size_t>(g + 1) * D);
+      const VecX xs(x_s + static_cast<size_t>(g) * D, x_s + static_cast<size_t>(g + 1) * D);
+      const EvalResult r = quasi_static_check(h, obj, cfg, e, xv, xs);
+      double* o = out_real + static_cast<size_t>(g) * 9;
+      o[0] = r.pd_mm;
+      o[1] = r.spd_mm;
+      o[2] = r.cdc_mm;
+      for (int j = 0; j < 6; ++j) o[3 + j] = r.residuals[j];
+      int* oi = out_int + static_cast<size_t>(g) * 3;
+      oi[0] = r.contact_count;
+      oi[1] = r.success ? 1 : 0;
+      oi[2] = r.note_flags;
+    }
+  });
+}
+
 // Lower QP batch, one 6-column batch per grasp (energy.cpp:60-92).
 int oracle_qp_batch(const grasp_run_params* p, int n_grasps, int m, const double* frames, const double* warm_x,
                     const double* warm_y, double* X, double* Y, double* Z, int* iters, int* converged,

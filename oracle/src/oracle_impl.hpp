@@ -140,7 +140,8 @@ struct EnergyReport {
 };
 MatX closure_directions();
 EnergyReport grasp_energy(const std::vector<Frame>& frames, double beta, double gamma_per_contact, double mu, int k,
-                          const QpParams& qp, const MatX* warm_x, const MatX* warm_y);
+                          const QpParams& qp, const MatX* warm_x, const MatX* warm_y,
+                          const MatX* targets = nullptr);
 VecX grasp_energy_gradient(const std::vector<Frame>& frames, const EnergyReport& rep, double mu, int k,
                            const std::vector<MatX>& jac_p, const std::vector<MatX>& jac_n);
 
@@ -168,6 +169,25 @@ struct Witness {
   int link = -1;
 };
 std::vector<Witness> fine_contact_query(const Hand& h, const Fk& fk, const Object& obj);
+
+// ---- eval (eval.cpp:51-158) --------------------------------------------
+struct EvalParams {
+  double mass = 0.03, gravity = 9.8, residual_rel_tol = 1e-3, force_budget_factor = 20.0;
+  double contact_tol = 0.002, penetration_tol = 0.003, qp_eps = 1e-8;
+};
+struct EvalResult {
+  bool success = false;
+  double residuals[6] = {0, 0, 0, 0, 0, 0};
+  double pd_mm = 0.0, spd_mm = 0.0, cdc_mm = 0.0;
+  int contact_count = 0;
+  int note_flags = 0;  // 1 no contacts, 2 qp unconverged, 4 residual, 8 < 2 contacts, 16 penetration
+};
+double penetration_depth(const Hand& h, const VecX& x, const Object& obj);
+double self_penetration_depth(const Hand& h, const VecX& x);
+double contact_distance_consistency(const Hand& h, const VecX& x, const Object& obj);
+struct Config;
+EvalResult quasi_static_check(const Hand& h, const Object& obj, const Config& cfg, const EvalParams& ep,
+                              const VecX& x, const VecX& x_s);
 
 struct QpScratch {
   MatX forces, duals;

@@ -470,10 +470,10 @@ MatX closure_directions() {
 
 // energy.cpp:60-92.
 EnergyReport grasp_energy(const std::vector<Frame>& frames, double beta, double gamma_per_contact, double mu, int k,
-                          const QpParams& qp, const MatX* warm_x, const MatX* warm_y) {
+                          const QpParams& qp, const MatX* warm_x, const MatX* warm_y, const MatX* targets) {
   const int m = static_cast<int>(frames.size());
   if (m < 1) throw std::invalid_argument("grasp energy needs at least one contact");
-  const MatX dirs = closure_directions();
+  const MatX dirs = targets ? *targets : closure_directions();
   const MatX W = wrench_basis(frames, mu, k);
   const SharedBatch batch = assemble_lower_qp(W, m, dirs, beta, gamma_per_contact * m);
   const BatchSolution sol = solve_shared(batch, qp, warm_x, warm_y);

@@ -53,6 +53,12 @@ class StageParams(C.Structure):
                 ("step_joints", C.c_double), ("step_floor", C.c_double)]
 
 
+class EvalParamsStruct(C.Structure):
+    _fields_ = [("mass", C.c_double), ("gravity", C.c_double), ("residual_rel_tol", C.c_double),
+                ("force_budget_factor", C.c_double), ("contact_tol", C.c_double), ("penetration_tol", C.c_double),
+                ("qp_eps", C.c_double)]
+
+
 class RunParams(C.Structure):
     _fields_ = [
         ("qp_rho", C.c_double), ("qp_sigma", C.c_double), ("qp_alpha", C.c_double),
@@ -101,6 +107,9 @@ SIGNATURES = {
     "grasp_ctx_set_object": (C.c_int, [C.c_void_p, C.POINTER(ObjectDesc)]),
     "grasp_synthesize": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.c_int, _dp, C.POINTER(Out)]),
     "grasp_synthesize_device": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.c_int, _dp, C.POINTER(Out)]),
+    "grasp_eval_params_default": (None, [C.POINTER(EvalParamsStruct)]),
+    "grasp_eval": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.POINTER(EvalParamsStruct), C.c_int, _dp, _dp, _dp,
+                             C.POINTER(C.c_int)]),
     "grasp_qp_batch": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp,
                                  _dp, _ip, _ip, _dp, C.c_int]),
     "grasp_point_to_mesh": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp]),

@@ -475,6 +475,23 @@ class Engine:
                 "gjk_pairs_le4", "gjk_pairs_le8", "gjk_pairs_le16", "gjk_pairs_le32", "gjk_pairs_le64",
                 "gjk_pairs_gt64", "gjk_cycle_jumps", "gjk_iters_skipped", "reserved18", "reserved19")
 
+    def evaluate(self, config: RunConfig, x, x_s) -> dict:
+        """quasi_static_check (eval.cpp:91-158) for each grasp on the device: pd_mm, spd_mm, cdc_mm,
+        residuals (6), contact_count, success, note_flags (1 no contacts, 2 resistance qp unconverged,
+        4 gravity residual above tolerance, 8 fewer than two contacts, 16 penetration above tolerance)."""
+        x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
+        x_s = np.ascontiguousarray(np.atleast_2d(x_s), dtype=np.float64)
+        n = len(x)
+        e = N.EvalParamsStruct(config.eval.mass, config.eval.gravity, config.eval.residual_rel_tol,
+                               config.eval.force_budget_factor, config.eval.contact_tol,
+                               config.eval.penetration_tol, config.eval.qp_eps)
+        real = np.zeros((n, 9))
+        ints = np.zeros((n, 3), dtype=np.int32)
+        N.check(N.lib().grasp_eval(self._ctx, C.byref(config.to_params()), C.byref(e), n, dptr(x), dptr(x_s),
+                                   dptr(real), iptr(ints)))
+        return dict(pd_mm=real[:, 0], spd_mm=real[:, 1], cdc_mm=real[:, 2], residuals=real[:, 3:9],
+                    contact_count=ints[:, 0], success=ints[:, 1].astype(bool), note_flags=ints[:, 2])
+
     def profile(self) -> dict:
         ms = (C.c_double * 8)()
         launches = (C.c_longlong * 8)()

@@ -89,6 +89,7 @@ struct grasp_ctx {
 
   // hand
   DevHand H{};
+  DevBuf<int> h_cpa, h_cpb;
   DevBuf<int> h_lpj, h_depth, h_path, h_jpl, h_proxy_link, h_tip_link, h_tip_proxy, h_spa, h_spb, h_lvbeg,
       h_tip_slots, h_tip_links_sorted, h_link_tip;
   DevBuf<unsigned> h_subtree;
@@ -293,6 +294,12 @@ struct grasp_ctx {
     h_tip_slots.upload(tip_proxy, s);
     h_envelope.upload(envelope, s);
     h_spa.upload(spa, s);
+    {
+      std::vector<int> ca(d->n_pairs), cb(d->n_pairs);
+      for (int i = 0; i < d->n_pairs; ++i) ca[i] = d->collision_pairs[2 * i], cb[i] = d->collision_pairs[2 * i + 1];
+      h_cpa.upload(ca, s);
+      h_cpb.upload(cb, s);
+    }
     h_spb.upload(spb, s);
     h_lvbeg.upload(std::vector<int>(d->link_vert_begin, d->link_vert_begin + L + 1), s);
     h_lverts.upload(std::vector<double>(d->verts, d->verts + 3 * d->n_verts), s);
@@ -328,6 +335,9 @@ struct grasp_ctx {
     H.tip_proxy = h_tip_proxy.p;
     H.tip_envelope = h_envelope.p;
     H.sp_a = h_spa.p;
+    H.ncp = d->n_pairs;
+    H.cp_a = h_cpa.p;
+    H.cp_b = h_cpb.p;
     H.sp_b = h_spb.p;
     H.link_vbeg = h_lvbeg.p;
     H.link_verts = h_lverts.p;
@@ -650,6 +660,7 @@ struct grasp_ctx {
     P.w_self = p->w_self_penetration;
     P.w_pen = p->w_object_penetration;
     P.fd_step = p->fd_step;
+    P.target_sign = 1.0;
     for (int j = 0; j < p->n_edges && j < kMaxEdges; ++j) {
       const double th = 2.0 * std::numbers::pi * j / p->n_edges;  // contact.cpp:35
       P.cos_t[j] = std::cos(th);
@@ -937,6 +948,158 @@ int grasp_synthesize(grasp_ctx* ctx, const grasp_run_params* p, int batch, const
 int grasp_synthesize_device(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0_dev,
                             grasp_out* out_dev) {
   return synthesize_impl(ctx, p, batch, x0_dev, out_dev, true);
+}
+
+void grasp_eval_params_default(grasp_eval_params* e) {
+  if (!e) return;
+  e->mass = 0.03;  // config.hpp EvalParams defaults
+  e->gravity = 9.8;
+  e->residual_rel_tol = 1e-3;
+  e->force_budget_factor = 20.0;
+  e->contact_tol = 0.002;
+  e->penetration_tol = 0.003;
+  e->qp_eps = 1e-8;
+}
+
+int grasp_eval(grasp_ctx* ctx, const grasp_run_params* p, const grasp_eval_params* e, int n, const double* x,
+               const double* x_s, double* out_real, int* out_int) {
+  return guard([&] {
+    if (!p || !e || !x || !x_s || !out_real || !out_int) throw std::invalid_argument("null argument");
+    require_models(ctx);
+    ctx->set_device();
+    const int m = ctx->H.m, D = ctx->H.D, k = p->n_edges;
+    if (k < 3 || k > kMaxEdges) throw std::invalid_argument("n_edges must lie in [3, 8]");
+    ctx->ensure_state(n, m, k);
+    ctx->reset_run_state(n);
+    cudaStream_t s = ctx->stream;
+    const DevParams P = ctx->make_params(p, m);
+    // eval.cpp:51-89 at x: every (link, part) pair, every collision pair, fingertip witnesses.
+    ck(cudaMemcpyAsync(ctx->x.p, x, sizeof(double) * n * D, cudaMemcpyHostToDevice, s), "x");
+    ctx->launch_fk(P);
+    ctx->launch_pairs(false);
+    DevBuf<double> self_d, pd, spd;
+    self_d.ensure(static_cast<size_t>(n) * std::max(ctx->H.ncp, 1));
+    pd.ensure(n);
+    spd.ensure(n);
+    if (ctx->H.ncp > 0)
+      k_eval_self_pairs<<<grasp_ctx::blocks(static_cast<long long>(n) * ctx->H.ncp, 128), 128, 0, s>>>(ctx->H, ctx->st,
+                                                                                                   self_d.p);
+    k_eval_depths<<<grasp_ctx::blocks(n, 128), 128, 0, s>>>(ctx->H, ctx->O, ctx->st, self_d.p, pd.p, spd.p);
+    ctx->launch_queries(true);
+    ctx->launch_pairs(true);
+    k_final_frames<<<grasp_ctx::blocks(static_cast<long long>(n) * m, 128), 128, 0, s>>>(ctx->H, ctx->O, ctx->st,
+                                                                                      ctx->witness.p);
+    ck(cudaGetLastError(), "launch");
+    ctx->check_errors();
+    std::vector<double> w_x(static_cast<size_t>(n) * m * 11), w_s(static_cast<size_t>(n) * m * 11), h_pd(n), h_spd(n);
+    copy_out(w_x.data(), ctx->witness.p, sizeof(double) * w_x.size(), cudaMemcpyDeviceToHost, s);
+    copy_out(h_pd.data(), pd.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+    copy_out(h_spd.data(), spd.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+    // fingertip witnesses at the squeeze pose (eval.cpp:109-112)
+    ck(cudaMemcpyAsync(ctx->x.p, x_s, sizeof(double) * n * D, cudaMemcpyHostToDevice, s), "x_s");
+    ctx->launch_fk(P);
+    ctx->launch_queries(true);
+    ctx->launch_pairs(true);
+    k_final_frames<<<grasp_ctx::blocks(static_cast<long long>(n) * m, 128), 128, 0, s>>>(ctx->H, ctx->O, ctx->st,
+                                                                                      ctx->witness.p);
+    ck(cudaGetLastError(), "launch");
+    ctx->check_errors();
+    copy_out(w_s.data(), ctx->witness.p, sizeof(double) * w_s.size(), cudaMemcpyDeviceToHost, s);
+    ck(cudaStreamSynchronize(s), "sync");
+    const double mg = e->mass * e->gravity;
+    const double tau = e->residual_rel_tol * mg;
+    std::vector<int> count(n, 0);
+    std::vector<std::vector<int>> groups(m + 1);
+    std::vector<double> frames(static_cast<size_t>(n) * m * 12, 0.0);
+    for (int g = 0; g < n; ++g) {
+      double* o = out_real + static_cast<size_t>(g) * 9;
+      o[0] = h_pd[g];
+      o[1] = h_spd[g];
+      // contact_distance_consistency (eval.cpp:84-89): max - min of the witness distances
+      double lo = INFINITY, hi = -INFINITY;
+      for (int f = 0; f < m; ++f) {
+        const double d = w_x[(static_cast<size_t>(g) * m + f) * 11 + 9];
+        lo = std::min(lo, d);
+        hi = std::max(hi, d);
+      }
+      o[2] = m > 0 ? 1000.0 * (hi - lo) : 0.0;
+      // attached contacts at x_s: frames build_frame(p_w, -n) (eval.cpp:109-112)
+      int c = 0;
+      for (int f = 0; f < m; ++f) {
+        const double* w = w_s.data() + (static_cast<size_t>(g) * m + f) * 11;
+        if (!(w[9] <= e->contact_tol)) continue;
+        build_frame(ld3(w + 3), -ld3(w + 6), frames.data() + (static_cast<size_t>(g) * m + c) * 12);
+        ++c;
+      }
+      count[g] = c;
+      groups[c].push_back(g);
+    }
+    // Resistance QPs (eval.cpp:119-137), batched by contact count: beta = mg / cap
+    // with cap = factor * mg / c, gamma = gamma_per_contact * c, eval tolerance,
+    // targets minus gravity.
+    std::vector<double> per(static_cast<size_t>(n) * 6, 0.0);
+    std::vector<int> conv(static_cast<size_t>(n) * 6, 1);
+    for (int c = 1; c <= m; ++c) {
+      const auto& gl = groups[c];
+      if (gl.empty()) continue;
+      const int ng = static_cast<int>(gl.size());
+      std::vector<double> fr(static_cast<size_t>(ng) * c * 12);
+      for (int i = 0; i < ng; ++i)
+        std::memcpy(fr.data() + static_cast<size_t>(i) * c * 12, frames.data() + static_cast<size_t>(gl[i]) * m * 12,
+                    sizeof(double) * c * 12);
+      const double cap = e->force_budget_factor * mg / static_cast<double>(c);
+      grasp_run_params q = *p;
+      q.beta = mg / cap;
+      q.qp_eps_primal = e->qp_eps;
+      q.qp_eps_dual = e->qp_eps;
+      DevParams PQ = ctx->make_params(&q, c);
+      PQ.target_sign = -1.0;
+      DevState saved = ctx->st;
+      ctx->st.G = ng;
+      ck(cudaMemsetAsync(ctx->failed.p, 0, sizeof(int) * ng, s), "memset");
+      ck(cudaMemsetAsync(ctx->qp_ready.p, 0, sizeof(int) * ng, s), "memset");
+      ck(cudaMemcpyAsync(ctx->frames.p, fr.data(), sizeof(double) * fr.size(), cudaMemcpyHostToDevice, s), "frames");
+      ctx->launch_qp(PQ, c, 2, 0);
+      ck(cudaGetLastError(), "k_qp launch");
+      std::vector<double> pd6(static_cast<size_t>(ng) * 6);
+      std::vector<int> cv6(static_cast<size_t>(ng) * 6);
+      copy_out(pd6.data(), ctx->qp_perdir.p, sizeof(double) * pd6.size(), cudaMemcpyDeviceToHost, s);
+      copy_out(cv6.data(), ctx->qp_conv.p, sizeof(int) * cv6.size(), cudaMemcpyDeviceToHost, s);
+      ck(cudaStreamSynchronize(s), "qp sync");
+      ctx->st = saved;
+      for (int i = 0; i < ng; ++i)
+        for (int j = 0; j < 6; ++j) {
+          per[static_cast<size_t>(gl[i]) * 6 + j] = cap * std::sqrt(std::max(pd6[static_cast<size_t>(i) * 6 + j], 0.0));
+          conv[static_cast<size_t>(gl[i]) * 6 + j] = cv6[static_cast<size_t>(i) * 6 + j];
+        }
+    }
+    for (int g = 0; g < n; ++g) {
+      double* o = out_real + static_cast<size_t>(g) * 9;
+      int* oi = out_int + static_cast<size_t>(g) * 3;
+      int flags = 0;
+      bool resisted = false;
+      if (count[g] == 0) {
+        for (int j = 0; j < 6; ++j) o[3 + j] = mg;
+        flags |= 1;
+      } else {
+        bool all_conv = true;
+        resisted = true;
+        for (int j = 0; j < 6; ++j) {
+          o[3 + j] = per[static_cast<size_t>(g) * 6 + j];
+          all_conv = all_conv && conv[static_cast<size_t>(g) * 6 + j];
+          resisted = resisted && o[3 + j] <= tau;
+        }
+        if (!all_conv) flags |= 2;
+        if (!resisted) flags |= 4;
+      }
+      if (count[g] < 2) flags |= 8;
+      const bool shallow = o[0] <= 1000.0 * e->penetration_tol;
+      if (!shallow) flags |= 16;
+      oi[0] = count[g];
+      oi[1] = (resisted && count[g] >= 2 && shallow) ? 1 : 0;
+      oi[2] = flags;
+    }
+  });
 }
 
 int grasp_qp_batch(grasp_ctx* ctx, const grasp_run_params* p, int n_grasps, int m, const double* frames,

@@ -1166,6 +1166,58 @@ __global__ void k_pairs_raw(DevHand H, DevObject O, int n, const int* __restrict
   }
 }
 
+// ------------------------------------------------------------- evaluation
+// Grasp evaluation (eval.cpp:51-89) on the state in st.x / st.world.
+// Self-penetration pairs: signed_distance(link a posed, link b posed)
+// (eval.cpp:63-72; geometry.cpp:500-525 with both poses), one thread per
+// (grasp, collision pair); d written to out[g * ncp + i].
+__global__ void __launch_bounds__(128) k_eval_self_pairs(DevHand H, DevState st, double* out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)st.G * H.ncp) return;
+  const int g = (int)(t / H.ncp), i = (int)(t % H.ncp);
+  const int la = H.cp_a[i], lb = H.cp_b[i];
+  Hull A, B;
+  M33 Ra, Rb;
+  const double* wa = st.world + ((size_t)g * H.L + la) * 12;
+  const double* wb = st.world + ((size_t)g * H.L + lb) * 12;
+  for (int k = 0; k < 9; ++k) Ra.m[k] = wa[k], Rb.m[k] = wb[k];
+  const D3 ta = ld3(wa + 9), tb = ld3(wb + 9);
+  A.verts = H.link_verts + 3 * (size_t)H.link_vbeg[la];
+  A.nv = H.link_vbeg[la + 1] - H.link_vbeg[la];
+  A.posed = true;
+  A.R = Ra;
+  A.t = ta;
+  B.verts = H.link_verts + 3 * (size_t)H.link_vbeg[lb];
+  B.nv = H.link_vbeg[lb + 1] - H.link_vbeg[lb];
+  B.posed = true;
+  B.R = Rb;
+  B.t = tb;
+  // cloud_scale (geometry.cpp:17-23)
+  double scale = 1.0;
+  scale = fmax(scale, scale_of(mul(Ra, ld3(H.link_centroid + 3 * la)) + ta, H.link_halfnorm[la]));
+  scale = fmax(scale, scale_of(mul(Rb, ld3(H.link_centroid + 3 * lb)) + tb, H.link_halfnorm[lb]));
+  EpaScratch scratch;
+  const PairResult r = signed_distance(A, B, scale, scratch);
+  if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
+  if (r.flags & kPairOverflow) atomicAdd(st.err + 1, 1);
+  out[t] = r.d;
+}
+
+// Per grasp: penetration depth over every (link, part) pair record and
+// self-penetration depth over the collision pairs, in mm (max(0, -d)).
+__global__ void k_eval_depths(DevHand H, DevObject O, DevState st, const double* __restrict__ self_d, double* pd,
+                              double* spd) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= st.G) return;
+  double depth = 0.0;
+  const int np = H.L * O.P;
+  for (int i = 0; i < np; ++i) depth = fmax(depth, -st.pairs[((size_t)g * st.NP + i) * 12]);
+  pd[g] = 1000.0 * depth;
+  depth = 0.0;
+  for (int i = 0; i < H.ncp; ++i) depth = fmax(depth, -self_d[(size_t)g * H.ncp + i]);
+  spd[g] = 1000.0 * depth;
+}
+
 // ------------------------------------------------------ gradient assembly
 // A force f (world) at world point p on link l contributes J(l,p)^T f to
 // the state gradient (hand.cpp:155-169). With v = R^T (p - t) and

@@ -41,6 +41,9 @@ struct DevHand {
   const int* tip_link;              // [m]
   const int* tip_proxy;             // [m] global proxy index
   const double* tip_envelope;       // [m] envelope_radius (pipeline.cpp:47-52)
+  int ncp;                          // collision link pairs (eval self-penetration depth)
+  const int* cp_a;                  // [ncp]
+  const int* cp_b;
   const int* sp_a;                  // [nsp] self-penetration proxy pairs, reference order
   const int* sp_b;
   const int* link_vbeg;             // [L+1]
@@ -88,6 +91,7 @@ struct DevParams {
   double beta, gamma_total;
   double w_grasp, w_distance, w_limit, w_self, w_pen;
   double fd_step;
+  double target_sign;  // QP targets beta * target_sign * (+-e_axis); -1 for the eval gravity wrenches
   double cos_t[kMaxEdges], sin_t[kMaxEdges];  // host libm cos/sin(2 pi j / k)
 };
 

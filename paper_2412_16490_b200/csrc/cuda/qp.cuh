@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
   const int c = active ? lane % m : 0;
   const int base = j * m;
   const int axis = j >> 1;
-  const double tsign = (j & 1) ? -1.0 : 1.0;
+  const double tsign = ((j & 1) ? -1.0 : 1.0) * P.target_sign;
   const double rho = P.rho, sigma = P.sigma, alpha = P.alpha, mu = P.mu;
   const double inv_a = 1.0 / a_diag;
   const double inv_rho = 1.0 / rho;

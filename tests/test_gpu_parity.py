@@ -344,6 +344,36 @@ def test_mesh_energy_late_stage_matches_oracle(G, O, engine):
     assert (ok | ties).all(), np.where(~(ok | ties))[0]
 
 
+def test_eval_matches_oracle(G, O, engine):
+    """Grasp evaluation on the device (eval.cpp:51-158) vs the oracle on
+    late-stage Shadow/drill states: penetration / self-penetration depths and contact-distance
+    consistency to 1e-6 mm, contact counts and success flags exact, gravity residuals to the
+    QP tolerance."""
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    hand = G.HandModel.from_file(root / "paper_2412_16490_b200/assets/hands/shadow_like.json")
+    obj = G.load_object(root / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+    use(engine, hand, obj)
+    d = np.load(root / "tests/golden/late_states_shadow_drill.npz")
+    x = d["x"]
+    x_s = np.array([G.squeeze_pose(hand, x[i], d["x0"][i]) for i in range(len(x))])
+    x_s2 = x.copy()
+    x_s2[:, 9:12] += 0.002
+    xs_all = np.concatenate([x_s, x_s2, x])
+    x_all = np.concatenate([x, x, x])
+    cfg = G.RunConfig()
+    ref = O.evaluate(hand, obj, cfg, x_all, xs_all)
+    got = engine.evaluate(cfg, x_all, xs_all)
+    np.testing.assert_allclose(got["pd_mm"], ref["pd_mm"], atol=1e-6, rtol=0)
+    np.testing.assert_allclose(got["spd_mm"], ref["spd_mm"], atol=1e-6, rtol=0)
+    np.testing.assert_allclose(got["cdc_mm"], ref["cdc_mm"], atol=1e-6, rtol=0)
+    assert (got["contact_count"] == ref["contact_count"]).all()
+    assert (got["success"] == ref["success"]).all()
+    assert (got["note_flags"] == ref["note_flags"]).all()
+    mg = cfg.eval.mass * cfg.eval.gravity
+    np.testing.assert_allclose(got["residuals"], ref["residuals"], atol=1e-6 * mg, rtol=1e-6)
+
+
 def test_fine_contact_query_matches_oracle(G, O, trident, engine):
     obj = G.make_primitive("box", 0.1)
     use(engine, trident, obj)
