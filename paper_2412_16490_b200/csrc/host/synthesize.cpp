@@ -4,12 +4,14 @@
 #include "../../../include/grasp_b200.h"
 
 #include "capi_common.hpp"
+#include "grasp/eval.hpp"
 #include "grasp/pipeline.hpp"
 
 #include <cmath>
 #include <limits>
 #include <map>
 #include <memory>
+#include <sstream>
 #include <stdexcept>
 
 namespace grasp::pipeline {
@@ -54,9 +56,7 @@ CachedCtx& context_for(int device) {
 
 }  // namespace
 
-std::vector<records::GraspRecord> synthesize(const hand::HandModel& model, const object::ObjectModel& object,
-                                             const RunConfig& cfg, int device) {
-  validate(cfg);
+CachedCtx& bound_context(const hand::HandModel& model, const object::ObjectModel& object, int device) {
   CachedCtx& c = context_for(device);
   if (c.hand != &model) {
     c.packed_hand = capi::pack_hand(model);
@@ -69,6 +69,13 @@ std::vector<records::GraspRecord> synthesize(const hand::HandModel& model, const
     check(grasp_ctx_set_object(c.ctx.get(), &c.packed_object.desc));
     c.object = &object;
   }
+  return c;
+}
+
+std::vector<records::GraspRecord> synthesize(const hand::HandModel& model, const object::ObjectModel& object,
+                                             const RunConfig& cfg, int device) {
+  validate(cfg);
+  CachedCtx& c = bound_context(model, object, device);
   const int B = cfg.batch, D = 12 + model.dof(), m = static_cast<int>(model.fingertip_links.size());
   const int n = m * cfg.contact.n_edges;
   const std::vector<VectorXd> starts = init_poses(model, object, B, cfg.seed, cfg.init);
@@ -128,3 +135,90 @@ std::vector<records::GraspRecord> synthesize(const hand::HandModel& model, const
 }
 
 }  // namespace grasp::pipeline
+
+namespace grasp::eval {
+namespace {
+
+// One device pass over (x, x_s) pairs; notes joined like eval.cpp:139-156.
+std::vector<EvalResult> run_eval(const hand::HandModel& model, const object::ObjectModel& object, const RunConfig& cfg,
+                                 const std::vector<const VectorXd*>& xs, const std::vector<const VectorXd*>& xss,
+                                 int device) {
+  const int n = static_cast<int>(xs.size()), D = 12 + model.dof();
+  for (int g = 0; g < n; ++g)
+    if (static_cast<int>(xs[g]->size()) != D || static_cast<int>(xss[g]->size()) != D)
+      throw std::invalid_argument("quasi_static_check: record poses do not match the hand");
+  pipeline::CachedCtx& c = pipeline::bound_context(model, object, device);
+  std::vector<double> x(static_cast<size_t>(n) * D), x_s(x.size()), real(static_cast<size_t>(n) * 9);
+  std::vector<int> ints(static_cast<size_t>(n) * 3);
+  for (int g = 0; g < n; ++g) {
+    std::copy(xs[g]->begin(), xs[g]->end(), x.begin() + static_cast<size_t>(g) * D);
+    std::copy(xss[g]->begin(), xss[g]->end(), x_s.begin() + static_cast<size_t>(g) * D);
+  }
+  grasp_run_params p;
+  capi::from_config(cfg, &p);
+  grasp_eval_params e{cfg.eval.mass, cfg.eval.gravity, cfg.eval.residual_rel_tol, cfg.eval.force_budget_factor,
+                      cfg.eval.contact_tol, cfg.eval.penetration_tol, cfg.eval.qp_eps};
+  if (n > 0) pipeline::check(grasp_eval(c.ctx.get(), &p, &e, n, x.data(), x_s.data(), real.data(), ints.data()));
+  std::vector<EvalResult> out(n);
+  for (int g = 0; g < n; ++g) {
+    EvalResult& r = out[g];
+    const double* o = real.data() + static_cast<size_t>(g) * 9;
+    r.pd_mm = o[0];
+    r.spd_mm = o[1];
+    r.cdc_mm = o[2];
+    for (int j = 0; j < 6; ++j) r.per_direction_residuals[j] = o[3 + j];
+    r.contact_count = ints[3 * g];
+    r.success = ints[3 * g + 1] != 0;
+    const int f = ints[3 * g + 2];
+    std::vector<std::string> notes;
+    if (f & 1) notes.push_back("no contacts at the squeeze pose");
+    if (f & 2) notes.push_back("resistance qp unconverged");
+    if (f & 4) notes.push_back("gravity wrench residual above tolerance");
+    if (f & 8) notes.push_back("fewer than two contacts");
+    if (f & 16) {
+      std::ostringstream msg;
+      msg << "penetration " << r.pd_mm << " mm above tolerance";
+      notes.push_back(msg.str());
+    }
+    for (const auto& s : notes) {
+      if (!r.notes.empty()) r.notes += "; ";
+      r.notes += s;
+    }
+  }
+  return out;
+}
+
+}  // namespace
+
+std::vector<EvalResult> quasi_static_check(const hand::HandModel& model,
+                                           const std::vector<records::GraspRecord>& records,
+                                           const object::ObjectModel& object, const RunConfig& cfg, int device) {
+  std::vector<const VectorXd*> xs, xss;
+  for (const auto& r : records) {
+    xs.push_back(&r.x);
+    xss.push_back(&r.x_s);
+  }
+  return run_eval(model, object, cfg, xs, xss, device);
+}
+
+EvalResult quasi_static_check(const hand::HandModel& model, const records::GraspRecord& record,
+                              const object::ObjectModel& object, const RunConfig& cfg, int device) {
+  return run_eval(model, object, cfg, {&record.x}, {&record.x_s}, device)[0];
+}
+
+double penetration_depth(const hand::HandModel& model, const VectorXd& x, const object::ObjectModel& object,
+                         int device) {
+  return run_eval(model, object, RunConfig{}, {&x}, {&x}, device)[0].pd_mm;
+}
+
+double self_penetration_depth(const hand::HandModel& model, const VectorXd& x, const object::ObjectModel& object,
+                              int device) {
+  return run_eval(model, object, RunConfig{}, {&x}, {&x}, device)[0].spd_mm;
+}
+
+double contact_distance_consistency(const hand::HandModel& model, const VectorXd& x,
+                                    const object::ObjectModel& object, int device) {
+  return run_eval(model, object, RunConfig{}, {&x}, {&x}, device)[0].cdc_mm;
+}
+
+}  // namespace grasp::eval

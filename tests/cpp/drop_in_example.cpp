@@ -2,6 +2,7 @@
 // (builtin_hand, make_primitive, RunConfig, synthesize), linked against
 // libgrasp_b200.so instead of the reference's static library.
 #include "grasp/config.hpp"
+#include "grasp/eval.hpp"
 #include "grasp/hand.hpp"
 #include "grasp/object.hpp"
 #include "grasp/pipeline.hpp"
@@ -31,6 +32,14 @@ int main() {
   }
   std::printf("records %zu ok %d stages %zu object %s\n", recs.size(), ok, recs[0].stages.size(),
               recs[0].object_id.c_str());
+  // grasp evaluation (eval.hpp): one device pass over all records
+  const auto evals = eval::quasi_static_check(model, recs, sphere, cfg);
+  if (evals.size() != recs.size()) return 5;
+  for (const auto& e : evals)
+    if (!(e.pd_mm >= 0.0) || !(e.spd_mm >= 0.0) || !(e.cdc_mm >= 0.0) || e.contact_count < 0 || e.contact_count > 3)
+      return 6;
+  std::printf("eval: success %d contacts %d pd %.3f mm notes '%s'\n", (int)evals[0].success, evals[0].contact_count,
+              evals[0].pd_mm, evals[0].notes.c_str());
   try {
     RunConfig bad = cfg;
     bad.qp.alpha = 2.5;
