@@ -490,3 +490,32 @@ def test_full_schedule_matches_oracle_statistics(G, O, trident, engine):
     ok = cpu.failed == 0
     for a, b in ((gpu.energy_total[ok], cpu.energy_total[ok]), (gpu.stage_energy[ok, 1, 1], cpu.stage_energy[ok, 1, 1])):
         assert abs(np.median(a) - np.median(b)) <= 0.05 * abs(np.median(b)) + 1e-3
+
+
+@pytest.mark.parametrize("shape", ["sphere", "box"])
+def test_config1_allegro_end_to_end_statistics(G, O, engine, shape):
+    """BASELINE config 1 (Allegro-like hand, primitive object at 0.08, batch 64, 4 contacts,
+    seed 17, default 300/100/100 schedule): GPU synthesis vs the oracle on the same x0 -
+    identical failure flags, matching final-energy statistics, and matching evaluation
+    statistics (quasi-static success rate and median penetration, eval.cpp:91-158), each
+    side evaluated with its own evaluator."""
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    hand = G.HandModel.from_file(root / "paper_2412_16490_b200/assets/hands/allegro_like.json")
+    obj = G.make_primitive(shape, 0.08)
+    use(engine, hand, obj)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 64, 17
+    x0 = G.init_poses(hand, obj, cfg.batch, cfg.seed, cfg.init)
+    gpu = engine.synthesize(cfg, x0)
+    cpu = O.synthesize(hand, obj, cfg, x0, workers=16)
+    assert (gpu.failed == cpu.failed).all()
+    ok = cpu.failed == 0
+    assert ok.sum() >= 48
+    for a, b in ((gpu.energy_total[ok], cpu.energy_total[ok]), (gpu.stage_energy[ok, 1, 1], cpu.stage_energy[ok, 1, 1])):
+        assert abs(np.median(a) - np.median(b)) <= 0.1 * abs(np.median(b)) + 1e-3
+    eg = engine.evaluate(cfg, gpu.x[ok], gpu.x_s[ok])
+    ec = O.evaluate(hand, obj, cfg, cpu.x[ok], cpu.x_s[ok])
+    n = ok.sum()
+    assert abs(eg["success"].mean() - ec["success"].mean()) <= 3.0 / np.sqrt(n) + 0.05
+    assert abs(np.median(eg["pd_mm"]) - np.median(ec["pd_mm"])) <= 0.25 * np.median(ec["pd_mm"]) + 0.5
