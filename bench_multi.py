@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--grasps", type=int, default=1024, help="grasps per object")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=8,
+                    help="engine contexts (streams) per GPU, each driven by a host thread, objects round-robin")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -57,37 +59,61 @@ def main():
     cfg = G.RunConfig()
     B, D, m = args.grasps, hand.dims(), hand.n_tips
     n = m * cfg.contact.n_edges
-    eng = G.Engine(local)
-    eng.set_hand(hand)
-    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)
+    S = max(1, min(args.streams, len(mine)))
+    engs = [G.Engine(local) for _ in range(S)]
+    for e in engs:
+        e.set_hand(hand)
+    streams = [torch.cuda.ExternalStream(e.stream_handle(), device=dev) for e in engs]
+    stream = streams[0]
     per_obj = []
     for idx, shape, scale in mine:
         obj = G.make_primitive(shape, scale)
         c = dataclasses.replace(cfg, batch=B, seed=idx)
         x0 = torch.from_numpy(G.init_poses(hand, obj, B, idx, cfg.init)).to(dev)
         per_obj.append((obj, c, x0))
-    outs = {
-        "x_p": torch.empty(B, D, dtype=torch.float64, device=dev),
-        "x": torch.empty(B, D, dtype=torch.float64, device=dev),
-        "x_s": torch.empty(B, D, dtype=torch.float64, device=dev),
-        "energy_total": torch.empty(B, dtype=torch.float64, device=dev),
-        "per_direction": torch.empty(B, 6, dtype=torch.float64, device=dev),
-        "contact_forces": torch.empty(B, 6 * n, dtype=torch.float64, device=dev),
-        "contacts": torch.empty(B, m * 12, dtype=torch.float64, device=dev),
-        "stage_energy": torch.empty(B, 6, dtype=torch.float64, device=dev),
-        "failed": torch.empty(B, dtype=torch.int32, device=dev),
-        "qp_converged": torch.empty(B, 6, dtype=torch.int32, device=dev),
-    }
-    ptrs = {k: v.data_ptr() for k, v in outs.items()}
+    def make_outs():
+        return {
+            "x_p": torch.empty(B, D, dtype=torch.float64, device=dev),
+            "x": torch.empty(B, D, dtype=torch.float64, device=dev),
+            "x_s": torch.empty(B, D, dtype=torch.float64, device=dev),
+            "energy_total": torch.empty(B, dtype=torch.float64, device=dev),
+            "per_direction": torch.empty(B, 6, dtype=torch.float64, device=dev),
+            "contact_forces": torch.empty(B, 6 * n, dtype=torch.float64, device=dev),
+            "contacts": torch.empty(B, m * 12, dtype=torch.float64, device=dev),
+            "stage_energy": torch.empty(B, 6, dtype=torch.float64, device=dev),
+            "failed": torch.empty(B, dtype=torch.int32, device=dev),
+            "qp_converged": torch.empty(B, 6, dtype=torch.int32, device=dev),
+        }
+    outs = [make_outs() for _ in range(S)]
+    ptrs = [{k: v.data_ptr() for k, v in o.items()} for o in outs]
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     failed = []
+    import threading
+
+    def run_lane(k, record):
+        e = engs[k]
+        for j in range(k, len(per_obj), S):
+            obj, c, x0 = per_obj[j]
+            e.set_object(obj)
+            e.synthesize_device(c, x0.data_ptr(), B, ptrs[k])
+            if record:
+                failed.append(int(outs[k]["failed"].sum().item()))
 
     def step(record=False):
-        for obj, c, x0 in per_obj:
-            eng.set_object(obj)
-            eng.synthesize_device(c, x0.data_ptr(), B, ptrs)
-            if record:
-                failed.append(int(outs["failed"].sum().item()))
+        # every lane's stream starts after the main stream's start event
+        start = torch.cuda.Event()
+        start.record(streams[0])
+        for st in streams[1:]:
+            st.wait_event(start)
+        threads = [threading.Thread(target=run_lane, args=(k, record)) for k in range(S)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for st in streams[1:]:
+            done = torch.cuda.Event()
+            done.record(st)
+            streams[0].wait_event(done)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -124,7 +150,8 @@ def main():
                 "config": {"workload": "BASELINE config 3", "objects": [f"{s}@{sc}" for s in SHAPES for sc in SCALES],
                            "grasps_per_object": B, "iters": [cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters,
                                                              cfg.pipeline.final_stage.iters],
-                           "parallelism": f"objects sharded over {world} rank(s), no collective",
+                           "parallelism": f"objects sharded over {world} rank(s), {S} concurrent engine streams "
+                                          "per GPU, no collective",
                            "l2": "flushed between timed steps (512 MiB device write)"},
                 "failed_grasps_rank0": sum(failed)}
         if not args.no_cpu_baseline:

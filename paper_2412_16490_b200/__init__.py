@@ -8,6 +8,6 @@ from .api import (  # noqa: F401
     ContactFrame, ContactParams, Engine, EnergyParams, EvalParams, GraspRecord, HandModel, InitParams,
     ObjectiveWeights, ObjectModel, PipelineParams, QpParams, RunConfig, StageSchedule, StageTrace,
     SynthesisOutput, builtin_hand_json, init_poses, load_object, make_primitive, parse_object_text,
-    parse_run_config, squeeze_pose, synthesize, validate, PRIMITIVE_NAMES, forward_kinematics,
+    parse_run_config, squeeze_pose, synthesize, synthesize_objects, validate, PRIMITIVE_NAMES, forward_kinematics,
 )
 from .errors import CudaError, GeometryError, GraspError, HandError, InvalidArgument, ObjectError  # noqa: F401

@@ -528,3 +528,45 @@ def synthesize(model: HandModel, obj: ObjectModel, cfg: RunConfig, device: int =
     if eng.obj is not obj:
         eng.set_object(obj)
     return eng.synthesize(cfg, x0).records(cfg, obj)
+
+
+def synthesize_objects(model: HandModel, objects: List[ObjectModel], configs, device: int = 0,
+                       streams: int = 8) -> List[List[GraspRecord]]:
+    """Many objects on one GPU (BASELINE config 3): one synthesize per
+    object (pipeline.cpp:436-457 each, so results equal per-object runs), issued from `streams`
+    host threads, each driving its own engine context and CUDA stream, so several objects'
+    batches share the GPU concurrently. `configs` is one RunConfig or one per object."""
+    import threading
+    from .errors import InvalidArgument
+    if isinstance(configs, RunConfig):
+        configs = [configs] * len(objects)
+    if len(configs) != len(objects):
+        raise InvalidArgument("one RunConfig per object")
+    for c in configs:
+        validate(c)
+    S = max(1, min(int(streams), len(objects)))
+    engines = [Engine(device) for _ in range(S)]
+    for e in engines:
+        e.set_hand(model)
+    out: List[Optional[List[GraspRecord]]] = [None] * len(objects)
+    errors: list = []
+
+    def lane(k):
+        try:
+            e = engines[k]
+            for j in range(k, len(objects), S):
+                obj, cfg = objects[j], configs[j]
+                x0 = init_poses(model, obj, cfg.batch, cfg.seed, cfg.init)
+                e.set_object(obj)
+                out[j] = e.synthesize(cfg, x0).records(cfg, obj)
+        except Exception as exc:  # surfaced on the caller's thread below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=lane, args=(k,)) for k in range(S)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return out  # type: ignore[return-value]

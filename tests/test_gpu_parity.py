@@ -519,3 +519,21 @@ def test_config1_allegro_end_to_end_statistics(G, O, engine, shape):
     n = ok.sum()
     assert abs(eg["success"].mean() - ec["success"].mean()) <= 3.0 / np.sqrt(n) + 0.05
     assert abs(np.median(eg["pd_mm"]) - np.median(ec["pd_mm"])) <= 0.25 * np.median(ec["pd_mm"]) + 0.5
+
+
+def test_synthesize_objects_equals_per_object_runs(G, trident, engine):
+    """Multi-object synthesis on concurrent engine contexts (config 3 path) returns, per
+    object, exactly the records of a plain per-object synthesize."""
+    import dataclasses
+    objs = [G.make_primitive(n, 0.09) for n in ("sphere", "box", "cylinder")]
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 8, 3
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 30, 10, 10
+    cfgs = [dataclasses.replace(cfg, seed=i) for i in range(len(objs))]
+    many = G.synthesize_objects(trident, objs, cfgs, streams=3)
+    for obj, c, recs in zip(objs, cfgs, many):
+        one = G.synthesize(trident, obj, c)
+        assert len(one) == len(recs)
+        for a, b in zip(one, recs):
+            assert np.array_equal(a.x, b.x) and np.array_equal(a.x_s, b.x_s)
+            assert a.energy_total == b.energy_total or (np.isnan(a.energy_total) and np.isnan(b.energy_total))
