@@ -144,7 +144,7 @@ struct grasp_ctx {
     return 0;
   }();
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
-  DevBuf<unsigned char> pair_need;
+  DevBuf<unsigned char> pair_need, pair_hist;
   long long list_grid = 148 * 4;  // persistent k_pairs_list blocks
   long long epa_grid = 148 * 4;   // grid-stride k_pairs_epa_warp blocks
   bool epa_thread = [] {  // the warp-per-job EPA measured slower (lane-0 polytope updates)
@@ -599,8 +599,11 @@ struct grasp_ctx {
     st.pair_count = pair_count.p;
     st.pair_list = pair_list.p;
     pair_need.ensure(g * NP);
-    seg_count.ensure(NP);
-    seg_offset.ensure(NP);
+    pair_hist.ensure(g * NP);
+    ck(cudaMemsetAsync(pair_hist.p, 0, g * NP, stream), "memset");
+    st.pair_hist = pair_hist.p;
+    seg_count.ensure(NP * kPairBuckets);
+    seg_offset.ensure(NP * kPairBuckets);
     st.pair_need = pair_need.p;
     st.seg_count = seg_count.p;
     st.seg_offset = seg_offset.p;
@@ -706,9 +709,9 @@ struct grasp_ctx {
         k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
       } else {
         ck(cudaMemsetAsync(pair_count.p, 0, 3 * sizeof(int), stream), "memset");
-        ck(cudaMemsetAsync(seg_count.p, 0, sizeof(int) * nl * O.P, stream), "memset");
+        ck(cudaMemsetAsync(seg_count.p, 0, sizeof(int) * nl * O.P * kPairBuckets, stream), "memset");
         k_pairs_cull<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
-        k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.P);
+        k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.P * kPairBuckets);
         k_pairs_scatter<<<blocks(n, 128), 128, 0, stream>>>(st, lk, nl, O.P);
         if (pairs_variant == 3)
           k_pairs_list_il<<<std::min<long long>(blocks(n, 128), list_grid), 128, 0, stream>>>(H, O, st);

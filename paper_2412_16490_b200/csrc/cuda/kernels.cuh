@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(128) k_pairs_cull(DevHand H, DevObject O, DevS
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long n = (long long)st.G * n_links * O.P;
   bool need = false;
-  int lp = 0;
+  int lp = 0, b = 0;
   if (t < n) {
     const int g = (int)(t % st.G);
     lp = (int)(t / st.G);
@@ -683,11 +683,13 @@ __global__ void __launch_bounds__(128) k_pairs_cull(DevHand H, DevObject O, DevS
         double* o = st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12;
         o[0] = INFINITY;
         o[10] = kPairCulled;
+      } else {
+        b = pair_bucket(st.pair_hist[(size_t)g * st.NP + link * O.P + part]);
       }
     }
-    st.pair_need[t] = need;
+    st.pair_need[t] = need ? (unsigned char)(1 + b) : 0;
   }
-  warp_segment_add(st.seg_count, lp, need);
+  warp_segment_add(st.seg_count, lp * kPairBuckets + b, need);
 }
 
 // Pass 1b: exclusive scan of the segment counts (one block); seg_count turns
@@ -722,9 +724,10 @@ __global__ void __launch_bounds__(128) k_pairs_scatter(DevState st, const int* _
                                                        int P) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long n = (long long)st.G * n_links * P;
-  const bool need = t < n && st.pair_need[t];
+  const int code = t < n ? st.pair_need[t] : 0;
+  const bool need = code != 0;
   const int lp = t < n ? (int)(t / st.G) : 0;
-  const int pos = warp_segment_add(st.seg_count, lp, need);
+  const int pos = warp_segment_add(st.seg_count, lp * kPairBuckets + (need ? code - 1 : 0), need);
   if (need) {
     const int g = (int)(t % st.G);
     const int link = links ? links[lp / P] : lp / P;
@@ -945,6 +948,7 @@ __global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHa
   SP simp[4];
   int ns;
   const bool overlap = gjk_phase(A, B, scale, r, simp, ns);
+  st.pair_hist[slot] = (unsigned char)min(255u, r.gjk_iters + 1);
   if (st.ops) {
     atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * (A.nv + B.nv));
     count_gjk(st.ops, r.gjk_iters + 1, r.gjk_skipped);

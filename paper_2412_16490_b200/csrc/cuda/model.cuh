@@ -144,7 +144,8 @@ struct DevState {
   int big_slots;
   int* pair_count;     // compacted list of pair slots that need GJK
   int* pair_list;      // [G*NP]
-  unsigned char* pair_need;  // [G*NP-slot order of the launch] 1 when the pair needs GJK
+  unsigned char* pair_need;  // [G*NP-slot order of the launch] 0, or 1 + bucket when the pair needs GJK
+  unsigned char* pair_hist;  // [G*NP] GJK closest-point calls of the slot's last evaluation (bucketing)
   int* seg_count;      // [NP] needed pairs per (link, part) segment, then the fill cursor
   int* seg_offset;     // [NP] exclusive scan of seg_count
   int* epa_count;      // overlapping pairs handed from GJK to the EPA kernel
@@ -153,6 +154,11 @@ struct DevState {
 };
 
 constexpr int kEpaJobStride = 40;
+// The GJK list is segmented by (link, part) and, inside a segment, by the
+// slot's previous GJK length (kPairBuckets buckets), so a warp's pairs tend
+// to need the same number of iterations.
+constexpr int kPairBuckets = 4;
+__host__ __device__ inline int pair_bucket(int calls) { return calls <= 4 ? 0 : calls <= 7 ? 1 : calls <= 12 ? 2 : 3; }
 
 // Op counters (profiling mode) for the roofline's algorithmic flop count
 // (SURVEY.md 8(d) constants are applied on the host).
