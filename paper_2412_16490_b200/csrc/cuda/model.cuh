@@ -157,8 +157,8 @@ constexpr int kEpaJobStride = 40;
 // The GJK list is segmented by (link, part) and, inside a segment, by the
 // slot's previous GJK length (kPairBuckets buckets), so a warp's pairs tend
 // to need the same number of iterations.
-constexpr int kPairBuckets = 4;
-__host__ __device__ inline int pair_bucket(int calls) { return calls <= 4 ? 0 : calls <= 7 ? 1 : calls <= 12 ? 2 : 3; }
+constexpr int kPairBuckets = 16;
+__host__ __device__ inline int pair_bucket(int calls) { return calls < 1 ? 0 : (calls > 16 ? 15 : calls - 1); }
 
 // Op counters (profiling mode) for the roofline's algorithmic flop count
 // (SURVEY.md 8(d) constants are applied on the host).
