@@ -718,7 +718,7 @@ struct grasp_ctx {
         else
           k_pairs_list<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
         if (epa_thread)
-          k_pairs_epa<<<blocks(std::min<long long>(n, st.epa_cap), 128), 128, 0, stream>>>(H, O, st);
+          k_pairs_epa<<<blocks(std::min<long long>(n, st.epa_cap), 32), 32, 0, stream>>>(H, O, st);
         else
           k_pairs_epa_warp<<<std::min<long long>(blocks(std::min<long long>(n, st.epa_cap), 4), epa_grid), 128, 0,
                              stream>>>(H, O, st);
