@@ -107,14 +107,8 @@ GDEV_FN D3 row(const M33& a, int r) { return {a.m[3 * r], a.m[3 * r + 1], a.m[3 
 GDEV_FN void set_col(M33& a, int c, D3 v) { a.m[c] = v.x; a.m[3 + c] = v.y; a.m[6 + c] = v.z; }
 
 // Eigen::AngleAxisd::toRotationMatrix expression order (hand.cpp:144).
-GDEV_FN M33 angle_axis(double angle, D3 axis) {
-  double s, c;
-#if defined(__CUDA_ARCH__)
-  cr_sincos(angle, &s, &c);  // correctly rounded: matches glibc except near midpoints (crmath.cuh)
-#else
-  s = ::sin(angle);
-  c = ::cos(angle);
-#endif
+// AngleAxis(angle, axis).toRotationMatrix() from a precomputed sin/cos.
+GDEV_FN M33 angle_axis_sc(double s, double c, D3 axis) {
   const D3 sa = s * axis;
   const D3 ka = (1.0 - c) * axis;
   M33 r;
@@ -131,6 +125,17 @@ GDEV_FN M33 angle_axis(double angle, D3 axis) {
   r.m[4] = ka.y * axis.y + c;
   r.m[8] = ka.z * axis.z + c;
   return r;
+}
+
+GDEV_FN M33 angle_axis(double angle, D3 axis) {
+  double s, c;
+#if defined(__CUDA_ARCH__)
+  cr_sincos(angle, &s, &c);  // correctly rounded: matches glibc except near midpoints (crmath.cuh)
+#else
+  s = ::sin(angle);
+  c = ::cos(angle);
+#endif
+  return angle_axis_sc(s, c, axis);
 }
 
 // Nearest proper rotation to a raw 3x3 block (hand.cpp:45-73): polar factor

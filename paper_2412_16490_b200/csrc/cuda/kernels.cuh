@@ -88,6 +88,7 @@ struct WarpScratch {
   double world[kMaxLinks * 12];
   double jo[kMaxDof * 6];
   double pc[kMaxProxies * 3];
+  double sn[kMaxDof], cs[kMaxDof];  // sin/cos of the joint angles (one correctly rounded pair per joint)
   double itF[32 * 3];
   double itT[32 * 3];
   int itL[32];
@@ -105,6 +106,7 @@ __device__ inline void warp_fk(const DevHand& H, const DevState& st, int g, int 
     const Pose ps = compute_pose(s.x);
     store_pose(s.pose, ps);
   }
+  for (int j = lane; j < H.dof; j += 32) cr_sincos(s.x[12 + j], s.sn + j, s.cs + j);
   __syncwarp();
   const Pose base = load_pose(s.pose);
   if (lane < H.L) {
@@ -118,7 +120,7 @@ __device__ inline void warp_fk(const DevHand& H, const DevState& st, int g, int 
       if (j < 0) continue;  // base link: identity chain
       const D3 origin = ld3(H.joint_origin + 3 * j);
       const D3 axis = ld3(H.joint_axis + 3 * j);
-      const M33 Rs = angle_axis(s.x[12 + j], axis);
+      const M33 Rs = angle_axis_sc(s.sn[j], s.cs[j], axis);
       const D3 jo = mul(Rc, origin) + tc;  // parent.apply(origin)
       const M33 Rn = mul(Rc, Rs);
       if (p == l) {
