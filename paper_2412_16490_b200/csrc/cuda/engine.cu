@@ -86,6 +86,8 @@ struct grasp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool has_hand = false, has_object = false;
+  DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
+  DevBuf<unsigned char> pair_need, pair_hist;
 
   // hand
   DevHand H{};
@@ -135,23 +137,7 @@ struct grasp_ctx {
   DevBuf<int> qp_iters, qp_conv, qp_ready, failed, have_pregrasp, err, ovf_count, ovf_list, qface;
   DevBuf<EpaScratchBig> big_scratch;
   static constexpr int kBigSlots = 1024;
-  // Pair kernel variant (GRASP_PAIRS=list|warp|thread, default list).
-  int pairs_variant = [] {
-    const char* v = std::getenv("GRASP_PAIRS");
-    if (v && std::string(v) == "warp") return 1;
-    if (v && std::string(v) == "thread") return 2;
-    if (v && std::string(v) == "interleaved") return 3;
-    return 0;
-  }();
-  DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
-  DevBuf<unsigned char> pair_need, pair_hist;
-  long long list_grid = 148 * 4;  // persistent k_pairs_list blocks
-  long long epa_grid = 148 * 4;   // grid-stride k_pairs_epa_warp blocks
-  bool epa_thread = [] {  // the warp-per-job EPA measured slower (lane-0 polytope updates)
-    const char* v = std::getenv("GRASP_EPA");
-    return !(v && std::string(v) == "warp");
-  }();
-  DevBuf<double> epa_jobs;
+  DevBuf<double> epa_jobs;  // EPA jobs handed from k_pairs_list to k_pairs_epa
 
   // Instrumentation: launch counts always; per-class CUDA-event time and
   // algorithmic op counters only while profiling.
@@ -703,26 +689,14 @@ struct grasp_ctx {
     launch(3, [&] {
       ck(cudaMemsetAsync(ovf_count.p, 0, sizeof(int), stream), "memset");
       const int* lk = tips_only ? h_tip_links_sorted.p : nullptr;
-      if (pairs_variant == 1) {
-        k_pairs_warp<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
-      } else if (pairs_variant == 2) {
-        k_pairs<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
-      } else {
-        ck(cudaMemsetAsync(pair_count.p, 0, 3 * sizeof(int), stream), "memset");
-        ck(cudaMemsetAsync(seg_count.p, 0, sizeof(int) * nl * O.P * kPairBuckets, stream), "memset");
-        k_pairs_cull<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
-        k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.P * kPairBuckets);
-        k_pairs_scatter<<<blocks(n, 128), 128, 0, stream>>>(st, lk, nl, O.P);
-        if (pairs_variant == 3)
-          k_pairs_list_il<<<std::min<long long>(blocks(n, 128), list_grid), 128, 0, stream>>>(H, O, st);
-        else
-          k_pairs_list<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
-        if (epa_thread)
-          k_pairs_epa<<<blocks(std::min<long long>(n, st.epa_cap), 32), 32, 0, stream>>>(H, O, st);
-        else
-          k_pairs_epa_warp<<<std::min<long long>(blocks(std::min<long long>(n, st.epa_cap), 4), epa_grid), 128, 0,
-                             stream>>>(H, O, st);
-      }
+      ck(cudaMemsetAsync(pair_count.p, 0, 3 * sizeof(int), stream), "memset");
+      ck(cudaMemsetAsync(seg_count.p, 0, sizeof(int) * nl * O.P * kPairBuckets, stream), "memset");
+      k_pairs_cull<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
+      k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.P * kPairBuckets);
+      k_pairs_scatter<<<blocks(n, 128), 128, 0, stream>>>(st, lk, nl, O.P);
+      k_pairs_list<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
+      // EPA jobs spread over all SMs (32-thread blocks; few jobs per launch)
+      k_pairs_epa<<<blocks(std::min<long long>(n, st.epa_cap), 32), 32, 0, stream>>>(H, O, st);
     });
     launch(7, [&] { k_pairs_big<<<kBigSlots / 128, 128, 0, stream>>>(H, O, st); });
   }
@@ -913,13 +887,6 @@ int grasp_ctx_create(int device, grasp_ctx** out) {
       ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
       // Large per-thread stacks for the EPA scratch of k_pairs.
       ck(cudaDeviceSetLimit(cudaLimitStackSize, 32 * 1024), "stack limit");
-      // Persistent GJK grid: every resident block slot on every SM.
-      int sms = 0, per_sm = 0;
-      ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
-      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gdev::k_pairs_list_il, 128, 0), "occupancy");
-      ctx->list_grid = static_cast<long long>(sms) * std::max(per_sm, 1);
-      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gdev::k_pairs_epa_warp, 128, 0), "occupancy");
-      ctx->epa_grid = static_cast<long long>(sms) * std::max(per_sm, 1);
     } catch (...) {
       delete ctx;
       throw;

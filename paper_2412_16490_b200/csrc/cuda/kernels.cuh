@@ -12,7 +12,6 @@
 
 #include "dmath.cuh"
 #include "gjk.cuh"
-#include "gjk_warp.cuh"
 #include "model.cuh"
 
 namespace gdev {
@@ -602,47 +601,6 @@ __device__ __forceinline__ bool pair_needed(const DevHand& H, const DevObject& O
   return !(H.link_box && boxes_separated(H.link_box + 15 * link, Rw, tw, O.part_box + 15 * part, kCullSlack));
 }
 
-// One thread per (grasp, link, part); consecutive threads share (link, part)
-// so the support scans read the same vertices across the warp.
-__global__ void __launch_bounds__(128) k_pairs(DevHand H, DevObject O, DevState st, const int* __restrict__ links,
-                                               int n_links) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)st.G * n_links * O.P) return;
-  const int g = (int)(t % st.G);
-  const int lp = (int)(t / st.G);
-  const int link = links ? links[lp / O.P] : lp / O.P;
-  const int part = lp % O.P;
-  if (st.failed[g]) return;
-  const double* w = st.world + ((size_t)g * H.L + link) * 12;
-  M33 Rw;
-  for (int i = 0; i < 9; ++i) Rw.m[i] = w[i];
-  double* o = st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12;
-  if (!pair_needed(H, O, st, g, link, part, Rw, ld3(w + 9))) {
-    o[0] = INFINITY;
-    o[10] = kPairCulled;
-    return;
-  }
-  EpaScratch scratch;
-  const PairResult r = link_part_distance(H, O, link, part, Rw, ld3(w + 9), scratch);
-  store_pair(o, r);
-  if (st.ops) {
-    const unsigned nv = (H.link_vbeg[link + 1] - H.link_vbeg[link]) + (O.part_vbeg[part + 1] - O.part_vbeg[part]);
-    atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * nv);
-    count_gjk(st.ops, r.gjk_iters + 1, r.gjk_skipped);
-    atomicAdd(st.ops + kOpEpaIters, (unsigned long long)r.epa_iters);
-    atomicAdd(st.ops + kOpPairsNeeded, 1ull);
-    if (r.flags & kPairOverflow) atomicAdd(st.ops + kOpEpaOverflow, 1ull);
-  }
-  if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
-  if (r.flags & kPairOverflow) {
-    // Outgrew the per-thread polytope: queue for k_pairs_big.
-    const int slot = atomicAdd(st.ovf_count, 1);
-    if (slot < st.ovf_cap)
-      st.ovf_list[slot] = (int)((size_t)g * st.NP + link * O.P + part);
-    else
-      atomicAdd(st.err + 1, 1);
-  }
-}
 
 // Compacted pair evaluation. The list is segmented by (link, part) so that a
 // GJK warp works on one hull pair: its vertex loads are warp-uniform
@@ -813,130 +771,6 @@ __device__ __forceinline__ void store_separated(double* o, const Simplex& sx, co
   o[10] = 0;
 }
 
-// Pass 2 variant (GRASP_PAIRS=interleaved): GJK over the pair list,
-// persistent and iteration-interleaved. A
-// lane owns one pair at a time and runs one GJK iteration (geometry.cpp:
-// 105-164) per trip of the warp loop; a lane whose pair finished takes the
-// next list entry at the top of the following trip. Lanes therefore stay
-// busy regardless of how many iterations their pairs need (the per-pair
-// iteration counts are heavy-tailed), all lanes share one support_pair call
-// per trip, and closest_on_simplex_var keeps mixed simplex sizes converged.
-// Results are those of gjk_phase: the same operations run per pair, only
-// interleaved with other pairs. Overlapping pairs pass their terminal
-// simplex to k_pairs_epa.
-__global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list_il(DevHand H, DevObject O, DevState st) {
-  const int lane = threadIdx.x & 31;
-  const int total = *(volatile int*)st.pair_count;
-  int* cursor = st.pair_count + 2;
-  int slot = -1, ns = 0, iter = 0;
-  bool fresh = false, exhausted = false;
-  unsigned nsup = 0, skipped = 0;
-  SP simp[4];
-  unsigned key[4];
-  GjkCycle cyc;
-  double scale = 1.0;
-  Hull A, B;
-  Simplex sx;
-  auto finish_stats = [&]() {
-    if (st.ops) {
-      atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)nsup * (A.nv + B.nv));
-      count_gjk(st.ops, iter + 1 - skipped, skipped);
-      atomicAdd(st.ops + kOpPairsNeeded, 1ull);
-    }
-  };
-  while (true) {
-    D3 dir = mk(1, 0, 0);
-    if (slot >= 0) {
-      const int jump = cycle_step(cyc, key, ns, iter);
-      iter += jump;
-      skipped += jump;
-      // closest point, reduce, overlap test (geometry.cpp:112-120)
-      sx = closest_on_simplex(simp, ns);
-      if (iter >= kGjkMaxIters) {
-        // iteration cap: estimate from the unreduced simplex (geometry.cpp:136-149)
-        finish_stats();
-        store_separated(st.pairs + (size_t)slot * 12, sx, simp, false);
-        slot = -1;
-      }
-    }
-    if (slot >= 0) {
-      SP red[4];
-      unsigned rkey[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int src = sx.keep[i];
-        red[i] = simp[0];
-        rkey[i] = key[0];
-        if (src == 1) red[i] = simp[1], rkey[i] = key[1];
-        if (src == 2) red[i] = simp[2], rkey[i] = key[2];
-        if (src == 3) red[i] = simp[3], rkey[i] = key[3];
-      }
-      ns = sx.nkeep;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) simp[i] = red[i], key[i] = rkey[i];
-      if (sx.contains || sqrt(sx.dist2) < kTouchTol * scale) {
-        finish_stats();
-        write_epa_job(st, slot, simp, ns);
-        slot = -1;
-      } else {
-        dir = -sx.v;
-      }
-    }
-    // refill idle lanes from the list
-    const unsigned want = __ballot_sync(kFull, slot < 0 && !exhausted);
-    if (want) {
-      const int leader = __ffs(want) - 1;
-      int base = 0;
-      if (lane == leader) base = atomicAdd(cursor, __popc(want));
-      base = __shfl_sync(kFull, base, leader);
-      if (slot < 0 && !exhausted) {
-        const int i = base + __popc(want & ((1u << lane) - 1));
-        if (i < total) {
-          slot = st.pair_list[i];
-          slot_hulls(H, O, st, slot, A, B, scale);
-          fresh = true;
-          dir = mk(1, 0, 0);
-        } else {
-          exhausted = true;
-        }
-      }
-    }
-    if (!__any_sync(kFull, slot >= 0)) break;
-    if (slot < 0) continue;
-    unsigned wkey;
-    const SP w = support_pair(A, B, dir, wkey);
-    if (fresh) {
-      simp[0] = simp[1] = simp[2] = simp[3] = w;
-      key[0] = key[1] = key[2] = key[3] = wkey;
-      ns = 1;
-      iter = 0;
-      nsup = 1;
-      skipped = 0;
-      cycle_init(cyc, A.nv, B.nv);
-      fresh = false;
-      continue;
-    }
-    ++nsup;
-    ++iter;
-    // termination tests, then grow the simplex (geometry.cpp:122-135)
-    const double gap = sx.dist2 - dot(sx.v, w.w);
-    bool repeat = false;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i < ns && nrm(simp[i].w - w.w) < 1e-14 * scale) repeat = true;
-    const bool done = gap <= kGjkRelTol * sx.dist2 + 1e-300 || repeat || ns == 4;
-    if (done) {
-      finish_stats();
-      store_separated(st.pairs + (size_t)slot * 12, sx, simp, true);
-      slot = -1;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i == ns) simp[i] = w, key[i] = wkey;
-      ++ns;
-    }
-  }
-}
 
 // Pass 2 (default): GJK, one thread per listed pair from start to end.
 __global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHand H, DevObject O, DevState st) {
@@ -976,55 +810,8 @@ __global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHa
   }
 }
 
-// Pass 3: EPA for the overlapping pairs (geometry.cpp:227-324).
-// Pass 3 variant (GRASP_EPA=warp; measured slower than the per-thread
-// kernel): EPA for the overlapping pairs, one warp per job
-// (warp_epa: support scans split over the lanes, polytope in shared memory,
-// its order-dependent updates on lane 0 - same faces, order and tie rules
-// as the per-thread epa(); geometry.cpp:168-205, 227-324). Grid-stride over
-// the job list so the grid can be sized without reading the job count.
-__global__ void __launch_bounds__(128) k_pairs_epa_warp(DevHand H, DevObject O, DevState st) {
-  __shared__ WarpEpa epa_smem[4];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int njobs = min(*(volatile int*)st.epa_count, st.epa_cap);
-  for (int i = blockIdx.x * 4 + warp; i < njobs; i += gridDim.x * 4) {
-    const double* jb = st.epa_jobs + (size_t)i * kEpaJobStride;
-    const int slot = (int)jb[0], ns = (int)jb[1];
-    SP simp[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      simp[k].w = ld3(jb + 2 + 9 * k);
-      simp[k].a = ld3(jb + 5 + 9 * k);
-      simp[k].b = ld3(jb + 8 + 9 * k);
-    }
-    Hull A, B;
-    double scale;
-    slot_hulls(H, O, st, slot, A, B, scale);
-    PairResult r;
-    r.flags = 0;
-    r.n_support = 0;
-    r.gjk_iters = 0;
-    r.epa_iters = 0;
-    r.gjk_skipped = 0;
-    warp_epa(simp, ns, A, B, scale, epa_smem[warp], lane, r);
-    if (lane == 0) {
-      if (st.ops) {
-        atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * (A.nv + B.nv));
-        atomicAdd(st.ops + kOpEpaIters, (unsigned long long)r.epa_iters);
-        if (r.flags & kPairOverflow) atomicAdd(st.ops + kOpEpaOverflow, 1ull);
-      }
-      if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
-      if (r.flags & kPairOverflow)
-        queue_overflow(st, slot);
-      else
-        store_pair(st.pairs + (size_t)slot * 12, r);
-    }
-    __syncwarp();
-  }
-}
-
-// Pass 3 (default): EPA for the overlapping pairs, one thread per job,
-// polytope in local memory.
+// Pass 3: EPA for the overlapping pairs (geometry.cpp:168-205, 227-324), one
+// thread per job, polytope in local memory.
 __global__ void __launch_bounds__(128) k_pairs_epa(DevHand H, DevObject O, DevState st) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= min(*st.epa_count, st.epa_cap)) return;
@@ -1060,80 +847,6 @@ __global__ void __launch_bounds__(128) k_pairs_epa(DevHand H, DevObject O, DevSt
   store_pair(st.pairs + (size_t)slot * 12, r);
 }
 
-// Warp-cooperative variant: each warp takes 32 consecutive pair slots, every
-// lane runs the cull test for its slot, then the whole warp evaluates the
-// needed pairs one after another (gjk_warp.cuh).
-__global__ void __launch_bounds__(128) k_pairs_warp(DevHand H, DevObject O, DevState st,
-                                                    const int* __restrict__ links, int n_links) {
-  __shared__ WarpEpa epa_smem[4];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long total = (long long)st.G * n_links * O.P;
-  const long long base = ((long long)blockIdx.x * 4 + warp) * 32;
-  if (base >= total) return;
-  const long long t = base + lane;
-  bool need = false;
-  if (t < total) {
-    const int g = (int)(t % st.G);
-    const int lp = (int)(t / st.G);
-    const int link = links ? links[lp / O.P] : lp / O.P;
-    const int part = lp % O.P;
-    if (!st.failed[g]) {
-      const double* w = st.world + ((size_t)g * H.L + link) * 12;
-      M33 Rw;
-      for (int i = 0; i < 9; ++i) Rw.m[i] = w[i];
-      need = pair_needed(H, O, st, g, link, part, Rw, ld3(w + 9));
-      if (!need) {
-        double* o = st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12;
-        o[0] = INFINITY;
-        o[10] = kPairCulled;
-      }
-    }
-  }
-  unsigned mask = __ballot_sync(kFull, need);
-  while (mask) {
-    const int src = __ffs(mask) - 1;
-    mask &= mask - 1;
-    const long long ts = base + src;
-    const int g = (int)(ts % st.G);
-    const int lp = (int)(ts / st.G);
-    const int link = links ? links[lp / O.P] : lp / O.P;
-    const int part = lp % O.P;
-    const double* w = st.world + ((size_t)g * H.L + link) * 12;
-    Hull A;
-    A.verts = H.link_verts + 3 * (size_t)H.link_vbeg[link];
-    A.nv = H.link_vbeg[link + 1] - H.link_vbeg[link];
-    A.posed = true;
-    for (int i = 0; i < 9; ++i) A.R.m[i] = w[i];
-    A.t = ld3(w + 9);
-    Hull B;
-    B.verts = O.verts + 3 * (size_t)O.part_vbeg[part];
-    B.nv = O.part_vbeg[part + 1] - O.part_vbeg[part];
-    B.posed = false;
-    B.R = eye();
-    B.t = mk(0, 0, 0);
-    double scale = 1.0;
-    scale = fmax(scale, scale_of(mul(A.R, ld3(H.link_centroid + 3 * link)) + A.t, H.link_halfnorm[link]));
-    scale = fmax(scale, scale_of(ld3(O.part_centroid + 3 * part), O.part_halfnorm[part]));
-    const PairResult r = warp_signed_distance(A, B, scale, epa_smem[warp], lane);
-    if (lane == 0) {
-      store_pair(st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12, r);
-      if (st.ops) {
-        atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * (A.nv + B.nv));
-        count_gjk(st.ops, r.gjk_iters + 1, r.gjk_skipped);
-        atomicAdd(st.ops + kOpEpaIters, (unsigned long long)r.epa_iters);
-      }
-      if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
-      if (r.flags & kPairOverflow) {
-        const int slot = atomicAdd(st.ovf_count, 1);
-        if (slot < st.ovf_cap)
-          st.ovf_list[slot] = (int)((size_t)g * st.NP + link * O.P + part);
-        else
-          atomicAdd(st.err + 1, 1);
-      }
-    }
-    __syncwarp();
-  }
-}
 
 // Redoes the queued pairs with the large global-memory EPA buffer.
 __global__ void __launch_bounds__(128) k_pairs_big(DevHand H, DevObject O, DevState st) {
