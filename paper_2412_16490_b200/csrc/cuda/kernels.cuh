@@ -424,7 +424,10 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int warm_face
 }
 
 // One thread per (grasp, query slot). slots == nullptr: all NQ slots.
-__global__ void k_point_query(DevObject O, DevState st, const int* __restrict__ slots, int n_slots) {
+// 6 blocks/SM (80 registers, small spills) measured best: the divergent, latency-bound
+// query loop needs the extra resident warps.
+__global__ void __launch_bounds__(128, 6) k_point_query(DevObject O, DevState st, const int* __restrict__ slots,
+                                                        int n_slots) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int per = slots ? n_slots : st.NQ;
   if (t >= (long long)st.G * per) return;
