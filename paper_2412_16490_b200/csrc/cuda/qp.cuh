@@ -24,15 +24,39 @@ namespace gdev {
 constexpr unsigned kFull = 0xffffffffu;
 #endif
 
-// Fixed-order sum over lanes base..base+cnt-1 (identical on all lanes).
+// Pairwise sum of N register values (short dependency chains: the sweep is
+// bound by fp64 latency at ~4 warps per scheduler, not by the fp64 pipe).
+template <int N>
+__device__ __forceinline__ double tree_sum(const double* v) {
+  if constexpr (N == 1) {
+    return v[0];
+  } else {
+    return tree_sum<N / 2>(v) + tree_sum<N - N / 2>(v + N / 2);
+  }
+}
+
+// max(v, 0) by clearing negative values' bits (ALU pipe, not the fp64 pipe).
+__device__ __forceinline__ double relu_bits(double v) {
+  const long long b = __double_as_longlong(v);
+  return __longlong_as_double(b & ~(b >> 63));
+}
+
+// Fixed-order sum over lanes base..base+cnt-1 (identical on all lanes): all
+// shuffles first, then a pairwise tree when the count is known.
 template <int CNT>
 __device__ __forceinline__ double qp_group_sum(double v, int base, int cnt) {
-  double s = 0.0;
-  const int n = CNT > 0 ? CNT : cnt;
+  if constexpr (CNT > 0) {
+    double t[CNT];
 #pragma unroll
-  for (int b = 0; b < (CNT > 0 ? CNT : kMaxTips); ++b)
-    if (b < n) s += __shfl_sync(kFull, v, base + b);
-  return s;
+    for (int b = 0; b < CNT; ++b) t[b] = __shfl_sync(kFull, v, base + b);
+    return tree_sum<CNT>(t);
+  } else {
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < kMaxTips; ++b)
+      if (b < cnt) s += __shfl_sync(kFull, v, base + b);
+    return s;
+  }
 }
 template <int CNT>
 __device__ __forceinline__ double qp_group_max(double v, int base, int cnt) {
@@ -214,8 +238,11 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     t = cross(fp, f);
   };
 
-  double x[KMAX], zid[KMAX], yid[KMAX], q[KMAX];
-  double zc, yc, ztot, ytot;
+  // Scaled duals u = y / rho (ADMM scaled form): the projection step costs
+  // two adds per row; y = rho u is formed only for the residual check and
+  // the snapshot. nq = -q.
+  double x[KMAX], zid[KMAX], uid[KMAX], nq[KMAX];
+  double zc, uc, ztot, utot;
   const bool warm = (mode == 0 || mode == 2) && st.qp_ready[g];
   const double* wx = st.warm_x + (size_t)g * n * 6;
   const double* wy = st.warm_y + (size_t)g * M * 6;
@@ -224,24 +251,22 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     if (e < k) {
       const int i = c * k + e;
       x[e] = warm ? wx[j * n + i] : 0.0;
-      yid[e] = warm ? wy[j * M + m + 1 + i] : 0.0;
-      q[e] = (-2.0 * P.beta) * (tsign * s.W[axis * wn + c * ws + e]);
+      uid[e] = warm ? wy[j * M + m + 1 + i] * inv_rho : 0.0;
+      nq[e] = (2.0 * P.beta) * (tsign * s.W[axis * wn + c * ws + e]);
     } else {
-      x[e] = yid[e] = q[e] = 0.0;
+      x[e] = uid[e] = nq[e] = 0.0;
     }
     zid[e] = x[e];
   }
-  yc = warm ? wy[j * M + c] : 0.0;
-  ytot = warm ? wy[j * M + m] : 0.0;
+  uc = warm ? wy[j * M + c] * inv_rho : 0.0;
+  utot = warm ? wy[j * M + m] * inv_rho : 0.0;
   {
-    double bs = 0.0;
-#pragma unroll
-    for (int e = 0; e < KMAX; ++e)
-      if (e < k) bs += x[e];
+    const double bs = tree_sum<KMAX>(x);
     zc = bs;
     ztot = qp_group_sum<MT>(bs, base, m);
   }
   const double gamma = P.gamma_total;
+  const double oma = 1.0 - alpha, a_inv_a = alpha * inv_a;
   bool frozen = !active;
   double* ox = st.warm_x + (size_t)g * n * 6;
   double* oy = st.warm_y + (size_t)g * M * 6;
@@ -250,33 +275,28 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
   int sweeps = 0;
   for (int iter = 1; iter <= P.max_iters; ++iter) {
     sweeps = iter;
-    // rhs = A'(rho z - y) + sigma x - q ; r' = B^-1 rhs
-    const double vc = rho * zc - yc, vt = rho * ztot - ytot;
-    double rp[KMAX];
-    double bsum = 0.0;
+    // rhs = A'(rho z - y) + sigma x - q = rq + vct (vct: the cap and total
+    // rows, common to the lane's edges) ; r' = B^-1 rhs
+    const double vct = rho * ((zc - uc) + (ztot - utot));
+    double rq[KMAX];
 #pragma unroll
-    for (int e = 0; e < KMAX; ++e) {
-      if (e < k) {
-        const double vi = rho * zid[e] - yid[e];
-        rp[e] = ((vc + vt) + vi) + (sigma * x[e] - q[e]);
-        bsum += rp[e];
-      } else {
-        rp[e] = 0.0;
-      }
-    }
-    // r' = B^-1 rhs = (rhs - betap sum rhs) / a is never formed: its sums
-    // over the edges follow from those of rhs, and xt below folds 1/a in.
+    for (int e = 0; e < KMAX; ++e) rq[e] = e < k ? rho * (zid[e] - uid[e]) + (sigma * x[e] + nq[e]) : 0.0;
+    const double bsum = tree_sum<KMAX>(rq) + k * vct;
     const double bb = betap * bsum;
     double tv[7];
     {
-      double s1r = 0.0, s2r = 0.0;
+      // two interleaved accumulators per sum (padded rq entries are zero)
+      double s1a = 0.0, s1b = 0.0, s2a = 0.0, s2b = 0.0;
 #pragma unroll
-      for (int e = 0; e < KMAX; ++e) {
-        if (e < k) {
-          s1r += P.cos_t[e] * rp[e];
-          s2r += P.sin_t[e] * rp[e];
+      for (int e = 0; e < KMAX; e += 2) {
+        s1a += P.cos_t[e] * rq[e];
+        s2a += P.sin_t[e] * rq[e];
+        if (e + 1 < KMAX) {
+          s1b += P.cos_t[e + 1] * rq[e + 1];
+          s2b += P.sin_t[e + 1] * rq[e + 1];
         }
       }
+      const double s1r = (s1a + s1b) + ccos * vct, s2r = (s2a + s2b) + csin * vct;
       const double s0 = (bsum - k * bb) * inv_a;
       const double s1 = (s1r - ccos * bb) * inv_a, s2 = (s2r - csin * bb) * inv_a;
       const D3 f = s0 * fn + mu * (s1 * fd + s2 * fe);
@@ -296,12 +316,15 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
 #pragma unroll
       for (int i = 0; i < RPL; ++i) {
         const int r = c + i * MT;
-        double acc = 0.0;
+        double a0 = 0.0, a1 = 0.0;
         if (r < 7) {
 #pragma unroll
-          for (int p = 0; p < 7; ++p) acc += s.Cinv[r * 7 + p] * tv[p];
+          for (int p = 0; p < 7; p += 2) {
+            a0 += s.Cinv[r * 7 + p] * tv[p];
+            if (p + 1 < 7) a1 += s.Cinv[r * 7 + p + 1] * tv[p + 1];
+          }
         }
-        mine[i] = acc;
+        mine[i] = a0 + a1;
       }
 #pragma unroll
       for (int r = 0; r < 7; ++r) sv[r] = __shfl_sync(kFull, mine[r / MT], base + r % MT);
@@ -316,45 +339,41 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     }
     const D3 wv = mk(sv[0], sv[1], sv[2]) + cross(mk(sv[3], sv[4], sv[5]), fp);
     const double nw = dot(fn, wv), dw = dot(fd, wv), ew = dot(fe, wv);
-    // (U s)_e = ua + ub cos_e + uc sin_e, so (G s)_e = (U s - betap sum U s)_e / a
+    // (U s)_e = ua + ub cos_e + ue sin_e, so (G s)_e = (U s - betap sum U s)_e / a
     // is ga + gb cos_e + gc sin_e.
-    const double ua = sqrt2 * nw + sqrt_rho * sv[6], ub = sqrt2 * mu * dw, uc = sqrt2 * mu * ew;
-    const double us_sum = k * ua + ccos * ub + csin * uc;
-    const double ga = (ua - betap * us_sum) * inv_a, gb = ub * inv_a, gc = uc * inv_a;
+    const double ua = sqrt2 * nw + sqrt_rho * sv[6], ub = sqrt2 * mu * dw, ue = sqrt2 * mu * ew;
+    const double us_sum = k * ua + ccos * ub + csin * ue;
+    const double ga = (ua - betap * us_sum) * inv_a, gb = ub * inv_a, gc = ue * inv_a;
     const double h0 = bb * inv_a + ga;
-    double xt[KMAX];
-    double ztc = 0.0;
+    // alpha xt_e = alpha (inv_a (rq_e + vct) - h0 - gb cos_e - gc sin_e)
+    const double hh = alpha * (inv_a * vct - h0), agb = alpha * gb, agc = alpha * gc;
+    double axt[KMAX];
+#pragma unroll
+    for (int e = 0; e < KMAX; ++e)
+      axt[e] = e < k ? ((a_inv_a * rq[e] + hh) - agb * P.cos_t[e]) - agc * P.sin_t[e] : 0.0;
+    const double aztc = tree_sum<KMAX>(axt);
+    const double aztt = qp_group_sum<MT>(aztc, base, m);
+    // Relaxed updates and projection (z = Pi(zbar + u), u += zbar - z).
 #pragma unroll
     for (int e = 0; e < KMAX; ++e) {
       if (e < k) {
-        xt[e] = ((inv_a * rp[e] - h0) - gb * P.cos_t[e]) - gc * P.sin_t[e];
-        ztc += xt[e];
-      } else {
-        xt[e] = 0.0;
-      }
-    }
-    const double ztt = qp_group_sum<MT>(ztc, base, m);
-    // Relaxed updates and projection.
-#pragma unroll
-    for (int e = 0; e < KMAX; ++e) {
-      if (e < k) {
-        x[e] = alpha * xt[e] + (1.0 - alpha) * x[e];
-        const double zbar = alpha * xt[e] + (1.0 - alpha) * zid[e];
-        const double zn = fmax(zbar + yid[e] * inv_rho, 0.0);
-        yid[e] += rho * (zbar - zn);
+        x[e] = oma * x[e] + axt[e];
+        const double v = (oma * zid[e] + axt[e]) + uid[e];
+        const double zn = relu_bits(v);
+        uid[e] = v - zn;
         zid[e] = zn;
       }
     }
     {
-      const double zbar = alpha * ztc + (1.0 - alpha) * zc;
-      const double zn = fmin(fmax(zbar + yc * inv_rho, 0.0), 1.0);
-      yc += rho * (zbar - zn);
+      const double v = (oma * zc + aztc) + uc;
+      const double zn = fmin(relu_bits(v), 1.0);
+      uc = v - zn;
       zc = zn;
     }
     {
-      const double zbar = alpha * ztt + (1.0 - alpha) * ztot;
-      const double zn = fmax(zbar + ytot * inv_rho, gamma);
-      ytot += rho * (zbar - zn);
+      const double v = (oma * ztot + aztt) + utot;
+      const double zn = fmax(v, gamma);
+      utot = v - zn;
       ztot = zn;
     }
     if (iter % P.check_interval == 0 || iter == P.max_iters) {
@@ -381,7 +400,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
       for (int e = 0; e < KMAX; ++e) {
         if (e < k) {
           const double px = nu + mu * (P.cos_t[e] * du + P.sin_t[e] * eu);
-          const double dual = (2.0 * px + ((yc + ytot) + yid[e])) + q[e];
+          const double dual = (2.0 * px + rho * ((uc + utot) + uid[e])) - nq[e];
           rd = fmax(rd, fabs(dual));
         }
       }
@@ -395,14 +414,14 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
             if (e < k) {
               const int i = c * k + e;
               ox[j * n + i] = x[e];
-              oy[j * M + m + 1 + i] = yid[e];
+              oy[j * M + m + 1 + i] = rho * uid[e];
               oz[j * M + m + 1 + i] = zid[e];
             }
           }
-          oy[j * M + c] = yc;
+          oy[j * M + c] = rho * uc;
           oz[j * M + c] = zc;
           if (c == 0) {
-            oy[j * M + m] = ytot;
+            oy[j * M + m] = rho * utot;
             oz[j * M + m] = ztot;
             st.qp_iters[(size_t)g * 6 + j] = iter;
             st.qp_conv[(size_t)g * 6 + j] = ok ? 1 : 0;
