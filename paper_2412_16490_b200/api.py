@@ -473,7 +473,7 @@ class Engine:
     OP_NAMES = ("plane_tests", "triangle_tests", "qp_column_sweeps", "qp_solves", "gjk_iters", "support_verts",
                 "epa_iters", "point_queries", "pairs_needed", "epa_overflow",
                 "gjk_pairs_le4", "gjk_pairs_le8", "gjk_pairs_le16", "gjk_pairs_le32", "gjk_pairs_le64",
-                "gjk_pairs_gt64", "gjk_cycle_jumps", "gjk_iters_skipped", "reserved18", "reserved19")
+                "gjk_pairs_gt64", "gjk_cycle_jumps", "gjk_iters_skipped", "epa_max_iters", "epa_long_jobs")
 
     def evaluate(self, config: RunConfig, x, x_s) -> dict:
         """quasi_static_check (eval.cpp:91-158) for each grasp on the device: pd_mm, spd_mm, cdc_mm,

@@ -87,7 +87,7 @@ struct grasp_ctx {
   cudaStream_t stream = nullptr;
   bool has_hand = false, has_object = false;
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
-  DevBuf<unsigned char> pair_need, pair_hist;
+  DevBuf<unsigned char> pair_need, pair_hist, epa_hist;
 
   // hand
   DevHand H{};
@@ -580,7 +580,7 @@ struct grasp_ctx {
     st.ovf_cap = static_cast<int>(g * NP);
     st.big_scratch = big_scratch.p;
     st.big_slots = kBigSlots;
-    pair_count.ensure(3);  // list length, EPA jobs, list cursor
+    pair_count.ensure(4);  // list length, EPA jobs, list cursor, long EPA jobs
     pair_list.ensure(g * NP);
     st.pair_count = pair_count.p;
     st.pair_list = pair_list.p;
@@ -588,6 +588,9 @@ struct grasp_ctx {
     pair_hist.ensure(g * NP);
     ck(cudaMemsetAsync(pair_hist.p, 0, g * NP, stream), "memset");
     st.pair_hist = pair_hist.p;
+    epa_hist.ensure(g * NP);
+    ck(cudaMemsetAsync(epa_hist.p, 0, g * NP, stream), "memset");
+    st.epa_hist = epa_hist.p;
     seg_count.ensure(NP * kPairBuckets);
     seg_offset.ensure(NP * kPairBuckets);
     st.pair_need = pair_need.p;
@@ -596,8 +599,9 @@ struct grasp_ctx {
     // EPA jobs: up to a quarter of all pair slots at once; beyond that the
     // pair is redone by k_pairs_big (never observed).
     const size_t epa_cap = std::max<size_t>(1024, g * NP / 4);
-    epa_jobs.ensure(epa_cap * kEpaJobStride);
+    epa_jobs.ensure(2 * epa_cap * kEpaJobStride);
     st.epa_count = pair_count.p + 1;
+    st.epa_long_count = pair_count.p + 3;
     st.epa_jobs = epa_jobs.p;
     st.epa_cap = static_cast<int>(epa_cap);
     st.G = G;
@@ -689,14 +693,14 @@ struct grasp_ctx {
     launch(3, [&] {
       ck(cudaMemsetAsync(ovf_count.p, 0, sizeof(int), stream), "memset");
       const int* lk = tips_only ? h_tip_links_sorted.p : nullptr;
-      ck(cudaMemsetAsync(pair_count.p, 0, 3 * sizeof(int), stream), "memset");
+      ck(cudaMemsetAsync(pair_count.p, 0, 4 * sizeof(int), stream), "memset");
       ck(cudaMemsetAsync(seg_count.p, 0, sizeof(int) * nl * O.P * kPairBuckets, stream), "memset");
       k_pairs_cull<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
       k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.P * kPairBuckets);
       k_pairs_scatter<<<blocks(n, 128), 128, 0, stream>>>(st, lk, nl, O.P);
       k_pairs_list<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
       // EPA jobs spread over all SMs (32-thread blocks; few jobs per launch)
-      k_pairs_epa<<<blocks(std::min<long long>(n, st.epa_cap), 32), 32, 0, stream>>>(H, O, st);
+      k_pairs_epa<<<blocks(2 * std::min<long long>(n, st.epa_cap), 32), 32, 0, stream>>>(H, O, st);
     });
     launch(7, [&] { k_pairs_big<<<kBigSlots / 128, 128, 0, stream>>>(H, O, st); });
   }

@@ -732,13 +732,18 @@ __device__ __forceinline__ void queue_overflow(const DevState& st, int slot) {
 #ifndef GDEV_PAIRS_MIN_BLOCKS
 #define GDEV_PAIRS_MIN_BLOCKS 4
 #endif
+// Jobs whose slot needed more than kEpaLongPred EPA iterations last time go
+// to a second region (launched first, packed into their own warps): a
+// thread-per-job warp otherwise runs as long as its longest lane.
+constexpr int kEpaLongPred = 6;
 __device__ __forceinline__ void write_epa_job(const DevState& st, int slot, const SP (&simp)[4], int ns) {
-  const int job = atomicAdd(st.epa_count, 1);
+  const bool long_job = st.epa_hist[slot] > kEpaLongPred;
+  const int job = atomicAdd(long_job ? st.epa_long_count : st.epa_count, 1);
   if (job >= st.epa_cap) {
     queue_overflow(st, slot);
     return;
   }
-  double* jb = st.epa_jobs + (size_t)job * kEpaJobStride;
+  double* jb = st.epa_jobs + ((size_t)job + (long_job ? st.epa_cap : 0)) * kEpaJobStride;
   jb[0] = slot;
   jb[1] = ns;
 #pragma unroll
@@ -797,28 +802,23 @@ __global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHa
     store_pair(st.pairs + (size_t)slot * 12, r);
     return;
   }
-  const int job = atomicAdd(st.epa_count, 1);
-  if (job >= st.epa_cap) {
-    queue_overflow(st, slot);
-    return;
-  }
-  double* jb = st.epa_jobs + (size_t)job * kEpaJobStride;
-  jb[0] = slot;
-  jb[1] = ns;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    st3(jb + 2 + 9 * k, simp[k].w);
-    st3(jb + 5 + 9 * k, simp[k].a);
-    st3(jb + 8 + 9 * k, simp[k].b);
-  }
+  write_epa_job(st, slot, simp, ns);
 }
 
 // Pass 3: EPA for the overlapping pairs (geometry.cpp:168-205, 227-324), one
 // thread per job, polytope in local memory.
-__global__ void __launch_bounds__(128) k_pairs_epa(DevHand H, DevObject O, DevState st) {
+#ifndef GDEV_EPA_MIN_BLOCKS
+#define GDEV_EPA_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(32, GDEV_EPA_MIN_BLOCKS) k_pairs_epa(DevHand H, DevObject O, DevState st) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= min(*st.epa_count, st.epa_cap)) return;
-  const double* jb = st.epa_jobs + (size_t)i * kEpaJobStride;
+  const int n_long = min(*st.epa_long_count, st.epa_cap);
+  int job = st.epa_cap + i;  // predicted-long jobs first
+  if (i >= n_long) {
+    job = i - n_long;
+    if (job >= min(*st.epa_count, st.epa_cap)) return;
+  }
+  const double* jb = st.epa_jobs + (size_t)job * kEpaJobStride;
   const int slot = (int)jb[0], ns = (int)jb[1];
   SP simp[4];
 #pragma unroll
@@ -840,8 +840,11 @@ __global__ void __launch_bounds__(128) k_pairs_epa(DevHand H, DevObject O, DevSt
   if (st.ops) {
     atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * (A.nv + B.nv));
     atomicAdd(st.ops + kOpEpaIters, (unsigned long long)r.epa_iters);
+    atomicMax(st.ops + kOpEpaMaxIters, (unsigned long long)r.epa_iters);
+    if (r.epa_iters > 8) atomicAdd(st.ops + kOpEpaLongJobs, 1ull);
     if (r.flags & kPairOverflow) atomicAdd(st.ops + kOpEpaOverflow, 1ull);
   }
+  st.epa_hist[slot] = (unsigned char)min(255, r.epa_iters);
   if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
   if (r.flags & kPairOverflow) {
     queue_overflow(st, slot);

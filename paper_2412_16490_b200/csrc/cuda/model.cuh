@@ -148,8 +148,10 @@ struct DevState {
   unsigned char* pair_hist;  // [G*NP] GJK closest-point calls of the slot's last evaluation (bucketing)
   int* seg_count;      // [NP] needed pairs per (link, part) segment, then the fill cursor
   int* seg_offset;     // [NP] exclusive scan of seg_count
-  int* epa_count;      // overlapping pairs handed from GJK to the EPA kernel
-  double* epa_jobs;    // [epa_cap * kEpaJobStride]: slot, ns, 4 x (w, a, b)
+  int* epa_count;       // overlapping pairs handed from GJK to the EPA kernel
+  int* epa_long_count;  // ... of them predicted long (epa_hist), stored from epa_cap on
+  double* epa_jobs;     // [2 * epa_cap * kEpaJobStride]: slot, ns, 4 x (w, a, b)
+  unsigned char* epa_hist;  // [G*NP] EPA iterations of the slot's last EPA run (job split)
   int epa_cap;
 };
 
@@ -176,6 +178,8 @@ enum OpCounter {
   kOpGjkHist = 10,       // 10..15: pairs by GJK iterations <=4, <=8, <=16, <=32, <=64, >64
   kOpGjkCycleJumps = 16, // pairs whose GJK state cycle was fast-forwarded to the iteration cap
   kOpGjkItersSkipped = 17,
+  kOpEpaMaxIters = 18,  // max EPA iterations of one job (atomicMax)
+  kOpEpaLongJobs = 19,  // EPA jobs with more than 8 iterations
   kNumOps = 20
 };
 
