@@ -607,7 +607,7 @@ struct EpaScratchT {
   static constexpr int kV = V, kF = F, kH = HZ;
   SP verts[V];
   EpaFace faces[F];
-  int hu[HZ], hv[HZ];
+  int hk[HZ];  // horizon edges (u << 16) | v, in kill order
 };
 using EpaScratch = EpaScratchT<64, 128, 96>;
 using EpaScratchBig = EpaScratchT<kEpaMaxIters + 8, 4 * kEpaMaxIters, 4 * kEpaMaxIters>;
@@ -702,17 +702,22 @@ GDEV_FN bool epa(const SP (&simp)[4], int ns, const Hull& A, const Hull& B, doub
 
   const double grow_tol = 1e-10 * scale;
   EpaFace best_copy = s.faces[0];
-  for (int iter = 0; iter < kEpaMaxIters; ++iter) {
-    int best = -1;
-    double best_d = INFINITY;
-    for (int i = 0; i < nf; ++i) {
-      const double di = s.faces[i].d;
-      if (di < best_d - 1e-12 * scale ||
-          (di < best_d + 1e-12 * scale && best >= 0 && lex_less(-s.faces[i].n, -s.faces[best].n))) {
-        best_d = fmin(best_d, di);
-        best = i;
-      }
+  // Closest face (geometry.cpp:255-262), scanned in face-array order. The
+  // scan of the next iteration runs incrementally as the kill loop compacts
+  // the kept faces and the horizon loop appends the new ones: the same
+  // comparisons in the same order, one pass over the faces fewer.
+  int best = -1;
+  double best_d = INFINITY;
+  auto consider = [&](int i) {
+    const double di = s.faces[i].d;
+    if (di < best_d - 1e-12 * scale ||
+        (di < best_d + 1e-12 * scale && best >= 0 && lex_less(-s.faces[i].n, -s.faces[best].n))) {
+      best_d = fmin(best_d, di);
+      best = i;
     }
+  };
+  for (int i = 0; i < nf; ++i) consider(i);
+  for (int iter = 0; iter < kEpaMaxIters; ++iter) {
     if (best < 0) {
       out.flags |= kPairDegenerate;
       return false;
@@ -732,18 +737,21 @@ GDEV_FN bool epa(const SP (&simp)[4], int ns, const Hull& A, const Hull& B, doub
     int nh = 0;
     int kept = 0;
     bool overflow = false;
+    best = -1;
+    best_d = INFINITY;
     for (int i = 0; i < nf; ++i) {
       const EpaFace f = s.faces[i];
       if (dot(f.n, w.w) - f.d > 1e-12 * scale) {
         if (nh + 3 > kEpaMaxHorizon) {
           overflow = true;
         } else {
-          s.hu[nh] = f.v0; s.hv[nh++] = f.v1;
-          s.hu[nh] = f.v1; s.hv[nh++] = f.v2;
-          s.hu[nh] = f.v2; s.hv[nh++] = f.v0;
+          s.hk[nh++] = (f.v0 << 16) | f.v1;
+          s.hk[nh++] = (f.v1 << 16) | f.v2;
+          s.hk[nh++] = (f.v2 << 16) | f.v0;
         }
       } else {
-        s.faces[kept++] = f;
+        s.faces[kept] = f;
+        consider(kept++);
       }
     }
     nf = kept;
@@ -753,15 +761,17 @@ GDEV_FN bool epa(const SP (&simp)[4], int ns, const Hull& A, const Hull& B, doub
     }
     int n_boundary = 0;
     for (int e = 0; e < nh; ++e) {
+      const int ke = s.hk[e], rev = ((ke & 0xffff) << 16) | (ke >> 16);
       bool paired = false;
       for (int o = 0; o < nh; ++o)
-        if (s.hu[o] == s.hv[e] && s.hv[o] == s.hu[e]) paired = true;
+        if (s.hk[o] == rev) paired = true;
       if (!paired) {
         if (nf >= kEpaMaxFaces) {
           overflow = true;
           break;
         }
-        s.faces[nf++] = epa_make_face(s.verts, interior, s.hu[e], s.hv[e], wi);
+        s.faces[nf] = epa_make_face(s.verts, interior, ke >> 16, ke & 0xffff, wi);
+        consider(nf++);
         ++n_boundary;
       }
     }
