@@ -683,8 +683,24 @@ struct grasp_ctx {
   void launch_queries(bool tips_only) {
     const int per = tips_only ? H.m : st.NQ;
     const long long n = static_cast<long long>(st.G) * per;
+    // Lanes per query: GRASP_QGROUP_TIPS (tip-only launches, default 4) and
+    // GRASP_QGROUP (full launches, default 1 = thread per query).
+    auto lanes = [](const char* var, int dflt) {
+      const char* v = std::getenv(var);
+      const int l = v ? std::atoi(v) : dflt;
+      return (l == 2 || l == 4 || l == 8 || l == 16 || l == 32) ? l : 1;
+    };
+    const int L = tips_only ? lanes("GRASP_QGROUP_TIPS", 4) : lanes("GRASP_QGROUP", 1);
+    const int* sl = tips_only ? h_tip_slots.p : nullptr;
     launch(0, [&] {
-      k_point_query<<<blocks(n, 128), 128, 0, stream>>>(O, st, tips_only ? h_tip_slots.p : nullptr, per);
+      switch (L) {
+        case 2: k_point_query_group<2><<<blocks(n * 2, 128), 128, 0, stream>>>(O, st, sl, per); break;
+        case 4: k_point_query_group<4><<<blocks(n * 4, 128), 128, 0, stream>>>(O, st, sl, per); break;
+        case 8: k_point_query_group<8><<<blocks(n * 8, 128), 128, 0, stream>>>(O, st, sl, per); break;
+        case 16: k_point_query_group<16><<<blocks(n * 16, 128), 128, 0, stream>>>(O, st, sl, per); break;
+        case 32: k_point_query_group<32><<<blocks(n * 32, 128), 128, 0, stream>>>(O, st, sl, per); break;
+        default: k_point_query<<<blocks(n, 128), 128, 0, stream>>>(O, st, sl, per);
+      }
     });
   }
   void launch_pairs(bool tips_only) {

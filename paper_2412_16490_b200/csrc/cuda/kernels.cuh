@@ -423,6 +423,248 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int warm_face
   return best;
 }
 
+// point_to_mesh by an aligned group of L lanes of one warp (gmask = the
+// group's lanes, gl = lane in group); every lane returns the same hit. Each
+// sequential scan is split over the lanes and merged with an order-free
+// reduction that reproduces it exactly: a strict '<' scan in index order
+// picks the lexicographic minimum of (value, index); the inside test is "no
+// plane separates" (any-vote) plus the (depth, face) minimum. The culls use
+// the lane's own running best, an upper bound on the group's final minimum,
+// so every skipped face is still strictly worse than it.
+template <int L>
+__device__ __forceinline__ void group_lexmin(unsigned gmask, double& v, int& i) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(gmask, v, o);
+    const int i2 = __shfl_xor_sync(gmask, i, o);
+    if (v2 < v || (v2 == v && i2 < i)) {
+      v = v2;
+      i = i2;
+    }
+  }
+}
+template <int L>
+__device__ __forceinline__ void group_lexmin(unsigned gmask, float& v, int& i) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) {
+    const float v2 = __shfl_xor_sync(gmask, v, o);
+    const int i2 = __shfl_xor_sync(gmask, i, o);
+    if (v2 < v || (v2 == v && i2 < i)) {
+      v = v2;
+      i = i2;
+    }
+  }
+}
+template <int L>
+__device__ __forceinline__ float group_fmin(unsigned gmask, float v) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(gmask, v, o));
+  return v;
+}
+
+template <int L>
+__device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int warm_face, int gl, unsigned gmask,
+                                        unsigned* plane_tests, unsigned* tri_tests) {
+  PointHit best;
+  best.d = INFINITY;
+  best.pb = mk(0, 0, 0);
+  best.n = mk(0, 0, 1);
+  best.part = -1;
+  best.face = -1;
+  unsigned planes = 0, tris = 0;
+  const float px = (float)p.x, py = (float)p.y, pz = (float)p.z;
+  double ub_warm = INFINITY;
+  if (warm_face >= 0 && warm_face < O.F) {
+    if (gl == 0) ++tris;
+    const double* F = O.faces + (size_t)warm_face * kFaceStride;
+    ub_warm = nrm(p - closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6)));
+  }
+  for (int part = 0; part < O.P; ++part) {
+    const int f0 = __ldg(O.part_fbeg + part), f1 = __ldg(O.part_fbeg + part + 1);
+    {
+      const double* S = O.part_sphere + 4 * part;
+      const double lb = nrm(p - ldg3(S)) - __ldg(S + 3) - kCullSlack;
+      if (lb > best.d || lb > ub_warm) continue;
+    }
+    const int c0 = __ldg(O.part_cbeg + part), c1 = __ldg(O.part_cbeg + part + 1);
+    float ubA = INFINITY;
+    int seed_f;
+    {
+      float lb_seed = INFINITY;
+      int seed_c = c0;
+      for (int c = c0 + gl; c < c1; c += L) {
+        const float4 S = __ldg(O.cluster_sphere32 + c);
+        const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
+        const float dist = sqrt_approx(dx * dx + dy * dy + dz * dz);
+        ubA = fminf(ubA, dist + S.w);
+        if (dist - S.w < lb_seed) {
+          lb_seed = dist - S.w;
+          seed_c = c;
+        }
+      }
+      ubA = group_fmin<L>(gmask, ubA);
+      group_lexmin<L>(gmask, lb_seed, seed_c);
+      const int s0 = __ldg(O.cluster_fbeg + seed_c), e = __ldg(O.cluster_fbeg + seed_c + 1);
+      float lbf = INFINITY;
+      seed_f = s0;
+      for (int f = s0 + gl; f < e; f += L) {
+        const float4 S = __ldg(O.face_sphere32 + f);
+        const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
+        const float lb = sqrt_approx(dx * dx + dy * dy + dz * dz) - S.w;
+        if (lb < lbf) {
+          lbf = lb;
+          seed_f = f;
+        }
+      }
+      group_lexmin<L>(gmask, lbf, seed_f);
+    }
+    bool inside;
+    double min_depth = INFINITY;
+    int min_face = INT_MAX;
+    {
+      const double4 Q = ld_plane(O, seed_f);
+      if (gl == 0) ++planes;
+      inside = !((Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z)) < -1e-12);
+    }
+    if (inside) {
+      // chunks of L planes; the group stops after the first chunk with a
+      // separating plane (whether one exists does not depend on the order)
+      for (int fb = f0; fb < f1; fb += L) {
+        const int f = fb + gl;
+        bool sep = false;
+        if (f < f1) {
+          const double4 Q = ld_plane(O, f);
+          ++planes;
+          const double depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
+          if (depth < -1e-12) {
+            sep = true;
+          } else if (depth < min_depth) {
+            min_depth = depth;
+            min_face = f;
+          }
+        }
+        if (__any_sync(gmask, sep)) {
+          inside = false;
+          break;
+        }
+      }
+      if (inside) group_lexmin<L>(gmask, min_depth, min_face);
+    }
+    double sd;
+    D3 pt, nn;
+    int sf = -1;
+    if (inside && isfinite(min_depth)) {
+      const double4 Q = ld_plane(O, min_face);
+      const D3 best_n = mk(Q.x, Q.y, Q.z);
+      sd = -min_depth;
+      nn = best_n;
+      pt = p + best_n * min_depth;
+    } else {
+      float bound;
+      {
+        if (gl == 0) ++tris;
+        const double* F = O.faces + (size_t)seed_f * kFaceStride;
+        const double d_seed = nrm(p - closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6)));
+        bound = fminf(fminf(ubA, __double2float_ru(d_seed)), __double2float_ru(ub_warm)) + kCullSlack32;
+      }
+      sd = INFINITY;
+      float sd32 = INFINITY;
+      pt = mk(0, 0, 0);
+      int lf = INT_MAX;
+      for (int c = c0; c < c1; ++c) {
+        {
+          const float4 S = __ldg(O.cluster_sphere32 + c);
+          const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
+          const float reach = fminf(bound, sd32) + S.w + kCullSlack32;
+          if (dx * dx + dy * dy + dz * dz > reach * reach) continue;
+        }
+        const int e = __ldg(O.cluster_fbeg + c + 1);
+        for (int f = __ldg(O.cluster_fbeg + c) + gl; f < e; f += L) {
+          const float cut = fminf(bound, sd32);
+          {
+            const float4 S = __ldg(O.face_sphere32 + f);
+            const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
+            const float reach = cut + S.w + kCullSlack32;
+            if (dx * dx + dy * dy + dz * dz > reach * reach) continue;
+          }
+          {
+            const float4 B0 = __ldg(O.face_box32 + 4 * f), B1 = __ldg(O.face_box32 + 4 * f + 1);
+            const float4 B2 = __ldg(O.face_box32 + 4 * f + 2), B3 = __ldg(O.face_box32 + 4 * f + 3);
+            const float rx = px - B0.x, ry = py - B0.y, rz = pz - B0.z;
+            const float eu = fmaxf(fabsf(rx * B1.x + ry * B1.y + rz * B1.z) - B0.w, 0.0f);
+            const float ev = fmaxf(fabsf(rx * B2.x + ry * B2.y + rz * B2.z) - B1.w, 0.0f);
+            const float en = fmaxf(fabsf(rx * B3.x + ry * B3.y + rz * B3.z) - B2.w, 0.0f);
+            const float reach = cut + kCullSlack32;
+            if (eu * eu + ev * ev + en * en > reach * reach) continue;
+          }
+          ++tris;
+          const double* F = O.faces + (size_t)f * kFaceStride;
+          const D3 cp = closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6));
+          const double d = nrm(p - cp);
+          if (d < sd) {
+            sd = d;
+            sd32 = __double2float_ru(d) + kCullSlack32;
+            pt = cp;
+            lf = f;
+          }
+        }
+      }
+      // winner: the lane holding the (distance, face) minimum
+      double wd = sd;
+      int wf = lf;
+      group_lexmin<L>(gmask, wd, wf);
+      const unsigned win = __ballot_sync(gmask, lf == wf && wf != INT_MAX);
+      const int src = win ? __ffs(win) - 1 : (threadIdx.x & 31);
+      pt = mk(__shfl_sync(gmask, pt.x, src), __shfl_sync(gmask, pt.y, src), __shfl_sync(gmask, pt.z, src));
+      sd = wd;
+      sf = wf == INT_MAX ? -1 : wf;
+      nn = sd > 1e-14 ? (p - pt) / sd : mk(0, 0, 1);
+    }
+    if (sd < best.d) {
+      best.d = sd;
+      best.pb = pt;
+      best.n = nn;
+      best.part = part;
+      best.face = sf;
+    }
+  }
+  if (plane_tests) *plane_tests = planes;
+  if (tri_tests) *tri_tests = tris;
+  return best;
+}
+
+// Group-per-query variant for launches with few queries (the coarse stage's
+// tip queries: one query per thread leaves most SMs idle).
+template <int L>
+__global__ void __launch_bounds__(128) k_point_query_group(DevObject O, DevState st, const int* __restrict__ slots,
+                                                           int n_slots) {
+  const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / L;
+  const int gl = threadIdx.x & (L - 1);
+  const unsigned gmask = L == 32 ? 0xffffffffu : (((1u << L) - 1) << ((threadIdx.x & 31) & ~(L - 1)));
+  const int per = slots ? n_slots : st.NQ;
+  if (t >= (long long)st.G * per) return;
+  const int g = (int)(t / per);
+  const int slot = slots ? slots[t % per] : (int)(t % per);
+  if (st.failed[g]) return;
+  const D3 p = ld3(st.qpts + ((size_t)g * st.NQ + slot) * 3);
+  unsigned planes, tris;
+  int* qf = st.qface + (size_t)g * st.NQ + slot;
+  const PointHit h = point_to_mesh_group<L>(O, p, *qf, gl, gmask, &planes, &tris);
+  __syncwarp(gmask);
+  if (st.ops) {
+    atomicAdd(st.ops + kOpPlaneTests, (unsigned long long)planes);
+    atomicAdd(st.ops + kOpTriangleTests, (unsigned long long)tris);
+    if (gl == 0) atomicAdd(st.ops + kOpPointQueries, 1ull);
+  }
+  if (gl != 0) return;
+  *qf = h.face;
+  double* o = st.qres + ((size_t)g * st.NQ + slot) * 8;
+  o[0] = h.d;
+  st3(o + 1, h.pb);
+  st3(o + 4, h.n);
+  o[7] = h.part;
+}
+
 // One thread per (grasp, query slot). slots == nullptr: all NQ slots.
 // 6 blocks/SM (80 registers, small spills) measured best: the divergent, latency-bound
 // query loop needs the extra resident warps.

@@ -568,3 +568,31 @@ np.save(sys.argv[1], eng.synthesize(cfg, x0).x)
     a, b = np.load(tmp_path / "a.npy"), np.load(tmp_path / "b.npy")
     same = (a == b).all(axis=1)
     assert same.mean() >= 0.75, same.mean()
+
+
+def test_group_point_queries_bitwise_equal_thread_queries(G, monkeypatch):
+    """The lane-group point query (tip queries of the coarse stage, 4 lanes per query by
+    default) merges its split scans with order-free reductions; any group size must give
+    the thread-per-query kernel's results bit for bit, on the tips and on all query slots."""
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    hand = G.HandModel.from_file(root / "paper_2412_16490_b200/assets/hands/shadow_like.json")
+    obj = G.load_object(root / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 96, 23
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 30, 10, 10
+    x0 = G.init_poses(hand, obj, cfg.batch, cfg.seed, cfg.init)
+    eng = G.Engine(0)
+    eng.set_hand(hand)
+    eng.set_object(obj)
+    outs = {}
+    for tips, full in (("1", "1"), ("4", "1"), ("8", "2"), ("32", "4")):
+        monkeypatch.setenv("GRASP_QGROUP_TIPS", tips)
+        monkeypatch.setenv("GRASP_QGROUP", full)
+        outs[(tips, full)] = eng.synthesize(cfg, x0)
+    ref = outs[("1", "1")]
+    for k, o in outs.items():
+        assert np.array_equal(o.x, ref.x), k
+        assert np.array_equal(o.x_s, ref.x_s), k
+        assert np.array_equal(o.failed, ref.failed), k
+        assert np.array_equal(o.contacts, ref.contacts, equal_nan=True), k
