@@ -86,7 +86,7 @@ struct QpSmem {
 // mode 1: final record (frames from st.frames, cold start).
 // mode 2: standalone batch (frames from st.frames, warm if qp_ready).
 #ifndef GDEV_QP_MIN_BLOCKS
-#define GDEV_QP_MIN_BLOCKS 4  // 128 registers, small spills (measured best)
+#define GDEV_QP_MIN_BLOCKS 3  // 168 registers, no spills (measured best since the scaled-dual sweep; 4 and 5 spill)
 #endif
 template <int KT, int MT>
 __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
