@@ -972,7 +972,7 @@ __device__ __forceinline__ void queue_overflow(const DevState& st, int slot) {
 // Pass 2: GJK, one thread per listed pair (dense warps, register simplex,
 // no EPA buffer). Overlapping pairs pass their terminal simplex to k_pairs_epa.
 #ifndef GDEV_PAIRS_MIN_BLOCKS
-#define GDEV_PAIRS_MIN_BLOCKS 3  // 168 registers (measured: 3 > 4 > 5 > 6 since the bucketed list)
+#define GDEV_PAIRS_MIN_BLOCKS 2  // 255 registers (measured: 2 > 3 > 4 > 5 > 6 since the bucketed list)
 #endif
 // Jobs whose slot needed more than kEpaLongPred EPA iterations last time go
 // to a second region (launched first, packed into their own warps): a
