@@ -272,15 +272,20 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
   double* oy = st.warm_y + (size_t)g * M * 6;
   double* oz = st.out_z + (size_t)g * M * 6;
 
-  int sweeps = 0;
-  for (int iter = 1; iter <= P.max_iters; ++iter) {
-    sweeps = iter;
+  // After a projection z = max(v, 0) and u = min(v, 0) for v = zbar + u, so
+  // z - u = |v| and (1 - alpha) z + u = (v >= 0 ? 1 - alpha : 1) v: from the
+  // second sweep on, the per-edge state is (x, v) and the edge update is four
+  // fp64 operations. The first sweep starts from the warm (z, u), which need
+  // not be complementary, and is peeled (kFirst).
+  double vz[KMAX];
+  auto sweep = [&]<bool kFirst>(int iter) -> bool {
     // rhs = A'(rho z - y) + sigma x - q = rq + vct (vct: the cap and total
     // rows, common to the lane's edges) ; r' = B^-1 rhs
     const double vct = rho * ((zc - uc) + (ztot - utot));
     double rq[KMAX];
 #pragma unroll
-    for (int e = 0; e < KMAX; ++e) rq[e] = e < k ? rho * (zid[e] - uid[e]) + (sigma * x[e] + nq[e]) : 0.0;
+    for (int e = 0; e < KMAX; ++e)
+      rq[e] = e < k ? rho * (kFirst ? zid[e] - uid[e] : fabs(vz[e])) + (sigma * x[e] + nq[e]) : 0.0;
     const double bsum = tree_sum<KMAX>(rq) + k * vct;
     const double bb = betap * bsum;
     double tv[7];
@@ -358,10 +363,14 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
     for (int e = 0; e < KMAX; ++e) {
       if (e < k) {
         x[e] = oma * x[e] + axt[e];
-        const double v = (oma * zid[e] + axt[e]) + uid[e];
-        const double zn = relu_bits(v);
-        uid[e] = v - zn;
-        zid[e] = zn;
+        if constexpr (kFirst) {
+          vz[e] = (oma * zid[e] + axt[e]) + uid[e];
+        } else {
+          const double fac = __double2hiint(vz[e]) >= 0 ? oma : 1.0;  // sign bit: ALU, not fp64
+          vz[e] = fac * vz[e] + axt[e];
+        }
+      } else {
+        vz[e] = 0.0;
       }
     }
     {
@@ -385,7 +394,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
       double rp_ = fmax(fabs(axc - zc), fabs(axt - ztot));
 #pragma unroll
       for (int e = 0; e < KMAX; ++e)
-        if (e < k) rp_ = fmax(rp_, fabs(x[e] - zid[e]));
+        if (e < k) rp_ = fmax(rp_, fabs(x[e] - relu_bits(vz[e])));
       rp_ = qp_group_max<MT>(rp_, base, m);
       // W x over the column, then (W^T W x)_e = edge_e . (wf + wt x p)
       D3 wf, wt;
@@ -400,7 +409,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
       for (int e = 0; e < KMAX; ++e) {
         if (e < k) {
           const double px = nu + mu * (P.cos_t[e] * du + P.sin_t[e] * eu);
-          const double dual = (2.0 * px + rho * ((uc + utot) + uid[e])) - nq[e];
+          const double dual = (2.0 * px + rho * ((uc + utot) + (vz[e] - relu_bits(vz[e])))) - nq[e];
           rd = fmax(rd, fabs(dual));
         }
       }
@@ -414,8 +423,8 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
             if (e < k) {
               const int i = c * k + e;
               ox[j * n + i] = x[e];
-              oy[j * M + m + 1 + i] = rho * uid[e];
-              oz[j * M + m + 1 + i] = zid[e];
+              oy[j * M + m + 1 + i] = rho * (vz[e] - relu_bits(vz[e]));
+              oz[j * M + m + 1 + i] = relu_bits(vz[e]);
             }
           }
           oy[j * M + c] = rho * uc;
@@ -428,7 +437,17 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
           }
         }
       }
-      if (__all_sync(kFull, frozen)) break;
+      if (__all_sync(kFull, frozen)) return true;
+    }
+    return false;
+  };
+  int sweeps = 0;
+  if (P.max_iters >= 1) {
+    sweeps = 1;
+    bool stop = sweep.template operator()<true>(1);
+    for (int iter = 2; iter <= P.max_iters && !stop; ++iter) {
+      sweeps = iter;
+      stop = sweep.template operator()<false>(iter);
     }
   }
   if (lane == 0) {
