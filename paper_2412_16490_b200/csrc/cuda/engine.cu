@@ -101,7 +101,7 @@ struct grasp_ctx {
   DevObject O{};
   DevBuf<int> o_fbeg, o_vbeg;
   DevBuf<double> o_faces, o_verts, o_centroid, o_half, o_obb, o_part_sphere, o_face_sphere, o_part_box;
-  DevBuf<float4> o_face_sphere32, o_cluster_sphere32, o_face_box32;
+  DevBuf<float4> o_face_sphere32, o_cluster_sphere32, o_face_box32, o_cluster_box32;
   DevBuf<double4> o_face_plane;
   DevBuf<int> o_part_cbeg, o_cluster_fbeg;
 
@@ -485,7 +485,7 @@ struct grasp_ctx {
     // each with a sphere containing its faces' spheres (fp32 centre, radius
     // from the rounded centre in fp64, rounded up).
     std::vector<int> part_cbeg(P + 1, 0), cluster_fbeg;
-    std::vector<float4> cluster32;
+    std::vector<float4> cluster32, cbox32;
     for (int p = 0; p < P; ++p) {
       part_cbeg[p] = static_cast<int>(cluster32.size());
       for (int a = fbeg[p]; a < fbeg[p + 1]; a += kFaceCluster) {
@@ -502,6 +502,68 @@ struct grasp_ctx {
         const float r32 = std::nextafter(std::nextafter(static_cast<float>(r * (1.0 + 1e-12)), 1e30f), 1e30f);
         cluster32.push_back(make_float4(cx, cy, cz, r32 * (1.0f + 1e-6f)));
         cluster_fbeg.push_back(a);
+        // Oriented box of the cluster's vertices: principal axes (Jacobi
+        // eigenvectors of the vertex covariance), rounded to fp32, extents
+        // measured along the rounded axes from the rounded centre and
+        // inflated like the face boxes (slack covers the fp32 axes' ~1e-7
+        // deviation from orthonormality).
+        {
+          double mean[3] = {0, 0, 0}, C[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+          const int nv = 3 * (b - a);
+          for (int f = a; f < b; ++f)
+            for (int q = 0; q < 3; ++q)
+              for (int k = 0; k < 3; ++k) mean[k] += faces[static_cast<size_t>(f) * kFaceStride + 3 * q + k] / nv;
+          for (int f = a; f < b; ++f)
+            for (int q = 0; q < 3; ++q) {
+              const double* X = faces.data() + static_cast<size_t>(f) * kFaceStride + 3 * q;
+              for (int r = 0; r < 3; ++r)
+                for (int k = 0; k < 3; ++k) C[r][k] += (X[r] - mean[r]) * (X[k] - mean[k]);
+            }
+          double E[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};  // columns = eigenvectors
+          for (int sweep = 0; sweep < 32; ++sweep) {
+            const double off = std::fabs(C[0][1]) + std::fabs(C[0][2]) + std::fabs(C[1][2]);
+            if (!(off > 1e-30)) break;
+            for (int pp = 0; pp < 2; ++pp)
+              for (int qq = pp + 1; qq < 3; ++qq) {
+                if (!(std::fabs(C[pp][qq]) > 1e-300)) continue;
+                const double th = 0.5 * std::atan2(2.0 * C[pp][qq], C[qq][qq] - C[pp][pp]);
+                const double cs = std::cos(th), sn = std::sin(th);
+                for (int k = 0; k < 3; ++k) {  // C <- C J
+                  const double ckp = C[k][pp], ckq = C[k][qq];
+                  C[k][pp] = cs * ckp - sn * ckq;
+                  C[k][qq] = sn * ckp + cs * ckq;
+                }
+                for (int k = 0; k < 3; ++k) {  // C <- J^T C
+                  const double cpk = C[pp][k], cqk = C[qq][k];
+                  C[pp][k] = cs * cpk - sn * cqk;
+                  C[qq][k] = sn * cpk + cs * cqk;
+                }
+                for (int k = 0; k < 3; ++k) {  // E <- E J
+                  const double ekp = E[k][pp], ekq = E[k][qq];
+                  E[k][pp] = cs * ekp - sn * ekq;
+                  E[k][qq] = sn * ekp + cs * ekq;
+                }
+              }
+          }
+          float ax[3][3], of[3];
+          for (int r = 0; r < 3; ++r)
+            for (int k = 0; k < 3; ++k) ax[r][k] = static_cast<float>(E[k][r]);
+          for (int k = 0; k < 3; ++k) of[k] = static_cast<float>(mean[k]);
+          double h[3] = {0, 0, 0};
+          for (int f = a; f < b; ++f)
+            for (int q = 0; q < 3; ++q) {
+              const double* X = faces.data() + static_cast<size_t>(f) * kFaceStride + 3 * q;
+              const double r3[3] = {X[0] - of[0], X[1] - of[1], X[2] - of[2]};
+              for (int r = 0; r < 3; ++r)
+                h[r] = std::max(h[r], std::fabs(r3[0] * ax[r][0] + r3[1] * ax[r][1] + r3[2] * ax[r][2]));
+            }
+          float hf[3];
+          for (int k = 0; k < 3; ++k) hf[k] = std::nextafter(static_cast<float>(h[k] * (1.0 + 1e-6) + 1e-9), 1e30f);
+          cbox32.push_back(make_float4(of[0], of[1], of[2], hf[0]));
+          cbox32.push_back(make_float4(ax[0][0], ax[0][1], ax[0][2], hf[1]));
+          cbox32.push_back(make_float4(ax[1][0], ax[1][1], ax[1][2], hf[2]));
+          cbox32.push_back(make_float4(ax[2][0], ax[2][1], ax[2][2], 0.0f));
+        }
       }
     }
     part_cbeg[P] = static_cast<int>(cluster32.size());
@@ -509,6 +571,7 @@ struct grasp_ctx {
     o_part_cbeg.upload(part_cbeg, s);
     o_cluster_fbeg.upload(cluster_fbeg, s);
     o_cluster_sphere32.upload(cluster32, s);
+    o_cluster_box32.upload(cbox32, s);
     ck(cudaStreamSynchronize(s), "object upload");
     O.part_sphere = o_part_sphere.p;
     O.part_box = o_part_box.p;
@@ -518,6 +581,7 @@ struct grasp_ctx {
     O.face_plane = o_face_plane.p;
     O.part_cbeg = o_part_cbeg.p;
     O.cluster_fbeg = o_cluster_fbeg.p;
+    O.cluster_box32 = o_cluster_box32.p;
     O.cluster_sphere32 = o_cluster_sphere32.p;
     O.P = P;
     O.F = d->n_faces;

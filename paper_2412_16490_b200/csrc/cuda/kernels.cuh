@@ -227,6 +227,19 @@ __device__ __forceinline__ double4 ld_plane(const DevObject& O, int f) {
   return make_double4(a.x, a.y, b.x, b.y);
 }
 
+// Distance from p to cluster c's oriented box (a lower bound on the distance
+// to every face of the cluster) exceeds reach.
+__device__ __forceinline__ bool cluster_box_far(const DevObject& O, int c, float px, float py, float pz,
+                                                float reach) {
+  const float4 B0 = __ldg(O.cluster_box32 + 4 * c), B1 = __ldg(O.cluster_box32 + 4 * c + 1);
+  const float4 B2 = __ldg(O.cluster_box32 + 4 * c + 2), B3 = __ldg(O.cluster_box32 + 4 * c + 3);
+  const float rx = px - B0.x, ry = py - B0.y, rz = pz - B0.z;
+  const float eu = fmaxf(fabsf(rx * B1.x + ry * B1.y + rz * B1.z) - B0.w, 0.0f);
+  const float ev = fmaxf(fabsf(rx * B2.x + ry * B2.y + rz * B2.z) - B1.w, 0.0f);
+  const float en = fmaxf(fabsf(rx * B3.x + ry * B3.y + rz * B3.z) - B2.w, 0.0f);
+  return eu * eu + ev * ev + en * en > reach * reach;
+}
+
 __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int warm_face = -1,
                                          unsigned* plane_tests = nullptr, unsigned* tri_tests = nullptr) {
   PointHit best;
@@ -371,6 +384,7 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int warm_face
           const float reach = fminf(bound, sd32) + S.w + kCullSlack32;
           if (dx * dx + dy * dy + dz * dz > reach * reach) continue;
         }
+        if (cluster_box_far(O, c, px, py, pz, fminf(bound, sd32) + kCullSlack32)) continue;
         const int e = __ldg(O.cluster_fbeg + c + 1);
         for (int f = __ldg(O.cluster_fbeg + c); f < e; ++f) {
           const float cut = fminf(bound, sd32);
@@ -578,6 +592,7 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int warm_face,
           const float reach = fminf(bound, sd32) + S.w + kCullSlack32;
           if (dx * dx + dy * dy + dz * dz > reach * reach) continue;
         }
+        if (cluster_box_far(O, c, px, py, pz, fminf(bound, sd32) + kCullSlack32)) continue;
         const int e = __ldg(O.cluster_fbeg + c + 1);
         for (int f = __ldg(O.cluster_fbeg + c) + gl; f < e; f += L) {
           const float cut = fminf(bound, sd32);

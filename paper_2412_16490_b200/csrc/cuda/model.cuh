@@ -73,6 +73,7 @@ struct DevObject {
   const int* part_cbeg;         // [P+1] face clusters of each part
   const int* cluster_fbeg;      // [NC+1] first face of each cluster (consecutive indices)
   const float4* cluster_sphere32;  // [NC] fp32 sphere bounding the cluster's face spheres
+  const float4* cluster_box32;     // [NC*4] fp32 oriented box of the cluster's vertices (face-box layout)
 };
 
 constexpr int kFaceCluster = 16;  // faces per point-query cluster
