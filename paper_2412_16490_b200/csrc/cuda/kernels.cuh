@@ -227,6 +227,23 @@ __device__ __forceinline__ double4 ld_plane(const DevObject& O, int f) {
   return make_double4(a.x, a.y, b.x, b.y);
 }
 
+// Signed distance from p to part's containing box (center, half extents,
+// axes column-major; model.cuh part_box): negative inside. The part lies in
+// the box, so this bounds the part's signed distance from below, also for
+// points inside (the part's depth is at most the box's).
+__device__ __forceinline__ double part_box_dist(const DevObject& O, int part, D3 p) {
+  const double* b = O.part_box + 15 * part;
+  const D3 r = p - ldg3(b);
+  double acc = 0.0, mx = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double e = fabs(dot(r, ldg3(b + 6 + 3 * k))) - __ldg(b + 3 + k);
+    mx = fmax(mx, e);
+    acc += e > 0.0 ? e * e : 0.0;
+  }
+  return mx > 0.0 ? sqrt(acc) : mx;
+}
+
 // Distance from p to cluster c's oriented box (a lower bound on the distance
 // to every face of the cluster) exceeds reach.
 __device__ __forceinline__ bool cluster_box_far(const DevObject& O, int c, float px, float py, float pz,
@@ -269,6 +286,9 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int warm_face
       const double* S = O.part_sphere + 4 * part;
       const double lb = nrm(p - ldg3(S)) - __ldg(S + 3) - kCullSlack;
       if (lb > best.d || lb > ub_warm) continue;
+      // the part's containing box (0 for points inside it)
+      const double lbb = part_box_dist(O, part, p) - kCullSlack;
+      if (lbb > best.d || lbb > ub_warm) continue;
     }
     // Face clusters (runs of consecutive faces with fp32 bounding spheres):
     // an upper bound on the part distance (min |p-C| + R) and a seed face,
@@ -499,6 +519,9 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int warm_face,
       const double* S = O.part_sphere + 4 * part;
       const double lb = nrm(p - ldg3(S)) - __ldg(S + 3) - kCullSlack;
       if (lb > best.d || lb > ub_warm) continue;
+      // the part's containing box (0 for points inside it)
+      const double lbb = part_box_dist(O, part, p) - kCullSlack;
+      if (lbb > best.d || lbb > ub_warm) continue;
     }
     const int c0 = __ldg(O.part_cbeg + part), c1 = __ldg(O.part_cbeg + part + 1);
     float ubA = INFINITY;
