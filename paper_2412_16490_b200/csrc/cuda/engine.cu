@@ -778,7 +778,7 @@ struct grasp_ctx {
       k_pairs_cull<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
       k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.P * kPairBuckets);
       k_pairs_scatter<<<blocks(n, 128), 128, 0, stream>>>(st, lk, nl, O.P);
-      k_pairs_list<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
+      k_pairs_list<<<blocks(n, GDEV_PAIRS_BLOCK), GDEV_PAIRS_BLOCK, 0, stream>>>(H, O, st);
       // EPA jobs spread over all SMs (32-thread blocks; few jobs per launch)
       k_pairs_epa<<<blocks(2 * std::min<long long>(n, st.epa_cap), 32), 32, 0, stream>>>(H, O, st);
     });

@@ -1009,6 +1009,9 @@ __device__ __forceinline__ void queue_overflow(const DevState& st, int slot) {
 
 // Pass 2: GJK, one thread per listed pair (dense warps, register simplex,
 // no EPA buffer). Overlapping pairs pass their terminal simplex to k_pairs_epa.
+#ifndef GDEV_PAIRS_BLOCK
+#define GDEV_PAIRS_BLOCK 128
+#endif
 #ifndef GDEV_PAIRS_MIN_BLOCKS
 #define GDEV_PAIRS_MIN_BLOCKS 2  // 255 registers (measured: 2 > 3 > 4 > 5 > 6 since the bucketed list)
 #endif
@@ -1061,7 +1064,7 @@ __device__ __forceinline__ void store_separated(double* o, const Simplex& sx, co
 
 
 // Pass 2 (default): GJK, one thread per listed pair from start to end.
-__global__ void __launch_bounds__(128, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHand H, DevObject O, DevState st) {
+__global__ void __launch_bounds__(GDEV_PAIRS_BLOCK, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHand H, DevObject O, DevState st) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *st.pair_count) return;
   const int slot = st.pair_list[i];
