@@ -671,8 +671,8 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int warm_face,
   return best;
 }
 
-// Group-per-query variant for launches with few queries (the coarse stage's
-// tip queries: one query per thread leaves most SMs idle).
+// Group-per-query variant for launches with few queries (the fine and final
+// stages' tip-centre queries, G x m: one query per thread leaves most SMs idle).
 template <int L>
 __global__ void __launch_bounds__(128) k_point_query_group(DevObject O, DevState st, const int* __restrict__ slots,
                                                            int n_slots) {

@@ -571,7 +571,7 @@ np.save(sys.argv[1], eng.synthesize(cfg, x0).x)
 
 
 def test_group_point_queries_bitwise_equal_thread_queries(G, monkeypatch):
-    """The lane-group point query (tip queries of the coarse stage, 4 lanes per query by
+    """The lane-group point query (tip-centre queries of the fine/final stages, 4 lanes per query by
     default) merges its split scans with order-free reductions; any group size must give
     the thread-per-query kernel's results bit for bit, on the tips and on all query slots."""
     from pathlib import Path
