@@ -217,13 +217,17 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
   // sin_e e), torque_e = p x edge_e. Every product with W or W^T is formed
   // from it: W v = (f, p x f) with f = n S0 + mu (d S1 + e S2), S0 = sum v_e,
   // S1 = sum cos_e v_e, S2 = sum sin_e v_e; (W^T u)_e = edge_e . (u_f + u_t x p).
-  const D3 fp = ld3(s.frame + 12 * c), fn = ld3(s.frame + 12 * c + 3);
-  const D3 fd = ld3(s.frame + 12 * c + 6), fe = ld3(s.frame + 12 * c + 9);
+  const D3 fp = ld3(s.frame + 12 * c);
+  // The sweep uses the frame only as sqrt2 n, sqrt2 mu d, sqrt2 mu e (the U
+  // rows); the residual check reloads the unscaled frame from shared memory.
+  const D3 sn = sqrt2 * ld3(s.frame + 12 * c + 3);
+  const D3 sdv = (sqrt2 * mu) * ld3(s.frame + 12 * c + 6), sev = (sqrt2 * mu) * ld3(s.frame + 12 * c + 9);
   double ccos = 0.0, csin = 0.0;
 #pragma unroll
   for (int e = 0; e < KMAX; ++e)
     if (e < k) ccos += P.cos_t[e], csin += P.sin_t[e];
   auto w_times = [&](const double (&v)[KMAX], D3& f, D3& t, double& s0) {
+    const D3 fn = ld3(s.frame + 12 * c + 3), fd = ld3(s.frame + 12 * c + 6), fe = ld3(s.frame + 12 * c + 9);
     double s1 = 0.0, s2 = 0.0;
     s0 = 0.0;
 #pragma unroll
@@ -304,10 +308,9 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
       const double s1r = (s1a + s1b) + ccos * vct, s2r = (s2a + s2b) + csin * vct;
       const double s0 = (bsum - k * bb) * inv_a;
       const double s1 = (s1r - ccos * bb) * inv_a, s2 = (s2r - csin * bb) * inv_a;
-      const D3 f = s0 * fn + mu * (s1 * fd + s2 * fe);
-      const D3 t = cross(fp, f);
-      const double tl[7] = {sqrt2 * f.x, sqrt2 * f.y, sqrt2 * f.z, sqrt2 * t.x, sqrt2 * t.y, sqrt2 * t.z,
-                            sqrt_rho * s0};
+      const D3 f2 = s0 * sn + (s1 * sdv + s2 * sev);  // sqrt2 f
+      const D3 t2 = cross(fp, f2);                       // sqrt2 t
+      const double tl[7] = {f2.x, f2.y, f2.z, t2.x, t2.y, t2.z, sqrt_rho * s0};
 #pragma unroll
       for (int p = 0; p < 7; ++p) tv[p] = qp_group_sum<MT>(tl[p], base, m);
     }
@@ -343,10 +346,9 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
       }
     }
     const D3 wv = mk(sv[0], sv[1], sv[2]) + cross(mk(sv[3], sv[4], sv[5]), fp);
-    const double nw = dot(fn, wv), dw = dot(fd, wv), ew = dot(fe, wv);
     // (U s)_e = ua + ub cos_e + ue sin_e, so (G s)_e = (U s - betap sum U s)_e / a
     // is ga + gb cos_e + gc sin_e.
-    const double ua = sqrt2 * nw + sqrt_rho * sv[6], ub = sqrt2 * mu * dw, ue = sqrt2 * mu * ew;
+    const double ua = dot(sn, wv) + sqrt_rho * sv[6], ub = dot(sdv, wv), ue = dot(sev, wv);
     const double us_sum = k * ua + ccos * ub + csin * ue;
     const double ga = (ua - betap * us_sum) * inv_a, gb = ub * inv_a, gc = ue * inv_a;
     const double h0 = bb * inv_a + ga;
@@ -403,6 +405,7 @@ __global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
       wf = mk(qp_group_sum<MT>(wf.x, base, m), qp_group_sum<MT>(wf.y, base, m), qp_group_sum<MT>(wf.z, base, m));
       wt = mk(qp_group_sum<MT>(wt.x, base, m), qp_group_sum<MT>(wt.y, base, m), qp_group_sum<MT>(wt.z, base, m));
       const D3 u = wf + cross(wt, fp);
+      const D3 fn = ld3(s.frame + 12 * c + 3), fd = ld3(s.frame + 12 * c + 6), fe = ld3(s.frame + 12 * c + 9);
       const double nu = dot(fn, u), du = dot(fd, u), eu = dot(fe, u);
       double rd = 0.0;
 #pragma unroll
