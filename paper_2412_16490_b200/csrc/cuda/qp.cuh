@@ -45,7 +45,15 @@ __device__ __forceinline__ double relu_bits(double v) {
 // shuffles first, then a pairwise tree when the count is known.
 template <int CNT>
 __device__ __forceinline__ double qp_group_sum(double v, int base, int cnt) {
-  if constexpr (CNT > 0) {
+  if constexpr (CNT == 4 || CNT == 5) {
+    // shift-down partial sums: the group's head lane (base) ends with the
+    // whole sum reading only lanes base..base+CNT-1, then broadcasts it
+    // (CNT = 5: 4 shuffles and 3 adds instead of 5 and 4)
+    const double s1 = v + __shfl_down_sync(kFull, v, 1);
+    double s = s1 + __shfl_down_sync(kFull, s1, 2);
+    if constexpr (CNT == 5) s += __shfl_down_sync(kFull, v, 4);
+    return __shfl_sync(kFull, s, base);
+  } else if constexpr (CNT > 0) {
     double t[CNT];
 #pragma unroll
     for (int b = 0; b < CNT; ++b) t[b] = __shfl_sync(kFull, v, base + b);
