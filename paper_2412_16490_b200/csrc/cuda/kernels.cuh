@@ -1018,7 +1018,10 @@ __device__ __forceinline__ void queue_overflow(const DevState& st, int slot) {
 // Jobs whose slot needed more than kEpaLongPred EPA iterations last time go
 // to a second region (launched first, packed into their own warps): a
 // thread-per-job warp otherwise runs as long as its longest lane.
-constexpr int kEpaLongPred = 6;
+#ifndef GDEV_EPA_LONG_PRED
+#define GDEV_EPA_LONG_PRED 6
+#endif
+constexpr int kEpaLongPred = GDEV_EPA_LONG_PRED;
 __device__ __forceinline__ void write_epa_job(const DevState& st, int slot, const SP (&simp)[4], int ns) {
   const bool long_job = st.epa_hist[slot] > kEpaLongPred;
   const int job = atomicAdd(long_job ? st.epa_long_count : st.epa_count, 1);
