@@ -145,7 +145,7 @@ def roofline(prof, hand, cfg, peak_tflops):
     # DRAM traffic per launch of the dominant kernel from the committed
     # `ncu --set full` capture (profiles/), when one exists for it.
     traffic, traffic_src = None, None
-    cap = {"qp": "profiles/r01_ncu_qp_full_v7.json", "pairs": "profiles/r01_ncu_pairs_list_full_v7.json"}.get(dom)
+    cap = {"qp": "profiles/r01_ncu_qp_full_v10.json", "pairs": "profiles/r01_ncu_pairs_list_full_v7.json"}.get(dom)
     if cap and (ROOT / cap).exists():
         traffic = json.loads((ROOT / cap).read_text()).get("traffic_bytes_per_launch")
         traffic_src = cap + " (dram__bytes_read.sum + dram__bytes_write.sum, bytes per launch)"
