@@ -596,3 +596,42 @@ def test_group_point_queries_bitwise_equal_thread_queries(G, monkeypatch):
         assert np.array_equal(o.x_s, ref.x_s), k
         assert np.array_equal(o.failed, ref.failed), k
         assert np.array_equal(o.contacts, ref.contacts, equal_nan=True), k
+
+
+def test_synthesis_deterministic_and_batch_prefix_independent(G, trident, engine):
+    """test_pipeline.cpp:399-421 on the device: the same start states give bitwise-equal
+    records on a rerun, and a grasp's record does not depend on the batch it is in
+    (a prefix of the batch, and a batch of one)."""
+    obj = G.make_primitive("box", 0.08)
+    use(engine, trident, obj)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 12, 5
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 15, 6, 6
+    x0 = G.init_poses(trident, obj, cfg.batch, cfg.seed, cfg.init)
+    a = engine.synthesize(cfg, x0)
+    b = engine.synthesize(cfg, x0)
+    for f in ("x", "x_p", "x_s", "energy_total", "stage_energy", "failed"):
+        assert np.array_equal(getattr(a, f), getattr(b, f), equal_nan=True), f
+    for k in (5, 1):
+        cfg.batch = k
+        p = engine.synthesize(cfg, np.ascontiguousarray(x0[:k]))
+        for f in ("x", "x_p", "x_s", "energy_total", "failed"):
+            assert np.array_equal(getattr(p, f), getattr(a, f)[:k], equal_nan=True), (k, f)
+
+
+def test_diverging_grasps_are_flagged_on_device(G, O, trident, engine):
+    """test_pipeline.cpp:475-488 on the device: a huge translation step diverges every
+    grasp; each is flagged failed (as the oracle flags it) with finite state and NaN energy."""
+    sphere = G.make_primitive("sphere", 0.1)
+    use(engine, trident, sphere)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 3, 17
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 120, 50, 50
+    cfg.pipeline.coarse.step_translation = 1e5
+    x0 = G.init_poses(trident, sphere, 3, 17, cfg.init)
+    gpu = engine.synthesize(cfg, x0)
+    cpu = O.synthesize(trident, sphere, cfg, x0, workers=3)
+    assert (gpu.failed != 0).all()
+    assert np.array_equal(gpu.failed, cpu.failed)
+    assert np.isfinite(gpu.x).all()
+    assert np.isnan(gpu.energy_total).all()
