@@ -763,7 +763,7 @@ struct grasp_ctx {
         case 8: k_point_query_group<8><<<blocks(n * 8, 128), 128, 0, stream>>>(O, st, sl, per); break;
         case 16: k_point_query_group<16><<<blocks(n * 16, 128), 128, 0, stream>>>(O, st, sl, per); break;
         case 32: k_point_query_group<32><<<blocks(n * 32, 128), 128, 0, stream>>>(O, st, sl, per); break;
-        default: k_point_query<<<blocks(n, 128), 128, 0, stream>>>(O, st, sl, per);
+        default: k_point_query<<<blocks(n, GDEV_PQ_BLOCK), GDEV_PQ_BLOCK, 0, stream>>>(O, st, sl, per);
       }
     });
   }

@@ -96,12 +96,15 @@ struct QpSmem {
 #ifndef GDEV_QP_MIN_BLOCKS
 #define GDEV_QP_MIN_BLOCKS 3  // 168 registers, no spills (measured best since the scaled-dual sweep; 4 and 5 spill)
 #endif
+#ifndef GDEV_QP_WARPS
+#define GDEV_QP_WARPS 4  // grasps (warps) per block; 1 and 2 measured slower (qp 440 / 434 vs 432 ms)
+#endif
 template <int KT, int MT>
-__global__ void __launch_bounds__(128, GDEV_QP_MIN_BLOCKS)
+__global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_MIN_BLOCKS * 4 / GDEV_QP_WARPS)
     k_qp_t(DevHand H, DevParams P, DevState st, int m_rt, int mode, int with_grad) {
-  __shared__ QpSmem smem_all[4];
+  __shared__ QpSmem smem_all[GDEV_QP_WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x * 4 + warp;
+  const int g = blockIdx.x * GDEV_QP_WARPS + warp;
   if (g >= st.G) return;
   if (st.failed[g]) return;
   QpSmem& s = smem_all[warp];
