@@ -758,11 +758,11 @@ struct grasp_ctx {
     const int* sl = tips_only ? h_tip_slots.p : nullptr;
     launch(0, [&] {
       switch (L) {
-        case 2: k_point_query_group<2><<<blocks(n * 2, 128), 128, 0, stream>>>(O, st, sl, per); break;
-        case 4: k_point_query_group<4><<<blocks(n * 4, 128), 128, 0, stream>>>(O, st, sl, per); break;
-        case 8: k_point_query_group<8><<<blocks(n * 8, 128), 128, 0, stream>>>(O, st, sl, per); break;
-        case 16: k_point_query_group<16><<<blocks(n * 16, 128), 128, 0, stream>>>(O, st, sl, per); break;
-        case 32: k_point_query_group<32><<<blocks(n * 32, 128), 128, 0, stream>>>(O, st, sl, per); break;
+        case 2: k_point_query_group<2><<<blocks(n * 2, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, stream>>>(O, st, sl, per); break;
+        case 4: k_point_query_group<4><<<blocks(n * 4, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, stream>>>(O, st, sl, per); break;
+        case 8: k_point_query_group<8><<<blocks(n * 8, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, stream>>>(O, st, sl, per); break;
+        case 16: k_point_query_group<16><<<blocks(n * 16, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, stream>>>(O, st, sl, per); break;
+        case 32: k_point_query_group<32><<<blocks(n * 32, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, stream>>>(O, st, sl, per); break;
         default: k_point_query<<<blocks(n, GDEV_PQ_BLOCK), GDEV_PQ_BLOCK, 0, stream>>>(O, st, sl, per);
       }
     });

@@ -674,7 +674,10 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int warm_face,
 // Group-per-query variant for launches with few queries (the fine and final
 // stages' tip-centre queries, G x m: one query per thread leaves most SMs idle).
 template <int L>
-__global__ void __launch_bounds__(128) k_point_query_group(DevObject O, DevState st, const int* __restrict__ slots,
+#ifndef GDEV_PQG_BLOCK
+#define GDEV_PQG_BLOCK 128  // 64: 270.7 vs 273.4 ms point queries (noise level), 256: 276.5
+#endif
+__global__ void __launch_bounds__(GDEV_PQG_BLOCK) k_point_query_group(DevObject O, DevState st, const int* __restrict__ slots,
                                                            int n_slots) {
   const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / L;
   const int gl = threadIdx.x & (L - 1);

@@ -100,7 +100,10 @@ struct QpSmem {
 #define GDEV_QP_WARPS 4  // grasps (warps) per block; 1 and 2 measured slower (qp 440 / 434 vs 432 ms)
 #endif
 template <int KT, int MT>
-__global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_MIN_BLOCKS * 4 / GDEV_QP_WARPS)
+#ifndef GDEV_QP_RESIDENT_WARPS
+#define GDEV_QP_RESIDENT_WARPS (GDEV_QP_MIN_BLOCKS * 4)
+#endif
+__global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_RESIDENT_WARPS / GDEV_QP_WARPS)
     k_qp_t(DevHand H, DevParams P, DevState st, int m_rt, int mode, int with_grad) {
   __shared__ QpSmem smem_all[GDEV_QP_WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
