@@ -244,6 +244,40 @@ int grasp_ctx_profile(grasp_ctx* ctx, double* ms /*[8]*/, long long* launches /*
                       unsigned long long* ops /*[20]*/);
 /* Kernels launched by this context so far. */
 long long grasp_ctx_launch_count(grasp_ctx* ctx);
+
+/* Per-iteration trace of the next grasp_synthesize* calls (teacher-forced parity:
+ * the reference's run_grasp loop, pipeline.cpp:254-281, restarted from any
+ * recorded state). Snapshot k is taken at iteration iter[k] of stage stage[k]
+ * (0 coarse, 1 fine, 2 final) for every grasp of the batch: the iteration's
+ * inputs before it runs (x_in, the device FK of x_in, the QP warm start and its
+ * ready flag, the anchors) and its outputs after the step (total_energy and its
+ * gradient, the stepped state, the QP snapshot and per-column sweep counts /
+ * convergence flags of that iteration's lower QP, the failure code). Buffers
+ * are HOST memory, snapshot-major ([n_snap][batch][...]), any may be NULL, and
+ * must stay valid until the synthesize call returns. Snapshots of grasps that
+ * failed earlier hold stale values (check `failed`). D = 12 + dof,
+ * n = m * n_edges, M = m + 1 + n. */
+typedef struct grasp_trace {
+  int n_snap;
+  const int* stage;   /* [n_snap] */
+  const int* iter;    /* [n_snap] */
+  double* x_in;       /* [n_snap*batch*D] */
+  double* world_in;   /* [n_snap*batch*n_links*12] R (9, row-major: the device layout), t (3) */
+  double* warm_x_in;  /* [n_snap*batch*n*6] column-major n x 6 */
+  double* warm_y_in;  /* [n_snap*batch*M*6] */
+  int* warm_ready_in; /* [n_snap*batch] */
+  double* anchors;    /* [n_snap*batch*m*3] */
+  double* energy;     /* [n_snap*batch] */
+  double* grad;       /* [n_snap*batch*D] */
+  double* x_out;      /* [n_snap*batch*D] */
+  double* warm_x_out; /* [n_snap*batch*n*6] */
+  double* warm_y_out; /* [n_snap*batch*M*6] */
+  int* qp_iters;      /* [n_snap*batch*6] */
+  int* qp_converged;  /* [n_snap*batch*6] */
+  int* failed;        /* [n_snap*batch] */
+} grasp_trace;
+/* Arms (trace != NULL, copied) or disarms (NULL) the trace. */
+int grasp_ctx_set_trace(grasp_ctx* ctx, const grasp_trace* trace);
 /* Measured dense fp64 FMA throughput of the device (TFLOP/s). */
 int grasp_measure_fp64_peak(int device, double* tflops);
 

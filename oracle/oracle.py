@@ -45,7 +45,9 @@ def lib():
             "oracle_point_to_mesh": (C.c_int, [_vp, C.c_int, _dp, _dp]),
             "oracle_part_pairs": (C.c_int, [_vp, _vp, C.c_int, _ip, _ip, _dp, _dp, C.c_int, _dp]),
             "oracle_signed_distance": (C.c_int, [_vp, _vp, C.c_int, _ip, _ip, _dp, _dp]),
-            "oracle_total_energy": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp]),
+            "oracle_total_energy": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _ip, _dp, _dp,
+                                              _ip, _ip, C.c_int]),
+            "oracle_forward_kinematics": (C.c_int, [_vp, C.c_int, _dp, _dp]),
             "oracle_apply_step": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _dp, _dp]),
             "oracle_coarse_distance_energy": (C.c_int, [_vp, _vp, C.c_int, _dp, C.c_double, C.c_double, _dp, _dp]),
             "oracle_fine_contact_query": (C.c_int, [_vp, _vp, C.c_int, _dp, _dp]),
@@ -108,16 +110,36 @@ def signed_distance(hand, obj, link_ids, part_ids, poses) -> np.ndarray:
     return out
 
 
-def total_energy(hand, obj, cfg, stage, x, anchors=None, warm_x=None, warm_y=None, with_grad=True):
+def total_energy(hand, obj, cfg, stage, x, anchors=None, warm_x=None, warm_y=None, with_grad=True,
+                 warm_ready=None, qp_stats=False, threads=None):
+    """total_energy (pipeline.cpp:96-210) per grasp. warm_x/warm_y (updated in place) are
+    the coarse QP's warm start, used for grasps with warm_ready != 0 (all when None).
+    With qp_stats, also returns the coarse QP's per-column (iters, converged)."""
     x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, hand.dims())
     n = len(x)
     energy = np.zeros(n)
     grad = np.zeros_like(x) if with_grad else None
     anc = None if anchors is None else np.ascontiguousarray(anchors, dtype=np.float64)
+    rdy = None if warm_ready is None else np.ascontiguousarray(warm_ready, dtype=np.int32)
+    its = np.zeros((n, 6), np.int32) if qp_stats else None
+    conv = np.zeros((n, 6), np.int32) if qp_stats else None
+    for a in (warm_x, warm_y):
+        assert a is None or (a.flags.c_contiguous and a.dtype == np.float64)
     p = cfg.to_params()
+    nt = threads if threads is not None else (os.cpu_count() or 1)
     _check(lib().oracle_total_energy(ref(hand.desc), ref(obj.desc), ref(p), stage, n, _d(x), _d(anc), _d(warm_x),
-                                     _d(warm_y), _d(energy), _d(grad)))
+                                     _d(warm_y), _i(rdy), _d(energy), _d(grad), _i(its), _i(conv), int(nt)))
+    if qp_stats:
+        return energy, grad, its, conv
     return energy, grad
+
+
+def forward_kinematics(hand, x) -> np.ndarray:
+    """forward_kinematics(pose_from_state(x)) (hand.cpp:108-153) -> (n, L, 12) world R (column-major), t."""
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, hand.dims())
+    out = np.zeros((len(x), hand.n_links, 12))
+    _check(lib().oracle_forward_kinematics(ref(hand.desc), len(x), _d(x), _d(out)))
+    return out
 
 
 def apply_step(hand, stage_params, it, grad, x):

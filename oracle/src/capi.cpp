@@ -5,6 +5,7 @@
 
 #include "../../include/grasp_b200.h"
 
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -176,6 +177,31 @@ void write_record(const Record& r, int g, int D, int n, int m, grasp_out* out) {
     for (int j = 0; j < 6; ++j) out->qp_converged[6 * g + j] = r.converged.empty() ? 0 : r.converged[j];
 }
 
+// Runs fn(g) for g in [0, n) on `threads` std::threads (strided, like
+// pipeline.cpp:443-455); rethrows the first exception on the caller.
+template <class F>
+void parallel_grasps(int n, int threads, F&& fn) {
+  const int nw = std::max(1, std::min(threads, n));
+  if (nw == 1) {
+    for (int g = 0; g < n; ++g) fn(g);
+    return;
+  }
+  std::mutex mu;
+  std::exception_ptr first;
+  std::vector<std::thread> pool;
+  for (int w = 0; w < nw; ++w)
+    pool.emplace_back([&, w] {
+      try {
+        for (int g = w; g < n; g += nw) fn(g);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!first) first = std::current_exception();
+      }
+    });
+  for (auto& t : pool) t.join();
+  if (first) std::rethrow_exception(first);
+}
+
 }  // namespace
 
 extern "C" {
@@ -241,21 +267,27 @@ int oracle_signed_distance(const grasp_hand_desc* hd, const grasp_object_desc* o
   });
 }
 
+// total_energy (pipeline.cpp:96-210) per grasp, grasps spread over `threads`
+// std::threads. warm_ready[g] (NULL = all) selects which grasps start the
+// coarse QP from warm_x/warm_y; those are updated in place like the
+// reference's QpScratch. qp_iters/qp_conv receive the coarse QP's per-column
+// sweep counts and convergence flags.
 int oracle_total_energy(const grasp_hand_desc* hd, const grasp_object_desc* od, const grasp_run_params* p, int stage,
-                        int n, const double* x, const double* anchors, double* warm_x, double* warm_y, double* energy,
-                        double* grad) {
+                        int n, const double* x, const double* anchors, double* warm_x, double* warm_y,
+                        const int* warm_ready, double* energy, double* grad, int* qp_iters, int* qp_conv,
+                        int threads) {
   return guarded([&] {
     const Hand h = make_hand(hd);
     const Object obj = make_object(od);
     const Config cfg = make_config(p);
     const int D = h.dims(), m = static_cast<int>(h.tips.size()), nv = m * cfg.n_edges, M = m + 1 + nv;
-    for (int g = 0; g < n; ++g) {
+    auto one = [&](int g) {
       VecX xv(x + static_cast<size_t>(g) * D, x + static_cast<size_t>(g + 1) * D);
       std::vector<V3> anc;
       if (anchors)
         for (int f = 0; f < m; ++f) anc.push_back(v3(anchors + (static_cast<size_t>(g) * m + f) * 3));
       QpScratch scratch;
-      if (warm_x && warm_y) {
+      if (warm_x && warm_y && (!warm_ready || warm_ready[g])) {
         scratch.forces = MatX(nv, 6);
         scratch.duals = MatX(M, 6);
         std::memcpy(scratch.forces.d.data(), warm_x + static_cast<size_t>(g) * nv * 6, sizeof(double) * nv * 6);
@@ -265,9 +297,33 @@ int oracle_total_energy(const grasp_hand_desc* hd, const grasp_object_desc* od, 
       VecX gr;
       energy[g] = total_energy(h, obj, cfg, stage, anc, xv, scratch, grad ? &gr : nullptr);
       if (grad) std::memcpy(grad + static_cast<size_t>(g) * D, gr.data(), sizeof(double) * D);
+      if (stage == 0)
+        for (int j = 0; j < 6; ++j) {
+          if (qp_iters) qp_iters[6 * g + j] = scratch.iters[j];
+          if (qp_conv) qp_conv[6 * g + j] = scratch.converged[j];
+        }
       if (warm_x && warm_y && stage == 0) {
         std::memcpy(warm_x + static_cast<size_t>(g) * nv * 6, scratch.forces.d.data(), sizeof(double) * nv * 6);
         std::memcpy(warm_y + static_cast<size_t>(g) * M * 6, scratch.duals.d.data(), sizeof(double) * M * 6);
+      }
+    };
+    parallel_grasps(n, threads, one);
+  });
+}
+
+// forward_kinematics(pose_from_state(x)) (hand.cpp:108-153): out[n*L*12] world R (column-major) t.
+int oracle_forward_kinematics(const grasp_hand_desc* hd, int n, const double* x, double* out) {
+  return guarded([&] {
+    const Hand h = make_hand(hd);
+    const int D = h.dims(), L = static_cast<int>(h.links.size());
+    for (int g = 0; g < n; ++g) {
+      VecX xv(x + static_cast<size_t>(g) * D, x + static_cast<size_t>(g + 1) * D);
+      const Fk fk = forward_kinematics(h, pose_from_state(h, xv));
+      for (int l = 0; l < L; ++l) {
+        double* o = out + (static_cast<size_t>(g) * L + l) * 12;
+        for (int c = 0; c < 3; ++c)
+          for (int i = 0; i < 3; ++i) o[3 * c + i] = fk.world[l].R(i, c);
+        for (int i = 0; i < 3; ++i) o[9 + i] = fk.world[l].t[i];
       }
     }
   });

@@ -137,6 +137,7 @@ struct EnergyReport {
   VecX per_direction;
   MatX forces, residuals, duals;
   std::vector<char> converged;
+  std::vector<int> iters;  // per-column sweep count at the freeze (qpsolve.cpp:99-117)
 };
 MatX closure_directions();
 EnergyReport grasp_energy(const std::vector<Frame>& frames, double beta, double gamma_per_contact, double mu, int k,
@@ -192,6 +193,8 @@ EvalResult quasi_static_check(const Hand& h, const Object& obj, const Config& cf
 struct QpScratch {
   MatX forces, duals;
   bool ready = false;
+  std::vector<int> iters;        // last solve's per-column sweep counts (instrumentation)
+  std::vector<char> converged;
 };
 // stage: 0 coarse, 1 fine, 2 final
 double total_energy(const Hand& h, const Object& obj, const Config& cfg, int stage, const std::vector<V3>& anchors,

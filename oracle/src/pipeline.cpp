@@ -170,6 +170,8 @@ double total_energy(const Hand& h, const Object& obj, const Config& cfg, int sta
     scratch.forces = rep.forces;
     scratch.duals = rep.duals;
     scratch.ready = true;
+    scratch.iters = rep.iters;
+    scratch.converged = rep.converged;
     total += cfg.w_grasp * rep.total;
     if (grad) add_scaled(*grad, grasp_energy_gradient(frames, rep, cfg.mu, cfg.n_edges, jac_p, jac_n), cfg.w_grasp);
   } else {

@@ -481,6 +481,7 @@ EnergyReport grasp_energy(const std::vector<Frame>& frames, double beta, double 
   rep.forces = sol.X;
   rep.duals = sol.Y;
   rep.converged = sol.converged;
+  rep.iters = sol.iters;
   rep.residuals = MatX(6, 6);
   rep.per_direction.assign(6, 0.0);
   for (int j = 0; j < 6; ++j) {

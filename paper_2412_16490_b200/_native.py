@@ -80,6 +80,13 @@ class Out(C.Structure):
                 ("qp_converged", _ip)]
 
 
+class Trace(C.Structure):
+    _fields_ = [("n_snap", C.c_int), ("stage", _ip), ("iter", _ip), ("x_in", _dp), ("world_in", _dp),
+                ("warm_x_in", _dp), ("warm_y_in", _dp), ("warm_ready_in", _ip), ("anchors", _dp),
+                ("energy", _dp), ("grad", _dp), ("x_out", _dp), ("warm_x_out", _dp), ("warm_y_out", _dp),
+                ("qp_iters", _ip), ("qp_converged", _ip), ("failed", _ip)]
+
+
 # Every symbol include/grasp_b200.h declares, with its ctypes signature.
 SIGNATURES = {
     "grasp_last_error": (C.c_char_p, []),
@@ -121,6 +128,7 @@ SIGNATURES = {
     "grasp_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "grasp_ctx_profile": (C.c_int, [C.c_void_p, _dp, C.POINTER(C.c_longlong), C.POINTER(C.c_ulonglong)]),
     "grasp_ctx_launch_count": (C.c_longlong, [C.c_void_p]),
+    "grasp_ctx_set_trace": (C.c_int, [C.c_void_p, C.POINTER(Trace)]),
     "grasp_measure_fp64_peak": (C.c_int, [C.c_int, _dp]),
 }
 

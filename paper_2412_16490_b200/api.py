@@ -454,6 +454,37 @@ class Engine:
         N.check(N.lib().grasp_synthesize(self._ctx, C.byref(cfg.to_params()), batch, dptr(x0), C.byref(s)))
         return out
 
+    def synthesize_traced(self, cfg: RunConfig, x0: np.ndarray, snaps) -> tuple:
+        """synthesize with a per-iteration trace (grasp_ctx_set_trace): snaps is a list of
+        (stage, iter); returns (SynthesisOutput, dict of snapshot-major arrays)."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        B, D, m, L = x0.shape[0], self.hand.dims(), self.hand.n_tips, self.hand.n_links
+        nv = m * cfg.contact.n_edges
+        M = m + 1 + nv
+        S = len(snaps)
+        stage = np.array([s for s, _ in snaps], dtype=np.int32)
+        it = np.array([i for _, i in snaps], dtype=np.int32)
+        t = dict(x_in=np.zeros((S, B, D)), world_in=np.zeros((S, B, L, 12)), warm_x_in=np.zeros((S, B, 6, nv)),
+                 warm_y_in=np.zeros((S, B, 6, M)), warm_ready_in=np.zeros((S, B), np.int32),
+                 anchors=np.zeros((S, B, m, 3)), energy=np.zeros((S, B)), grad=np.zeros((S, B, D)),
+                 x_out=np.zeros((S, B, D)), warm_x_out=np.zeros((S, B, 6, nv)), warm_y_out=np.zeros((S, B, 6, M)),
+                 qp_iters=np.zeros((S, B, 6), np.int32), qp_converged=np.zeros((S, B, 6), np.int32),
+                 failed=np.zeros((S, B), np.int32))
+        ptr = {k: (iptr(v) if v.dtype == np.int32 else dptr(v)) for k, v in t.items()}
+        spec = N.Trace(S, iptr(stage), iptr(it), ptr["x_in"], ptr["world_in"], ptr["warm_x_in"], ptr["warm_y_in"],
+                       ptr["warm_ready_in"], ptr["anchors"], ptr["energy"], ptr["grad"], ptr["x_out"],
+                       ptr["warm_x_out"], ptr["warm_y_out"], ptr["qp_iters"], ptr["qp_converged"], ptr["failed"])
+        N.check(N.lib().grasp_ctx_set_trace(self._ctx, C.byref(spec)))
+        try:
+            out = self.synthesize(cfg, x0)
+        finally:
+            N.check(N.lib().grasp_ctx_set_trace(self._ctx, None))
+        # device link transforms store R row-major; report column-major like forward_kinematics
+        w = t["world_in"]
+        w[..., :9] = w[..., :9].reshape(w.shape[:-1] + (3, 3)).swapaxes(-1, -2).reshape(w.shape[:-1] + (9,))
+        t["stage"], t["iter"] = stage, it
+        return out, t
+
     def synthesize_device(self, cfg: RunConfig, x0_ptr: int, batch: int, out_ptrs: dict) -> None:
         """grasp_synthesize_device: x0 and outputs are device pointers (ints)."""
         vp = lambda k: C.cast(C.c_void_p(out_ptrs[k]), _dp) if out_ptrs.get(k) else None

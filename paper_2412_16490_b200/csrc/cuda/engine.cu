@@ -185,6 +185,89 @@ struct grasp_ctx {
     pending.push_back({cls, {a, b}});
   }
 
+  // Per-iteration trace (grasp_ctx_set_trace): device staging, copied to the
+  // caller's host buffers at the end of run().
+  bool tracing = false;
+  grasp_trace trace{};
+  std::vector<int> trace_stage, trace_iter;
+  DevBuf<double> t_x_in, t_world_in, t_wx_in, t_wy_in, t_anchors, t_energy, t_grad, t_x_out, t_wx_out, t_wy_out;
+  DevBuf<int> t_ready_in, t_iters, t_conv, t_failed;
+
+  int trace_slot(int stage, int it) const {
+    if (!tracing) return -1;
+    for (size_t k = 0; k < trace_stage.size(); ++k)
+      if (trace_stage[k] == stage && trace_iter[k] == it) return static_cast<int>(k);
+    return -1;
+  }
+  template <class T>
+  void snap(DevBuf<T>& dst, const T* host_dst, const T* src, int slot, size_t per_grasp) {
+    if (!host_dst) return;
+    const size_t n = static_cast<size_t>(st.G) * per_grasp;
+    ck(cudaMemcpyAsync(dst.p + slot * n, src, n * sizeof(T), cudaMemcpyDeviceToDevice, stream), "trace copy");
+  }
+  template <class T>
+  void presize(DevBuf<T>& dst, const T* host_dst, size_t per_grasp) {
+    if (host_dst) dst.ensure(static_cast<size_t>(st.G) * per_grasp * trace_stage.size());
+  }
+  // Sizes the staging buffers before the run (DevBuf::ensure reallocates).
+  void trace_prepare(int nv, int M) {
+    presize(t_x_in, trace.x_in, H.D);
+    presize(t_world_in, trace.world_in, static_cast<size_t>(H.L) * 12);
+    presize(t_wx_in, trace.warm_x_in, static_cast<size_t>(nv) * 6);
+    presize(t_wy_in, trace.warm_y_in, static_cast<size_t>(M) * 6);
+    presize(t_ready_in, trace.warm_ready_in, 1);
+    presize(t_anchors, trace.anchors, static_cast<size_t>(H.m) * 3);
+    presize(t_energy, trace.energy, 1);
+    presize(t_grad, trace.grad, H.D);
+    presize(t_x_out, trace.x_out, H.D);
+    presize(t_wx_out, trace.warm_x_out, static_cast<size_t>(nv) * 6);
+    presize(t_wy_out, trace.warm_y_out, static_cast<size_t>(M) * 6);
+    presize(t_iters, trace.qp_iters, 6);
+    presize(t_conv, trace.qp_converged, 6);
+    presize(t_failed, trace.failed, 1);
+  }
+  void trace_before(int slot, int nv, int M) {
+    snap(t_x_in, trace.x_in, st.x, slot, H.D);
+    snap(t_world_in, trace.world_in, st.world, slot, static_cast<size_t>(H.L) * 12);
+    snap(t_wx_in, trace.warm_x_in, st.warm_x, slot, static_cast<size_t>(nv) * 6);
+    snap(t_wy_in, trace.warm_y_in, st.warm_y, slot, static_cast<size_t>(M) * 6);
+    snap(t_ready_in, trace.warm_ready_in, st.qp_ready, slot, 1);
+    snap(t_anchors, trace.anchors, st.anchors, slot, static_cast<size_t>(H.m) * 3);
+  }
+  void trace_after(int slot, int nv, int M) {
+    snap(t_energy, trace.energy, st.energy, slot, 1);
+    snap(t_grad, trace.grad, st.grad, slot, H.D);
+    snap(t_x_out, trace.x_out, st.x, slot, H.D);
+    snap(t_wx_out, trace.warm_x_out, st.warm_x, slot, static_cast<size_t>(nv) * 6);
+    snap(t_wy_out, trace.warm_y_out, st.warm_y, slot, static_cast<size_t>(M) * 6);
+    snap(t_iters, trace.qp_iters, st.qp_iters, slot, 6);
+    snap(t_conv, trace.qp_converged, st.qp_conv, slot, 6);
+    snap(t_failed, trace.failed, st.failed, slot, 1);
+  }
+  template <class T>
+  void unsnap(T* host_dst, const DevBuf<T>& src, size_t per_grasp) {
+    if (!host_dst) return;
+    const size_t n = static_cast<size_t>(st.G) * per_grasp * trace_stage.size();
+    ck(cudaMemcpyAsync(host_dst, src.p, n * sizeof(T), cudaMemcpyDeviceToHost, stream), "trace out");
+  }
+  void trace_flush(int nv, int M) {
+    unsnap(trace.x_in, t_x_in, H.D);
+    unsnap(trace.world_in, t_world_in, static_cast<size_t>(H.L) * 12);
+    unsnap(trace.warm_x_in, t_wx_in, static_cast<size_t>(nv) * 6);
+    unsnap(trace.warm_y_in, t_wy_in, static_cast<size_t>(M) * 6);
+    unsnap(trace.warm_ready_in, t_ready_in, 1);
+    unsnap(trace.anchors, t_anchors, static_cast<size_t>(H.m) * 3);
+    unsnap(trace.energy, t_energy, 1);
+    unsnap(trace.grad, t_grad, H.D);
+    unsnap(trace.x_out, t_x_out, H.D);
+    unsnap(trace.warm_x_out, t_wx_out, static_cast<size_t>(nv) * 6);
+    unsnap(trace.warm_y_out, t_wy_out, static_cast<size_t>(M) * 6);
+    unsnap(trace.qp_iters, t_iters, 6);
+    unsnap(trace.qp_converged, t_conv, 6);
+    unsnap(trace.failed, t_failed, 1);
+    ck(cudaStreamSynchronize(stream), "trace sync");
+  }
+
   void collect_profile() {
     if (pending.empty()) return;
     ck(cudaStreamSynchronize(stream), "sync");
@@ -822,11 +905,15 @@ struct grasp_ctx {
     const grasp_stage_params* scheds[3] = {&p->coarse, &p->fine, &p->final_stage};
     const double offsets[3] = {p->contact_offset, p->contact_offset, 0.0};
     const int n_stages = p->skip_fine_stages ? 1 : 3;
+    const int nv = H.m * p->n_edges, Mq = H.m + 1 + nv;
+    if (tracing) trace_prepare(nv, Mq);
     for (int s = 0; s < n_stages; ++s) {
       const bool coarse = s == 0;
       launch_fk(P);
       for (int it = 0; it < scheds[s]->iters; ++it) {
         const StageArgs A = stage_args(s, *scheds[s], offsets[s], it, 0);
+        const int slot = trace_slot(s, it);
+        if (slot >= 0) trace_before(slot, nv, Mq);
         if (coarse) {
           launch_queries(false);
           launch_qp(P, H.m, 0, 1);
@@ -835,6 +922,7 @@ struct grasp_ctx {
           launch_pairs(false);
         }
         launch_step(P, A, coarse);
+        if (slot >= 0) trace_after(slot, nv, Mq);
       }
       // Stage-end energy (pipeline.cpp:279-280); in the coarse stage this
       // also solves the QP and refreshes the warm start.
@@ -862,6 +950,7 @@ struct grasp_ctx {
     launch(6, [&] { k_squeeze<<<blocks(st.G, 128), 128, 0, stream>>>(H, st, x_s.p); });
     ck(cudaGetLastError(), "kernel launch");
     collect_profile();
+    if (tracing) trace_flush(nv, Mq);
   }
 };
 
@@ -1457,6 +1546,27 @@ int grasp_ctx_profile(grasp_ctx* ctx, double* ms, long long* launches, unsigned 
     if (ops) {
       ck(cudaMemcpy(ops, ctx->ops.p, sizeof(unsigned long long) * kNumOps, cudaMemcpyDeviceToHost), "ops");
     }
+  });
+}
+
+int grasp_ctx_set_trace(grasp_ctx* ctx, const grasp_trace* t) {
+  return guard([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    ctx->tracing = false;
+    ctx->trace = grasp_trace{};
+    ctx->trace_stage.clear();
+    ctx->trace_iter.clear();
+    if (!t) return;
+    if (t->n_snap < 0 || (t->n_snap > 0 && (!t->stage || !t->iter))) throw std::invalid_argument("bad trace spec");
+    for (int k = 0; k < t->n_snap; ++k) {
+      if (t->stage[k] < 0 || t->stage[k] > 2 || t->iter[k] < 0) throw std::invalid_argument("bad trace snapshot");
+      for (int q = 0; q < k; ++q)
+        if (t->stage[q] == t->stage[k] && t->iter[q] == t->iter[k]) throw std::invalid_argument("duplicate snapshot");
+    }
+    ctx->trace = *t;
+    ctx->trace_stage.assign(t->stage, t->stage + t->n_snap);
+    ctx->trace_iter.assign(t->iter, t->iter + t->n_snap);
+    ctx->tracing = t->n_snap > 0;
   });
 }
 

@@ -21,15 +21,36 @@ struct CtxDeleter {
   void operator()(grasp_ctx* c) const { grasp_ctx_destroy(c); }
 };
 
-// One device context per (thread, device); models are re-uploaded only when
-// the caller passes different model objects.
+// One device context per (thread, device). The packed copy of the models last
+// uploaded is kept, and a model is re-uploaded whenever its packed content
+// differs: a new model at a recycled address, or one changed in place, is
+// never served from the previous upload (packing is a few vector copies,
+// nothing next to a synthesis run).
 struct CachedCtx {
   std::unique_ptr<grasp_ctx, CtxDeleter> ctx;
-  const hand::HandModel* hand = nullptr;
-  const object::ObjectModel* object = nullptr;
+  bool has_hand = false, has_object = false;
   capi::PackedHand packed_hand;
   capi::PackedObject packed_object;
 };
+
+bool same_content(const capi::PackedHand& a, const capi::PackedHand& b) {
+  return a.link_parent_joint == b.link_parent_joint && a.link_tip_proxy == b.link_tip_proxy &&
+         a.link_vert_begin == b.link_vert_begin && a.link_face_begin == b.link_face_begin &&
+         a.link_proxy_begin == b.link_proxy_begin && a.verts == b.verts && a.faces == b.faces &&
+         a.link_obb == b.link_obb && a.link_centroid == b.link_centroid && a.link_volume == b.link_volume &&
+         a.proxies == b.proxies && a.joint_parent_link == b.joint_parent_link &&
+         a.joint_child_link == b.joint_child_link && a.joint_origin == b.joint_origin &&
+         a.joint_axis == b.joint_axis && a.joint_lower == b.joint_lower && a.joint_upper == b.joint_upper &&
+         a.tip_links == b.tip_links && a.collision_pairs == b.collision_pairs;
+}
+
+bool same_content(const capi::PackedObject& a, const capi::PackedObject& b) {
+  return a.part_vert_begin == b.part_vert_begin && a.part_face_begin == b.part_face_begin && a.verts == b.verts &&
+         a.faces == b.faces && a.part_obb == b.part_obb && a.part_centroid == b.part_centroid &&
+         a.part_volume == b.part_volume && a.source == b.source && a.desc.scale == b.desc.scale &&
+         a.desc.bbox_diagonal == b.desc.bbox_diagonal && a.desc.mass_center[0] == b.desc.mass_center[0] &&
+         a.desc.mass_center[1] == b.desc.mass_center[1] && a.desc.mass_center[2] == b.desc.mass_center[2];
+}
 
 void check(int status) {
   if (status == GRASP_OK) return;
@@ -58,16 +79,20 @@ CachedCtx& context_for(int device) {
 
 CachedCtx& bound_context(const hand::HandModel& model, const object::ObjectModel& object, int device) {
   CachedCtx& c = context_for(device);
-  if (c.hand != &model) {
-    c.packed_hand = capi::pack_hand(model);
+  capi::PackedHand ph = capi::pack_hand(model);
+  if (!c.has_hand || !same_content(ph, c.packed_hand)) {
+    c.has_hand = false;
+    c.packed_hand = std::move(ph);  // vector buffers (and the desc's pointers into them) move along
     check(grasp_ctx_set_hand(c.ctx.get(), &c.packed_hand.desc));
-    c.hand = &model;
+    c.has_hand = true;
   }
-  if (c.object != &object) {
-    c.packed_object = capi::pack_object(object);
-    c.packed_object.desc.source = c.packed_object.source.c_str();
+  capi::PackedObject po = capi::pack_object(object);
+  if (!c.has_object || !same_content(po, c.packed_object)) {
+    c.has_object = false;
+    c.packed_object = std::move(po);
+    c.packed_object.desc.source = c.packed_object.source.c_str();  // SSO strings do not move their buffer
     check(grasp_ctx_set_object(c.ctx.get(), &c.packed_object.desc));
-    c.object = &object;
+    c.has_object = true;
   }
   return c;
 }

@@ -248,18 +248,67 @@ def test_signed_distance_late_stage_matches_oracle(G, O, engine):
 
 # ---------------------------------------------------------------------- QP
 @pytest.mark.parametrize("m", [3, 4, 5])
-def test_qp_batch_matches_oracle(G, O, engine, m):
+def test_qp_batch_cold_capped_matches_oracle(G, O, engine, m):
+    """Cold starts from test_energy.cpp:82-91-style frames: at beta = 10 none of these columns
+    reaches the 1e-5 tolerance within 500 sweeps (the oracle agrees), so this pins the
+    capped path: every column reports 500 sweeps, unconverged, and the same iterate."""
     cfg = G.RunConfig()
     rng = np.random.default_rng(100 + m)
     frames = random_frames(rng, 200, m)
     ref = O.qp_batch(cfg, frames, m)
     got = gpu_qp(engine, cfg, frames, m)
-    same = (got["iters"] == ref["iters"])
-    assert same.mean() > 0.97, f"iteration counts agree on {same.mean():.3f}"
-    assert (got["converged"] == ref["converged"]).mean() > 0.97
-    rows = same.all(axis=1)
-    np.testing.assert_allclose(got["X"][rows], ref["X"][rows], atol=1e-7)
-    np.testing.assert_allclose(got["per_direction"][rows], ref["per_direction"][rows], rtol=1e-7, atol=1e-9)
+    assert (ref["iters"] == 500).all() and not ref["converged"].any()
+    assert np.array_equal(got["iters"], ref["iters"]) and np.array_equal(got["converged"], ref["converged"])
+    np.testing.assert_allclose(got["X"], ref["X"], atol=1e-7)
+    np.testing.assert_allclose(got["per_direction"], ref["per_direction"], rtol=1e-7, atol=1e-9)
+
+
+def warm_qp_batch(G, O, m, g, pert, seed):
+    """Contacts on spheres of radius 3-12 cm with noisy inward normals, warm-started from a
+    long (20k-sweep) cold solve of the unperturbed frames, then solved at default settings on
+    frames moved by `pert` m: the columns freeze at every check sweep from 10 to 500
+    (qpsolve.cpp:99-117), like the pipeline's warm-started coarse QPs."""
+    rng = np.random.default_rng(seed)
+    fr = np.zeros((g, m, 12))
+    for i in range(g):
+        r = rng.uniform(0.03, 0.12)
+        for c in range(m):
+            u = rng.normal(size=3)
+            u /= np.linalg.norm(u)
+            n = -u + rng.normal(size=3) * rng.uniform(0, 0.3)
+            n /= np.linalg.norm(n)
+            seed_v = np.array([0.0, 1.0, 0.0]) if abs(n[0]) > 0.99 else np.array([1.0, 0.0, 0.0])
+            d = np.cross(n, seed_v)
+            d /= np.linalg.norm(d)
+            fr[i, c] = np.concatenate([r * u, n, d, np.cross(n, d)])
+    long = G.RunConfig()
+    long.qp.max_iters = 20000
+    base = O.qp_batch(long, fr, m, threads=8)
+    fr2 = fr.copy()
+    fr2[:, :, 0:3] += rng.normal(size=fr2[:, :, 0:3].shape) * pert
+    return fr2, np.ascontiguousarray(base["X"]), np.ascontiguousarray(base["Y"])
+
+
+@pytest.mark.parametrize("m,pert", [(3, 1e-3), (4, 1e-3), (5, 1e-3), (4, 1e-2), (5, 1e-2)])
+def test_qp_warm_freeze_semantics_match_oracle(G, O, engine, m, pert):
+    """Discriminating QP parity: columns converge at different check sweeps, so the per-column
+    freeze and snapshot (qpsolve.cpp:99-117) are compared, not just the 500-sweep cap. Sweep
+    counts and convergence flags must be identical on every column; forces and duals agree to
+    rounding (Woodbury sweep vs the reference's dense LLT)."""
+    cfg = G.RunConfig()
+    fr, wx, wy = warm_qp_batch(G, O, m, 300, pert, 7 + m)
+    ref = O.qp_batch(cfg, fr, m, warm_x=wx.copy(), warm_y=wy.copy(), threads=8)
+    got = gpu_qp(engine, cfg, fr, m, warm_x=wx.copy(), warm_y=wy.copy())
+    its = ref["iters"].ravel()
+    assert len(np.unique(its)) >= 10, "freeze sweeps not spread"
+    assert ref["converged"].mean() >= 0.8
+    mism = got["iters"] != ref["iters"]
+    assert not mism.any(), (f"{mism.sum()} / {mism.size} columns froze at a different sweep",
+                            got["iters"][mism][:8], ref["iters"][mism][:8])
+    assert np.array_equal(got["converged"], ref["converged"])
+    np.testing.assert_allclose(got["X"], ref["X"], atol=1e-7, rtol=0)
+    np.testing.assert_allclose(got["Y"], ref["Y"], atol=1e-7, rtol=0)
+    np.testing.assert_allclose(got["per_direction"], ref["per_direction"], rtol=1e-7, atol=1e-9)
 
 
 # ------------------------------------------------------ teacher-forced energy

@@ -1,0 +1,157 @@
+"""Teacher-forced per-iteration parity along real GPU trajectories (SURVEY.md 8(d) parity row).
+
+The production engine runs the full 300/100/100 schedule on the BASELINE configs and records,
+at selected iterations of every stage, each grasp's inputs (x, device FK, QP warm start,
+anchors) and outputs (total_energy, gradient, stepped x, QP snapshot and sweep counts)
+through grasp_ctx_set_trace. Every snapshot is then restarted on the CPU oracle
+(oracle/src/pipeline.cpp, restating pipeline.cpp:96-231) from exactly the recorded inputs:
+
+  * FK of x_in (hand.cpp:126-153)                       <= 1e-6 m (8(d)); measured ~1e-16
+  * total_energy (pipeline.cpp:96-210)                  <= 1e-4 relative (8(d))
+  * gradient (max-norm relative per grasp)              <= 1e-4 (8(d))
+  * coarse QP forces lambda (energy.cpp:60-92)          <= 1e-4 abs (8(d)); sweep counts reported
+  * apply_step (pipeline.cpp:214-231) from the GPU's own gradient  <= 1e-6 (8(d))
+  * apply_step from the oracle's gradient vs the GPU's stepped x   <= 1e-6
+
+A per-snapshot summary is written to $GRASP_PARITY_OUT (default gpurun_out/) so the measured
+agreement can be committed under profiles/.
+"""
+import json
+import os
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import use
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+COARSE = (0, 1, 2, 5, 10, 20, 40, 70, 100, 150, 200, 250, 298, 299)
+MESH = (0, 1, 2, 10, 30, 60, 98, 99)
+SNAPS = [(0, i) for i in COARSE] + [(1, i) for i in MESH] + [(2, i) for i in MESH]
+
+TOL = dict(fk=1e-6, energy=1e-4, grad=1e-4, lam=1e-4, step=1e-6)
+
+
+def _stage_params(cfg, s):
+    return (cfg.pipeline.coarse, cfg.pipeline.fine, cfg.pipeline.final_stage)[s]
+
+
+def run_trajectory_parity(G, O, engine, hand, obj, batch, seed, name):
+    use(engine, hand, obj)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = batch, seed
+    x0 = G.init_poses(hand, obj, batch, seed, cfg.init)
+    out, T = engine.synthesize_traced(cfg, x0, SNAPS)
+    # The traced run is the production run: same records as an untraced one.
+    plain = engine.synthesize(cfg, x0)
+    assert np.array_equal(plain.x, out.x) and np.array_equal(plain.failed, out.failed)
+
+    rows, worst = [], {k: 0.0 for k in TOL}
+    qp_cols = qp_same = 0
+    for k, (s, it) in enumerate(SNAPS):
+        live = T["failed"][k] == 0
+        if not live.any():
+            continue
+        x_in = T["x_in"][k][live]
+        # FK on the device vs the oracle's Eigen-restated chain
+        fk_ref = O.forward_kinematics(hand, x_in)
+        fk_err = np.abs(T["world_in"][k][live] - fk_ref).max()
+        # energy / gradient / QP from the recorded inputs
+        anchors = T["anchors"][k][live] if s > 0 else None
+        if s == 0:
+            wx = np.ascontiguousarray(T["warm_x_in"][k][live])
+            wy = np.ascontiguousarray(T["warm_y_in"][k][live])
+            e_ref, g_ref, its, conv = O.total_energy(hand, obj, cfg, 0, x_in, warm_x=wx, warm_y=wy,
+                                                     warm_ready=T["warm_ready_in"][k][live], qp_stats=True)
+            lam_err = np.abs(wx - T["warm_x_out"][k][live]).max()
+            same = its == T["qp_iters"][k][live]
+            qp_cols += same.size
+            qp_same += int(same.sum())
+            iters_match = float(same.mean())
+            conv_match = float((conv == T["qp_converged"][k][live]).mean())
+            mean_sweeps = float(its.mean())
+        else:
+            e_ref, g_ref = O.total_energy(hand, obj, cfg, s, x_in, anchors=anchors)
+            lam_err, iters_match, conv_match, mean_sweeps = 0.0, None, None, None
+        e_got, g_got = T["energy"][k][live], T["grad"][k][live]
+        e_err = (np.abs(e_got - e_ref) / np.maximum(np.abs(e_ref), 1e-300)).max()
+        gscale = np.maximum(np.abs(g_ref).max(axis=1), 1e-300)
+        g_err_rows = np.abs(g_got - g_ref).max(axis=1) / gscale
+        sp = _stage_params(cfg, s)
+        x_own = O.apply_step(hand, sp, it, g_got, x_in)
+        x_ref = O.apply_step(hand, sp, it, g_ref, x_in)
+        step_err = np.abs(x_own - T["x_out"][k][live]).max()
+        traj_err = np.abs(x_ref - T["x_out"][k][live]).max()
+        row = dict(stage=s, iter=it, grasps=int(live.sum()), fk=float(fk_err), energy=float(e_err),
+                   grad=float(g_err_rows.max()), grad_p99=float(np.quantile(g_err_rows, 0.99)),
+                   lam=float(lam_err), step=float(step_err), step_from_oracle_grad=float(traj_err),
+                   qp_iters_match=iters_match, qp_conv_match=conv_match, qp_mean_sweeps=mean_sweeps)
+        rows.append(row)
+        worst["fk"] = max(worst["fk"], fk_err)
+        worst["energy"] = max(worst["energy"], e_err)
+        worst["grad"] = max(worst["grad"], g_err_rows.max())
+        worst["lam"] = max(worst["lam"], lam_err)
+        worst["step"] = max(worst["step"], step_err, traj_err)
+    summary = dict(config=name, batch=batch, seed=seed, snapshots=rows, worst={k: float(v) for k, v in worst.items()},
+                   tolerance=TOL, qp_columns=qp_cols, qp_iters_identical=qp_same,
+                   failed=int((out.failed != 0).sum()))
+    dst = Path(os.environ.get("GRASP_PARITY_OUT", ROOT / "gpurun_out"))
+    dst.mkdir(parents=True, exist_ok=True)
+    (dst / f"trajectory_parity_{name}.json").write_text(json.dumps(summary, indent=1))
+    print(json.dumps(dict(config=name, worst=summary["worst"], qp_iters_identical=f"{qp_same}/{qp_cols}")))
+    assert len(rows) == len(SNAPS), "a stage was skipped (all grasps failed?)"
+    for key, tol in TOL.items():
+        assert worst[key] <= tol, (key, worst[key], [r for r in rows if r[key] > tol][:3])
+    return out, summary
+
+
+def test_trajectory_parity_config2_shadow_drill(G, O, engine):
+    """BASELINE config 2 (the benchmarked workload): Shadow-like hand, 6-part drill mesh at 0.10."""
+    hand = G.HandModel.from_file(ROOT / "paper_2412_16490_b200/assets/hands/shadow_like.json")
+    obj = G.load_object(ROOT / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+    run_trajectory_parity(G, O, engine, hand, obj, 64, 17, "config2_shadow_drill")
+
+
+@pytest.mark.parametrize("shape", ["sphere", "box"])
+def test_trajectory_parity_config1_allegro(G, O, engine, shape):
+    """BASELINE config 1: Allegro-like hand, primitive at 0.08, batch 64, seed 17."""
+    hand = G.HandModel.from_file(ROOT / "paper_2412_16490_b200/assets/hands/allegro_like.json")
+    obj = G.make_primitive(shape, 0.08)
+    run_trajectory_parity(G, O, engine, hand, obj, 64, 17, f"config1_allegro_{shape}")
+
+
+def test_config2_end_to_end_matches_oracle(G, O, engine):
+    """End-to-end on the benchmarked config: GPU synthesize vs the oracle's run_grasp on the same
+    x0 (64 grasps, full schedule). Failure flags identical; final energy, stage energies and
+    evaluation statistics (eval.cpp:91-158, each side with its own evaluator) agree."""
+    hand = G.HandModel.from_file(ROOT / "paper_2412_16490_b200/assets/hands/shadow_like.json")
+    obj = G.load_object(ROOT / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+    use(engine, hand, obj)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 64, 17
+    x0 = G.init_poses(hand, obj, cfg.batch, cfg.seed, cfg.init)
+    gpu = engine.synthesize(cfg, x0)
+    cpu = O.synthesize(hand, obj, cfg, x0, workers=os.cpu_count() or 8)
+    assert (gpu.failed == cpu.failed).all()
+    ok = cpu.failed == 0
+    close = np.abs(gpu.x - cpu.x).max(axis=1)
+    for a, b in ((gpu.energy_total[ok], cpu.energy_total[ok]), (gpu.stage_energy[ok, 0, 1], cpu.stage_energy[ok, 0, 1]),
+                 (gpu.stage_energy[ok, 2, 1], cpu.stage_energy[ok, 2, 1])):
+        assert abs(np.median(a) - np.median(b)) <= 0.1 * abs(np.median(b)) + 1e-3
+    eg = engine.evaluate(cfg, gpu.x[ok], gpu.x_s[ok])
+    ec = O.evaluate(hand, obj, cfg, cpu.x[ok], cpu.x_s[ok])
+    n = int(ok.sum())
+    summary = dict(grasps=n, x_close_1e6=float((close <= 1e-6).mean()), x_close_1e4=float((close <= 1e-4).mean()),
+                   success_gpu=float(eg["success"].mean()), success_cpu=float(ec["success"].mean()),
+                   pd_median_gpu=float(np.median(eg["pd_mm"])), pd_median_cpu=float(np.median(ec["pd_mm"])),
+                   energy_median_gpu=float(np.median(gpu.energy_total[ok])),
+                   energy_median_cpu=float(np.median(cpu.energy_total[ok])))
+    dst = Path(os.environ.get("GRASP_PARITY_OUT", ROOT / "gpurun_out"))
+    dst.mkdir(parents=True, exist_ok=True)
+    (dst / "end_to_end_config2.json").write_text(json.dumps(summary, indent=1))
+    print(json.dumps(summary))
+    assert abs(eg["success"].mean() - ec["success"].mean()) <= 3.0 / np.sqrt(n) + 0.05
+    assert abs(np.median(eg["pd_mm"]) - np.median(ec["pd_mm"])) <= 0.25 * np.median(ec["pd_mm"]) + 0.5
