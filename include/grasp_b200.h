@@ -226,6 +226,9 @@ int grasp_signed_distance(grasp_ctx* ctx, int n, const int* link_ids, const int*
  * (pipeline.cpp:96-210). energy[g], grad[g*D]. */
 int grasp_total_energy(grasp_ctx* ctx, const grasp_run_params* p, int stage, int n, const double* x,
                        const double* anchors, double* warm_x, double* warm_y, double* energy, double* grad);
+/* forward_kinematics(pose_from_state(x)) on the device, the FK every iteration of
+ * synthesize runs (hand.cpp:108-153): out[n*n_links*12] = R (9, column-major), t (3). */
+int grasp_device_forward_kinematics(grasp_ctx* ctx, int n, const double* x, double* out);
 /* fine_contact_query at states x (pipeline.cpp:320-353): out[g*m*11] =
  * c_w(3) p_w(3) n(3) distance link. */
 int grasp_fine_contact_query(grasp_ctx* ctx, int n, const double* x, double* out);

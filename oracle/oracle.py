@@ -46,8 +46,23 @@ def lib():
             "oracle_part_pairs": (C.c_int, [_vp, _vp, C.c_int, _ip, _ip, _dp, _dp, C.c_int, _dp]),
             "oracle_signed_distance": (C.c_int, [_vp, _vp, C.c_int, _ip, _ip, _dp, _dp]),
             "oracle_total_energy": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _ip, _dp, _dp,
-                                              _ip, _ip, C.c_int]),
+                                              _dp, _ip, _ip, C.c_int]),
             "oracle_forward_kinematics": (C.c_int, [_vp, C.c_int, _dp, _dp]),
+            "oracle_project_rotation": (C.c_int, [C.c_int, _dp, _dp, _ip]),
+            "oracle_pose_state": (C.c_int, [C.c_int, _dp, _dp, _dp, _ip, _dp]),
+            "oracle_hand_jacobian": (C.c_int, [_vp, _dp, C.c_int, _dp, C.c_int, _dp]),
+            "oracle_hand_energy": (C.c_int, [_vp, C.c_int, C.c_int, _dp, _dp, _dp]),
+            "oracle_build_frame": (C.c_int, [C.c_int, _dp, _dp, _dp]),
+            "oracle_wrench_basis": (C.c_int, [C.c_int, _dp, C.c_double, C.c_int, _dp]),
+            "oracle_assemble_lower_qp": (C.c_int, [_dp, C.c_int, C.c_int, _dp, C.c_int, C.c_double, C.c_double,
+                                                   _dp, _dp, _dp, _dp, _dp]),
+            "oracle_solve_shared": (C.c_int, [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _vp, _dp, _dp,
+                                              _dp, _dp, _dp, _ip, _ip]),
+            "oracle_grasp_energy": (C.c_int, [_vp, C.c_int, _dp, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                              _ip, _ip]),
+            "oracle_grasp_energy_gradient": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp, C.c_int, _dp, _dp, _dp]),
+            "oracle_stage_surrogate": (C.c_int, [C.c_int, _dp, _dp, C.c_int, _dp, _dp, _dp]),
+            "oracle_fine_grasp_surrogate": (C.c_int, [_vp, _dp, C.c_int, _dp, _ip, _dp, _dp, _dp]),
             "oracle_apply_step": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _dp, _dp]),
             "oracle_coarse_distance_energy": (C.c_int, [_vp, _vp, C.c_int, _dp, C.c_double, C.c_double, _dp, _dp]),
             "oracle_fine_contact_query": (C.c_int, [_vp, _vp, C.c_int, _dp, _dp]),
@@ -111,10 +126,11 @@ def signed_distance(hand, obj, link_ids, part_ids, poses) -> np.ndarray:
 
 
 def total_energy(hand, obj, cfg, stage, x, anchors=None, warm_x=None, warm_y=None, with_grad=True,
-                 warm_ready=None, qp_stats=False, threads=None):
+                 warm_ready=None, qp_stats=False, threads=None, world=None):
     """total_energy (pipeline.cpp:96-210) per grasp. warm_x/warm_y (updated in place) are
     the coarse QP's warm start, used for grasps with warm_ready != 0 (all when None).
-    With qp_stats, also returns the coarse QP's per-column (iters, converged)."""
+    With qp_stats, also returns the coarse QP's per-column (iters, converged). world
+    ((n, L, 12), R column-major) teacher-forces the link transforms instead of the oracle's FK."""
     x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, hand.dims())
     n = len(x)
     energy = np.zeros(n)
@@ -127,8 +143,9 @@ def total_energy(hand, obj, cfg, stage, x, anchors=None, warm_x=None, warm_y=Non
         assert a is None or (a.flags.c_contiguous and a.dtype == np.float64)
     p = cfg.to_params()
     nt = threads if threads is not None else (os.cpu_count() or 1)
+    wd = None if world is None else np.ascontiguousarray(world, dtype=np.float64)
     _check(lib().oracle_total_energy(ref(hand.desc), ref(obj.desc), ref(p), stage, n, _d(x), _d(anc), _d(warm_x),
-                                     _d(warm_y), _i(rdy), _d(energy), _d(grad), _i(its), _i(conv), int(nt)))
+                                     _d(warm_y), _i(rdy), _d(wd), _d(energy), _d(grad), _i(its), _i(conv), int(nt)))
     if qp_stats:
         return energy, grad, its, conv
     return energy, grad
@@ -215,3 +232,170 @@ def synthesize(hand, obj, cfg, x0, workers=1, with_stats=False):
     if with_stats:
         return out, dict(zip(STAT_NAMES, (int(v) for v in stats)))
     return out
+
+
+# ------------------------------------------------------------------------------
+# Fine-grained entry points for the reference's own KATs (oracle/src/kats.cpp).
+def _f(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a if shape is None else a.reshape(shape)
+
+
+def _colmajor(M):
+    """3x3 (or (n, 3, 3)) row-index matrices -> column-major 9-vectors."""
+    M = np.asarray(M, dtype=np.float64)
+    return np.ascontiguousarray(M.swapaxes(-1, -2).reshape(M.shape[:-2] + (9,)))
+
+
+def _from_colmajor(v):
+    v = np.asarray(v)
+    return v.reshape(v.shape[:-1] + (3, 3)).swapaxes(-1, -2)
+
+
+def project_rotation(raw):
+    """hand.cpp:45-73 on (n, 3, 3) -> (R (n, 3, 3), fallback (n,))."""
+    raw = np.asarray(raw, dtype=np.float64).reshape(-1, 3, 3)
+    n = len(raw)
+    R = np.zeros((n, 9))
+    fb = np.zeros(n, np.int32)
+    _check(lib().oracle_project_rotation(n, _d(_colmajor(raw)), _d(R), _i(fb)))
+    return _from_colmajor(R), fb.astype(bool)
+
+
+def pose_state(raw):
+    """make_pose_state + rotation_tangent_jacobian (hand.cpp:75-106) -> R, a_inv, degenerate, J (n, 3, 9)."""
+    raw = np.asarray(raw, dtype=np.float64).reshape(-1, 3, 3)
+    n = len(raw)
+    R, ai, J = np.zeros((n, 9)), np.zeros((n, 9)), np.zeros((n, 3, 9))
+    dg = np.zeros(n, np.int32)
+    _check(lib().oracle_pose_state(n, _d(_colmajor(raw)), _d(R), _d(ai), _i(dg), _d(J)))
+    return _from_colmajor(R), _from_colmajor(ai), dg.astype(bool), J
+
+
+def hand_jacobian(hand, x, link, vec, direction=False):
+    """point_jacobian (hand.cpp:155-169) or direction_jacobian (:171-183) -> (3, D)."""
+    x = _f(x)
+    J = np.zeros((3, hand.dims()))
+    _check(lib().oracle_hand_jacobian(ref(hand.desc), _d(x), int(link), _d(_f(vec)), 1 if direction else 0, _d(J)))
+    return J
+
+
+def limit_energy(hand, x):
+    """hand.cpp:207-218 on states (n, D) -> (e, grad)."""
+    x = _f(x).reshape(-1, hand.dims())
+    e, g = np.zeros(len(x)), np.zeros_like(x)
+    _check(lib().oracle_hand_energy(ref(hand.desc), 0, len(x), _d(x), _d(e), _d(g)))
+    return e, g
+
+
+def self_penetration_energy(hand, x):
+    """hand.cpp:220-245 on states (n, D) -> (e, grad)."""
+    x = _f(x).reshape(-1, hand.dims())
+    e, g = np.zeros(len(x)), np.zeros_like(x)
+    _check(lib().oracle_hand_energy(ref(hand.desc), 1, len(x), _d(x), _d(e), _d(g)))
+    return e, g
+
+
+def build_frame(p, n):
+    """contact.cpp:13-21 -> (k, 12) rows p n d e."""
+    p = _f(p).reshape(-1, 3)
+    n = _f(n).reshape(-1, 3)
+    out = np.zeros((len(p), 12))
+    _check(lib().oracle_build_frame(len(p), _d(p), _d(n), _d(out)))
+    return out
+
+
+def wrench_basis(frames, mu, k):
+    """contact.cpp:47-53 -> W (6, m*k)."""
+    fr = _f(frames).reshape(-1, 12)
+    m = len(fr)
+    W = np.zeros((m * k, 6))
+    _check(lib().oracle_wrench_basis(m, _d(fr), float(mu), int(k), _d(W)))
+    return W.T.copy()
+
+
+def assemble_lower_qp(W, m, targets, beta, gamma_total):
+    """qpsolve.cpp:193-235 -> dict P, A, Q, L, U (numpy, row-index)."""
+    W = np.asarray(W, dtype=np.float64)
+    nv = W.shape[1]
+    T = np.asarray(targets, dtype=np.float64).reshape(6, -1)
+    B = T.shape[1]
+    M = m + 1 + nv
+    P, A, Q, L, U = np.zeros(nv * nv), np.zeros(M * nv), np.zeros(nv * B), np.zeros(M * B), np.zeros(M * B)
+    _check(lib().oracle_assemble_lower_qp(_d(_f(W.T)), int(m), nv, _d(_f(T.T)), B, float(beta), float(gamma_total),
+                                          _d(P), _d(A), _d(Q), _d(L), _d(U)))
+    cm = lambda v, r, c: v.reshape(c, r).T
+    return dict(P=cm(P, nv, nv), A=cm(A, M, nv), Q=cm(Q, nv, B), L=cm(L, M, B), U=cm(U, M, B))
+
+
+def solve_shared(P, A, Q, L, U, cfg, warm_x=None, warm_y=None):
+    """qpsolve.cpp:45-120 on a general batch (numpy, row-index; Q/L/U (rows, B)) -> dict."""
+    P, A = np.asarray(P, float), np.asarray(A, float)
+    Q, L, U = (np.asarray(v, float).reshape(len(v), -1) for v in (Q, L, U))
+    n, M, B = P.shape[0], A.shape[0], Q.shape[1]
+    X, Y, Z = np.zeros(n * B), np.zeros(M * B), np.zeros(M * B)
+    it, cv = np.zeros(B, np.int32), np.zeros(B, np.int32)
+    p = cfg.to_params()
+    wx = None if warm_x is None else _f(np.asarray(warm_x, float).reshape(n, B).T)
+    wy = None if warm_y is None else _f(np.asarray(warm_y, float).reshape(M, B).T)
+    _check(lib().oracle_solve_shared(n, M, B, _d(_f(P.T)), _d(_f(A.T)), _d(_f(Q.T)), _d(_f(L.T)), _d(_f(U.T)),
+                                     ref(p), _d(wx), _d(wy), _d(X), _d(Y), _d(Z), _i(it), _i(cv)))
+    cm = lambda v, r: v.reshape(B, r).T
+    return dict(X=cm(X, n), Y=cm(Y, M), Z=cm(Z, M), iters=it, converged=cv.astype(bool))
+
+
+def grasp_energy(cfg, frames, targets=None, warm_x=None, warm_y=None):
+    """energy.cpp:60-92 with targets (6, B) (None = the six closure directions) -> dict."""
+    fr = _f(frames).reshape(-1, 12)
+    m = len(fr)
+    nv = m * cfg.contact.n_edges
+    M = m + 1 + nv
+    T = None if targets is None else np.asarray(targets, float).reshape(6, -1)
+    B = 6 if T is None else T.shape[1]
+    tot = C.c_double()
+    per, conv, its = np.zeros(B), np.zeros(B, np.int32), np.zeros(B, np.int32)
+    F, R, Yd = np.zeros(nv * B), np.zeros(6 * B), np.zeros(M * B)
+    p = cfg.to_params()
+    _check(lib().oracle_grasp_energy(ref(p), m, _d(fr), B, None if T is None else _d(_f(T.T)),
+                                     None if warm_x is None else _d(_f(np.asarray(warm_x).T)),
+                                     None if warm_y is None else _d(_f(np.asarray(warm_y).T)),
+                                     C.byref(tot), _d(per), _d(F), _d(R), _d(Yd), _i(conv), _i(its)))
+    return dict(total=tot.value, per_direction=per, forces=F.reshape(B, nv).T, residuals=R.reshape(B, 6).T,
+                duals=Yd.reshape(B, M).T, converged=conv.astype(bool), iters=its)
+
+
+def grasp_energy_gradient(cfg, frames, report, jac_p, jac_n):
+    """energy.cpp:94-145: jac_p/jac_n (m, 3, D) -> grad (D,)."""
+    fr = _f(frames).reshape(-1, 12)
+    m = len(fr)
+    jp, jn = _f(jac_p).reshape(m, 3, -1), _f(jac_n).reshape(m, 3, -1)
+    D = jp.shape[2]
+    g = np.zeros(D)
+    p = cfg.to_params()
+    _check(lib().oracle_grasp_energy_gradient(ref(p), m, _d(fr), _d(_f(report["forces"].T)),
+                                              _d(_f(report["residuals"].T)), D, _d(jp), _d(jn), _d(g)))
+    return g
+
+
+def stage_surrogate(points, anchors, jacobians=None):
+    """fine_stage_surrogate (energy.cpp:208-229) -> (value, grad or None)."""
+    pts, anc = _f(points).reshape(-1, 3), _f(anchors).reshape(-1, 3)
+    v = C.c_double()
+    if jacobians is None:
+        _check(lib().oracle_stage_surrogate(len(pts), _d(pts), _d(anc), 0, None, C.byref(v), None))
+        return v.value, None
+    J = _f(jacobians).reshape(len(pts), 3, -1)
+    g = np.zeros(J.shape[2])
+    _check(lib().oracle_stage_surrogate(len(pts), _d(pts), _d(anc), J.shape[2], _d(J), C.byref(v), _d(g)))
+    return v.value, g
+
+
+def fine_grasp_surrogate(hand, x, c_w, links, anchors):
+    """pipeline.cpp:54-65 / 382-386 (witnesses rigid on their links) -> (value, grad)."""
+    x = _f(x)
+    cw, anc = _f(c_w).reshape(-1, 3), _f(anchors).reshape(-1, 3)
+    lk = np.ascontiguousarray(links, dtype=np.int32)
+    v = C.c_double()
+    g = np.zeros(hand.dims())
+    _check(lib().oracle_fine_grasp_surrogate(ref(hand.desc), _d(x), len(cw), _d(cw), _i(lk), _d(anc), C.byref(v), _d(g)))
+    return v.value, g

@@ -204,6 +204,15 @@ void parallel_grasps(int n, int threads, F&& fn) {
 
 }  // namespace
 
+namespace oracle {
+Hand make_hand_desc(const grasp_hand_desc* d) { return make_hand(d); }
+Config make_config_params(const grasp_run_params* p) { return make_config(p); }
+int set_error(int code, const char* what) {
+  g_err = what;
+  return code;
+}
+}  // namespace oracle
+
 extern "C" {
 
 const char* oracle_last_error(void) { return g_err.c_str(); }
@@ -271,11 +280,12 @@ int oracle_signed_distance(const grasp_hand_desc* hd, const grasp_object_desc* o
 // std::threads. warm_ready[g] (NULL = all) selects which grasps start the
 // coarse QP from warm_x/warm_y; those are updated in place like the
 // reference's QpScratch. qp_iters/qp_conv receive the coarse QP's per-column
-// sweep counts and convergence flags.
+// sweep counts and convergence flags. world (optional, [n*L*12]) teacher-forces
+// the link transforms (set_world_override).
 int oracle_total_energy(const grasp_hand_desc* hd, const grasp_object_desc* od, const grasp_run_params* p, int stage,
                         int n, const double* x, const double* anchors, double* warm_x, double* warm_y,
-                        const int* warm_ready, double* energy, double* grad, int* qp_iters, int* qp_conv,
-                        int threads) {
+                        const int* warm_ready, const double* world, double* energy, double* grad, int* qp_iters,
+                        int* qp_conv, int threads) {
   return guarded([&] {
     const Hand h = make_hand(hd);
     const Object obj = make_object(od);
@@ -295,7 +305,14 @@ int oracle_total_energy(const grasp_hand_desc* hd, const grasp_object_desc* od, 
         scratch.ready = true;
       }
       VecX gr;
-      energy[g] = total_energy(h, obj, cfg, stage, anc, xv, scratch, grad ? &gr : nullptr);
+      set_world_override(world ? world + static_cast<size_t>(g) * h.links.size() * 12 : nullptr);
+      try {
+        energy[g] = total_energy(h, obj, cfg, stage, anc, xv, scratch, grad ? &gr : nullptr);
+      } catch (...) {
+        set_world_override(nullptr);
+        throw;
+      }
+      set_world_override(nullptr);
       if (grad) std::memcpy(grad + static_cast<size_t>(g) * D, gr.data(), sizeof(double) * D);
       if (stage == 0)
         for (int j = 0; j < 6; ++j) {

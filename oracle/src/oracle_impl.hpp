@@ -104,6 +104,8 @@ M3 raw_block(const VecX& x);
 Pose pose_from_state(const Hand& h, const VecX& x);
 Fk forward_kinematics(const Hand& h, const Pose& pose);
 MatX point_jacobian(const Hand& h, const PoseState& ps, const Pose& pose, const Fk& fk, int link, const V3& pw);
+MatX direction_jacobian(const Hand& h, const PoseState& ps, const Pose& pose, const Fk& fk, int link, const V3& dw);
+void tangent_jacobian(const PoseState& ps, double J[3][9]);  // hand.cpp:97-106
 double limit_energy(const Hand& h, const Pose& pose, VecX* grad);
 double self_penetration_energy(const Hand& h, const PoseState& ps, const Pose& pose, const Fk& fk, VecX* grad);
 
@@ -143,6 +145,8 @@ MatX closure_directions();
 EnergyReport grasp_energy(const std::vector<Frame>& frames, double beta, double gamma_per_contact, double mu, int k,
                           const QpParams& qp, const MatX* warm_x, const MatX* warm_y,
                           const MatX* targets = nullptr);
+double fine_stage_surrogate(const std::vector<V3>& points, const std::vector<V3>& anchors,
+                            const std::vector<MatX>& jacobians, VecX* grad);
 VecX grasp_energy_gradient(const std::vector<Frame>& frames, const EnergyReport& rep, double mu, int k,
                            const std::vector<MatX>& jac_p, const std::vector<MatX>& jac_n);
 
@@ -199,6 +203,9 @@ struct QpScratch {
 // stage: 0 coarse, 1 fine, 2 final
 double total_energy(const Hand& h, const Object& obj, const Config& cfg, int stage, const std::vector<V3>& anchors,
                     const VecX& x, QpScratch& scratch, VecX* grad);
+// Test-only teacher forcing: world link transforms for this thread's next
+// pose_hand calls ([L*12] R column-major, t), nullptr = own FK.
+void set_world_override(const double* world);
 void apply_step(const Hand& h, const Stage& s, int it, const VecX& grad, VecX& x);
 double coarse_distance_energy(const Hand& h, const VecX& x, const Object& obj, double offset, double fd, VecX* grad);
 

@@ -19,12 +19,25 @@ struct Posed {
   Fk fk;
 };
 
+// Teacher forcing of the kinematics (tests only): when set, the world link
+// transforms of the next pose_hand calls on this thread are taken from here
+// ([L*12], R column-major, t) instead of this oracle's own FK, so the rest of
+// total_energy runs on exactly the device's link poses.
+thread_local const double* tl_world_override = nullptr;
+
 // pipeline.cpp:36-42 (projection is done twice, as in the reference).
 Posed pose_hand(const Hand& h, const VecX& x) {
   Posed p;
   p.ps = make_pose_state(raw_block(x));
   p.pose = pose_from_state(h, x);
   p.fk = forward_kinematics(h, p.pose);
+  if (tl_world_override)
+    for (size_t l = 0; l < p.fk.world.size(); ++l) {
+      const double* w = tl_world_override + 12 * l;
+      for (int c = 0; c < 3; ++c)
+        for (int i = 0; i < 3; ++i) p.fk.world[l].R(i, c) = w[3 * c + i];
+      p.fk.world[l].t = V3(w[9], w[10], w[11]);
+    }
   return p;
 }
 
@@ -67,6 +80,8 @@ V3 tip_center(const Hand& h, const Fk& fk, int f) {
 }
 
 }  // namespace
+
+void set_world_override(const double* world) { tl_world_override = world; }
 
 // pipeline.cpp:320-353.
 std::vector<Witness> fine_contact_query(const Hand& h, const Fk& fk, const Object& obj) {

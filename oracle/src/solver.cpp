@@ -210,6 +210,25 @@ MatX point_jacobian(const Hand& h, const PoseState& ps, const Pose& pose, const 
   return J;
 }
 
+// hand.cpp:171-183: like point_jacobian for a direction (no translation columns).
+MatX direction_jacobian(const Hand& h, const PoseState& ps, const Pose& pose, const Fk& fk, int link, const V3& dw) {
+  MatX J(3, h.dims());
+  const V3 v = pose.R.t() * dw;
+  double T[3][9];
+  rotation_tangent_jacobian(ps, T);
+  const M3 A = pose.R * skew(v);
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 9; ++c) J(r, c) = -(A(r, 0) * T[0][c] + A(r, 1) * T[1][c] + A(r, 2) * T[2][c]);
+  for (int jo = 0; jo < h.dof(); ++jo) {
+    if (!is_ancestor_joint(h, jo, link)) continue;
+    const V3 col = pose.R * cross(fk.joint_axis[jo], v);
+    for (int r = 0; r < 3; ++r) J(r, 12 + jo) = col[r];
+  }
+  return J;
+}
+
+void tangent_jacobian(const PoseState& ps, double J[3][9]) { rotation_tangent_jacobian(ps, J); }
+
 // hand.cpp:207-218.
 double limit_energy(const Hand& h, const Pose& pose, VecX* grad) {
   double e = 0.0;
@@ -382,8 +401,23 @@ SharedBatch assemble_lower_qp(const MatX& W, int m, const MatX& targets, double 
   return b;
 }
 
+// qpsolve.cpp:14-25.
+void check_dims(const SharedBatch& b) {
+  const int n = b.P.rows, m = b.A.rows;
+  if (b.P.cols != n || b.A.cols != n) throw std::invalid_argument("qp: P/A dimension mismatch");
+  if (b.Q.rows != n || b.L.rows != m || b.U.rows != m)
+    throw std::invalid_argument("qp: vector block dimension mismatch");
+  if (b.Q.cols != b.L.cols || b.Q.cols != b.U.cols || b.Q.cols < 1)
+    throw std::invalid_argument("qp: batch width mismatch");
+  double asym = 0.0;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) asym = std::max(asym, std::abs(b.P(i, j) - b.P(j, i)));
+  if (asym > 1e-9) throw std::invalid_argument("qp: P must be symmetric");
+}
+
 // qpsolve.cpp:45-120 (OSQP-form ADMM, lockstep columns, freeze at checks).
 BatchSolution solve_shared(const SharedBatch& b, const QpParams& p, const MatX* warm_x, const MatX* warm_y) {
+  check_dims(b);
   const int n = b.P.rows, M = b.A.rows, B = b.Q.cols;
   const double rho = p.rho, sigma = p.sigma, alpha = p.alpha;
   const MatX At = transpose(b.A);
@@ -498,6 +532,28 @@ EnergyReport grasp_energy(const std::vector<Frame>& frames, double beta, double 
   rep.total = 0.0;
   for (int j = 0; j < 6; ++j) rep.total += rep.per_direction[j];
   return rep;
+}
+
+// energy.cpp:208-229.
+double fine_stage_surrogate(const std::vector<V3>& points, const std::vector<V3>& anchors,
+                            const std::vector<MatX>& jacobians, VecX* grad) {
+  if (points.size() != anchors.size()) throw std::invalid_argument("point and anchor counts differ");
+  if (!jacobians.empty() && jacobians.size() != points.size())
+    throw std::invalid_argument("need one Jacobian per point when given");
+  const int dims = jacobians.empty() ? 0 : jacobians[0].cols;
+  if (grad) grad->assign(dims, 0.0);
+  double value = 0.0;
+  for (size_t i = 0; i < points.size(); ++i) {
+    const V3 diff = points[i] - anchors[i];
+    value += sqnorm(diff);
+    if (!jacobians.empty() && grad) {
+      if (jacobians[i].rows != 3 || jacobians[i].cols != dims)
+        throw std::invalid_argument("point Jacobians must be 3 x dims");
+      for (int c = 0; c < dims; ++c)
+        (*grad)[c] += 2.0 * (jacobians[i](0, c) * diff[0] + jacobians[i](1, c) * diff[1] + jacobians[i](2, c) * diff[2]);
+    }
+  }
+  return value;
 }
 
 // energy.cpp:94-145 (envelope gradient, lambda* fixed).

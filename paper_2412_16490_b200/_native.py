@@ -124,6 +124,7 @@ SIGNATURES = {
     "grasp_total_energy": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.c_int, C.c_int, _dp, _dp, _dp, _dp,
                                      _dp, _dp]),
     "grasp_fine_contact_query": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp]),
+    "grasp_device_forward_kinematics": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp]),
     "grasp_ctx_stream": (C.c_void_p, [C.c_void_p]),
     "grasp_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "grasp_ctx_profile": (C.c_int, [C.c_void_p, _dp, C.POINTER(C.c_longlong), C.POINTER(C.c_ulonglong)]),

@@ -1367,6 +1367,33 @@ int grasp_total_energy(grasp_ctx* ctx, const grasp_run_params* p, int stage, int
   });
 }
 
+int grasp_device_forward_kinematics(grasp_ctx* ctx, int n, const double* x, double* out) {
+  return guard([&] {
+    if (!ctx || !ctx->has_hand) throw std::invalid_argument("no hand uploaded");
+    if (n < 0 || (n > 0 && (!x || !out))) throw std::invalid_argument("null argument");
+    if (n == 0) return;
+    ctx->set_device();
+    ctx->ensure_state(n, ctx->H.m, 8);
+    ctx->reset_run_state(n);
+    cudaStream_t s = ctx->stream;
+    const int L = ctx->H.L;
+    ck(cudaMemcpyAsync(ctx->x.p, x, sizeof(double) * n * ctx->H.D, cudaMemcpyHostToDevice, s), "x");
+    grasp_run_params def;
+    grasp_run_params_default(&def);
+    ctx->launch_fk(ctx->make_params(&def, ctx->H.m));
+    ck(cudaGetLastError(), "launch");
+    std::vector<double> w(static_cast<size_t>(n) * L * 12);
+    copy_out(w.data(), ctx->world.p, sizeof(double) * w.size(), cudaMemcpyDeviceToHost, s);
+    ck(cudaStreamSynchronize(s), "sync");
+    // device layout: R row-major; the ABI reports R column-major like grasp_forward_kinematics
+    for (size_t t = 0; t < static_cast<size_t>(n) * L; ++t)
+      for (int i = 0; i < 3; ++i) {
+        for (int c = 0; c < 3; ++c) out[12 * t + 3 * c + i] = w[12 * t + 3 * i + c];
+        out[12 * t + 9 + i] = w[12 * t + 9 + i];
+      }
+  });
+}
+
 int grasp_fine_contact_query(grasp_ctx* ctx, int n, const double* x, double* out) {
   return guard([&] {
     require_models(ctx);

@@ -4,14 +4,24 @@ The production engine runs the full 300/100/100 schedule on the BASELINE configs
 at selected iterations of every stage, each grasp's inputs (x, device FK, QP warm start,
 anchors) and outputs (total_energy, gradient, stepped x, QP snapshot and sweep counts)
 through grasp_ctx_set_trace. Every snapshot is then restarted on the CPU oracle
-(oracle/src/pipeline.cpp, restating pipeline.cpp:96-231) from exactly the recorded inputs:
+(oracle/src/pipeline.cpp, restating pipeline.cpp:96-231) from exactly the recorded inputs.
 
-  * FK of x_in (hand.cpp:126-153)                       <= 1e-6 m (8(d)); measured ~1e-16
-  * total_energy (pipeline.cpp:96-210)                  <= 1e-4 relative (8(d))
-  * gradient (max-norm relative per grasp)              <= 1e-4 (8(d))
-  * coarse QP forces lambda (energy.cpp:60-92)          <= 1e-4 abs (8(d)); sweep counts reported
-  * apply_step (pipeline.cpp:214-231) from the GPU's own gradient  <= 1e-6 (8(d))
-  * apply_step from the oracle's gradient vs the GPU's stepped x   <= 1e-6
+The oracle is run twice per snapshot: once on the device's own link transforms (teacher-forced
+FK, oracle total_energy(world=...)) and once on its own FK. Asserted (SURVEY 8(d) bounds in
+brackets; the asserted bounds are the measured agreement with margin):
+
+  * FK of x_in on the device (hand.cpp:126-153)          <= 1e-14 m      [1e-6 m]
+  * total_energy (pipeline.cpp:96-210), FK forced         <= 1e-10 rel    [1e-4]
+  * gradient (max-norm relative per grasp), FK forced     <= 1e-7         [1e-4]
+  * coarse QP forces lambda (energy.cpp:60-92)            <= 1e-9 abs     [1e-4]
+  * coarse QP sweep counts / convergence flags (qpsolve.cpp:99-117): identical on every column
+  * apply_step (pipeline.cpp:214-231) from the GPU's gradient: bitwise the GPU's stepped x
+  * apply_step from the oracle's gradient vs the GPU's x   <= 1e-6 when the FK is forced
+
+With the oracle's own FK (glibc sin/cos vs the device's correctly rounded ones: 1-3 ulp in a
+few link transforms), the reference's GJK/EPA is discontinuous in degenerate contacts, so a few
+mesh-stage grasps pick a different (equally valid) witness. Those are counted and bounded
+(<= 2% of mesh-stage grasp-snapshots); every one of them is exact once the FK is forced.
 
 A per-snapshot summary is written to $GRASP_PARITY_OUT (default gpurun_out/) so the measured
 agreement can be committed under profiles/.
@@ -32,7 +42,8 @@ COARSE = (0, 1, 2, 5, 10, 20, 40, 70, 100, 150, 200, 250, 298, 299)
 MESH = (0, 1, 2, 10, 30, 60, 98, 99)
 SNAPS = [(0, i) for i in COARSE] + [(1, i) for i in MESH] + [(2, i) for i in MESH]
 
-TOL = dict(fk=1e-6, energy=1e-4, grad=1e-4, lam=1e-4, step=1e-6)
+TOL = dict(fk=1e-14, energy=1e-10, grad=1e-7, lam=1e-9, step=0.0, step_from_oracle_grad=1e-6)
+OWN_FK_MISMATCH_RATE = 0.02
 
 
 def _stage_params(cfg, s):
@@ -50,61 +61,76 @@ def run_trajectory_parity(G, O, engine, hand, obj, batch, seed, name):
     assert np.array_equal(plain.x, out.x) and np.array_equal(plain.failed, out.failed)
 
     rows, worst = [], {k: 0.0 for k in TOL}
-    qp_cols = qp_same = 0
+    qp_cols = qp_same = qp_conv_same = 0
+    own_fk_mismatch = mesh_grasp_snaps = 0
     for k, (s, it) in enumerate(SNAPS):
         live = T["failed"][k] == 0
         if not live.any():
             continue
         x_in = T["x_in"][k][live]
+        world = T["world_in"][k][live]
         # FK on the device vs the oracle's Eigen-restated chain
         fk_ref = O.forward_kinematics(hand, x_in)
-        fk_err = np.abs(T["world_in"][k][live] - fk_ref).max()
-        # energy / gradient / QP from the recorded inputs
+        fk_err = np.abs(world - fk_ref).max()
+        fk_bitwise = (world == fk_ref).all(axis=(1, 2))
         anchors = T["anchors"][k][live] if s > 0 else None
         if s == 0:
             wx = np.ascontiguousarray(T["warm_x_in"][k][live])
             wy = np.ascontiguousarray(T["warm_y_in"][k][live])
+            rdy = T["warm_ready_in"][k][live]
+            e_own, g_own = O.total_energy(hand, obj, cfg, 0, x_in, warm_x=wx.copy(), warm_y=wy.copy(),
+                                          warm_ready=rdy)
             e_ref, g_ref, its, conv = O.total_energy(hand, obj, cfg, 0, x_in, warm_x=wx, warm_y=wy,
-                                                     warm_ready=T["warm_ready_in"][k][live], qp_stats=True)
+                                                     warm_ready=rdy, qp_stats=True, world=world)
             lam_err = np.abs(wx - T["warm_x_out"][k][live]).max()
             same = its == T["qp_iters"][k][live]
             qp_cols += same.size
             qp_same += int(same.sum())
-            iters_match = float(same.mean())
-            conv_match = float((conv == T["qp_converged"][k][live]).mean())
-            mean_sweeps = float(its.mean())
+            qp_conv_same += int((conv == T["qp_converged"][k][live]).sum())
+            iters_match, mean_sweeps = float(same.mean()), float(its.mean())
         else:
-            e_ref, g_ref = O.total_energy(hand, obj, cfg, s, x_in, anchors=anchors)
-            lam_err, iters_match, conv_match, mean_sweeps = 0.0, None, None, None
+            e_own, g_own = O.total_energy(hand, obj, cfg, s, x_in, anchors=anchors)
+            e_ref, g_ref = O.total_energy(hand, obj, cfg, s, x_in, anchors=anchors, world=world)
+            lam_err, iters_match, mean_sweeps = 0.0, None, None
         e_got, g_got = T["energy"][k][live], T["grad"][k][live]
-        e_err = (np.abs(e_got - e_ref) / np.maximum(np.abs(e_ref), 1e-300)).max()
+        rel = lambda a, b: np.abs(a - b) / np.maximum(np.abs(b), 1e-300)
+        e_err = rel(e_got, e_ref).max()
         gscale = np.maximum(np.abs(g_ref).max(axis=1), 1e-300)
         g_err_rows = np.abs(g_got - g_ref).max(axis=1) / gscale
+        g_own_rows = np.abs(g_got - g_own).max(axis=1) / np.maximum(np.abs(g_own).max(axis=1), 1e-300)
+        own_bad = (g_own_rows > 1e-4) | (rel(e_got, e_own) > 1e-4)
+        if s > 0:
+            own_fk_mismatch += int(own_bad.sum())
+            mesh_grasp_snaps += int(live.sum())
+            assert not (own_bad & fk_bitwise).any(), "own-FK mismatch although the FK is bitwise equal"
         sp = _stage_params(cfg, s)
         x_own = O.apply_step(hand, sp, it, g_got, x_in)
         x_ref = O.apply_step(hand, sp, it, g_ref, x_in)
         step_err = np.abs(x_own - T["x_out"][k][live]).max()
         traj_err = np.abs(x_ref - T["x_out"][k][live]).max()
-        row = dict(stage=s, iter=it, grasps=int(live.sum()), fk=float(fk_err), energy=float(e_err),
-                   grad=float(g_err_rows.max()), grad_p99=float(np.quantile(g_err_rows, 0.99)),
-                   lam=float(lam_err), step=float(step_err), step_from_oracle_grad=float(traj_err),
-                   qp_iters_match=iters_match, qp_conv_match=conv_match, qp_mean_sweeps=mean_sweeps)
+        row = dict(stage=s, iter=it, grasps=int(live.sum()), fk=float(fk_err), fk_bitwise=float(fk_bitwise.mean()),
+                   energy=float(e_err), grad=float(g_err_rows.max()),
+                   grad_p99=float(np.quantile(g_err_rows, 0.99)), lam=float(lam_err), step=float(step_err),
+                   step_from_oracle_grad=float(traj_err), qp_iters_match=iters_match, qp_mean_sweeps=mean_sweeps,
+                   own_fk_energy=float(rel(e_got, e_own).max()), own_fk_grad=float(g_own_rows.max()),
+                   own_fk_mismatched_grasps=int(own_bad.sum()))
         rows.append(row)
-        worst["fk"] = max(worst["fk"], fk_err)
-        worst["energy"] = max(worst["energy"], e_err)
-        worst["grad"] = max(worst["grad"], g_err_rows.max())
-        worst["lam"] = max(worst["lam"], lam_err)
-        worst["step"] = max(worst["step"], step_err, traj_err)
+        for key in TOL:
+            worst[key] = max(worst[key], row[key])
     summary = dict(config=name, batch=batch, seed=seed, snapshots=rows, worst={k: float(v) for k, v in worst.items()},
-                   tolerance=TOL, qp_columns=qp_cols, qp_iters_identical=qp_same,
+                   tolerance=TOL, qp_columns=qp_cols, qp_iters_identical=qp_same, qp_converged_identical=qp_conv_same,
+                   own_fk_mesh_mismatches=own_fk_mismatch, mesh_grasp_snapshots=mesh_grasp_snaps,
                    failed=int((out.failed != 0).sum()))
     dst = Path(os.environ.get("GRASP_PARITY_OUT", ROOT / "gpurun_out"))
     dst.mkdir(parents=True, exist_ok=True)
     (dst / f"trajectory_parity_{name}.json").write_text(json.dumps(summary, indent=1))
-    print(json.dumps(dict(config=name, worst=summary["worst"], qp_iters_identical=f"{qp_same}/{qp_cols}")))
+    print(json.dumps(dict(config=name, worst=summary["worst"], qp_iters_identical=f"{qp_same}/{qp_cols}",
+                          own_fk_mesh_mismatches=f"{own_fk_mismatch}/{mesh_grasp_snaps}")))
     assert len(rows) == len(SNAPS), "a stage was skipped (all grasps failed?)"
     for key, tol in TOL.items():
         assert worst[key] <= tol, (key, worst[key], [r for r in rows if r[key] > tol][:3])
+    assert qp_same == qp_cols and qp_conv_same == qp_cols, (qp_same, qp_conv_same, qp_cols)
+    assert own_fk_mismatch <= OWN_FK_MISMATCH_RATE * mesh_grasp_snaps
     return out, summary
 
 
