@@ -56,8 +56,8 @@ def lib():
             "oracle_wrench_basis": (C.c_int, [C.c_int, _dp, C.c_double, C.c_int, _dp]),
             "oracle_assemble_lower_qp": (C.c_int, [_dp, C.c_int, C.c_int, _dp, C.c_int, C.c_double, C.c_double,
                                                    _dp, _dp, _dp, _dp, _dp]),
-            "oracle_solve_shared": (C.c_int, [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _vp, _dp, _dp,
-                                              _dp, _dp, _dp, _ip, _ip]),
+            "oracle_solve_shared": (C.c_int, [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _ip, _vp, _dp,
+                                              _dp, _dp, _dp, _dp, _ip, _ip]),
             "oracle_grasp_energy": (C.c_int, [_vp, C.c_int, _dp, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                               _ip, _ip]),
             "oracle_grasp_energy_gradient": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp, C.c_int, _dp, _dp, _dp]),
@@ -338,8 +338,9 @@ def solve_shared(P, A, Q, L, U, cfg, warm_x=None, warm_y=None):
     p = cfg.to_params()
     wx = None if warm_x is None else _f(np.asarray(warm_x, float).reshape(n, B).T)
     wy = None if warm_y is None else _f(np.asarray(warm_y, float).reshape(M, B).T)
+    rows = np.array([Q.shape[0], L.shape[0], U.shape[0]], np.int32)
     _check(lib().oracle_solve_shared(n, M, B, _d(_f(P.T)), _d(_f(A.T)), _d(_f(Q.T)), _d(_f(L.T)), _d(_f(U.T)),
-                                     ref(p), _d(wx), _d(wy), _d(X), _d(Y), _d(Z), _i(it), _i(cv)))
+                                     _i(rows), ref(p), _d(wx), _d(wy), _d(X), _d(Y), _d(Z), _i(it), _i(cv)))
     cm = lambda v, r: v.reshape(B, r).T
     return dict(X=cm(X, n), Y=cm(Y, M), Z=cm(Z, M), iters=it, converged=cv.astype(bool))
 

@@ -188,16 +188,17 @@ int oracle_assemble_lower_qp(const double* W, int m, int nv, const double* targe
 
 // solve_shared (qpsolve.cpp:45-120) on a general shared-structure batch: P[n*n], A[M*n],
 // Q[n*B], L/U[M*B] column-major; QP settings from p's qp_* fields.
+// rows[3] = row counts of Q, L, U as given (checked against n and M like qpsolve.cpp:14-25).
 int oracle_solve_shared(int n, int M, int B, const double* P, const double* A, const double* Q, const double* L,
-                        const double* U, const grasp_run_params* p, const double* warm_x, const double* warm_y,
-                        double* X, double* Y, double* Z, int* iters, int* converged) {
+                        const double* U, const int* rows, const grasp_run_params* p, const double* warm_x,
+                        const double* warm_y, double* X, double* Y, double* Z, int* iters, int* converged) {
   return kat_guard([&] {
     SharedBatch b;
     b.P = matx(P, n, n);
     b.A = matx(A, M, n);
-    b.Q = matx(Q, n, B);
-    b.L = matx(L, M, B);
-    b.U = matx(U, M, B);
+    b.Q = matx(Q, rows[0], B);
+    b.L = matx(L, rows[1], B);
+    b.U = matx(U, rows[2], B);
     MatX wx, wy;
     if (warm_x && warm_y) {
       wx = matx(warm_x, n, B);

@@ -516,9 +516,10 @@ EnergyReport grasp_energy(const std::vector<Frame>& frames, double beta, double 
   rep.duals = sol.Y;
   rep.converged = sol.converged;
   rep.iters = sol.iters;
-  rep.residuals = MatX(6, 6);
-  rep.per_direction.assign(6, 0.0);
-  for (int j = 0; j < 6; ++j) {
+  const int B = dirs.cols;  // closure directions (6) or caller targets (energy.cpp:66-70)
+  rep.residuals = MatX(6, B);
+  rep.per_direction.assign(B, 0.0);
+  for (int j = 0; j < B; ++j) {
     double e = 0.0;
     for (int r = 0; r < 6; ++r) {
       double wl = 0.0;
@@ -530,7 +531,7 @@ EnergyReport grasp_energy(const std::vector<Frame>& frames, double beta, double 
     rep.per_direction[j] = e;
   }
   rep.total = 0.0;
-  for (int j = 0; j < 6; ++j) rep.total += rep.per_direction[j];
+  for (int j = 0; j < B; ++j) rep.total += rep.per_direction[j];
   return rep;
 }
 
