@@ -155,6 +155,13 @@ typedef struct grasp_ctx grasp_ctx;
 
 /* One context drives one CUDA device on one stream. */
 int grasp_ctx_create(int device, grasp_ctx** out);
+/* A context over several devices: models are uploaded to every
+ * device, and grasp_synthesize splits the batch into contiguous shards
+ * [k*B/n, (k+1)*B/n), each run by its own host thread and stream, writing its
+ * rows of the caller's outputs (results equal the single-device run's).
+ * Repeated device ids are allowed (several streams on one GPU). The other
+ * entry points use the first device; grasp_synthesize_device is single-device only. */
+int grasp_ctx_create_devices(const int* devices, int n, grasp_ctx** out);
 void grasp_ctx_destroy(grasp_ctx* ctx);
 /* Uploads the packed hand / object (replaces any previous one). */
 int grasp_ctx_set_hand(grasp_ctx* ctx, const grasp_hand_desc* hand);
@@ -229,6 +236,9 @@ int grasp_total_energy(grasp_ctx* ctx, const grasp_run_params* p, int stage, int
 /* forward_kinematics(pose_from_state(x)) on the device, the FK every iteration of
  * synthesize runs (hand.cpp:108-153): out[n*n_links*12] = R (9, column-major), t (3). */
 int grasp_device_forward_kinematics(grasp_ctx* ctx, int n, const double* x, double* out);
+/* fine_contact_query(model, fk, object) (pipeline.hpp:32-34) from given world link
+ * transforms world[n*n_links*12] (R column-major, t), e.g. a host FkResult: out as below. */
+int grasp_fine_contact_query_world(grasp_ctx* ctx, int n, const double* world, double* out);
 /* fine_contact_query at states x (pipeline.cpp:320-353): out[g*m*11] =
  * c_w(3) p_w(3) n(3) distance link. */
 int grasp_fine_contact_query(grasp_ctx* ctx, int n, const double* x, double* out);

@@ -109,6 +109,7 @@ SIGNATURES = {
     "grasp_squeeze_pose": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "grasp_forward_kinematics": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp]),
     "grasp_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "grasp_ctx_create_devices": (C.c_int, [_ip, C.c_int, C.POINTER(C.c_void_p)]),
     "grasp_ctx_destroy": (None, [C.c_void_p]),
     "grasp_ctx_set_hand": (C.c_int, [C.c_void_p, C.POINTER(HandDesc)]),
     "grasp_ctx_set_object": (C.c_int, [C.c_void_p, C.POINTER(ObjectDesc)]),
@@ -125,6 +126,7 @@ SIGNATURES = {
                                      _dp, _dp]),
     "grasp_fine_contact_query": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp]),
     "grasp_device_forward_kinematics": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp]),
+    "grasp_fine_contact_query_world": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp]),
     "grasp_ctx_stream": (C.c_void_p, [C.c_void_p]),
     "grasp_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "grasp_ctx_profile": (C.c_int, [C.c_void_p, _dp, C.POINTER(C.c_longlong), C.POINTER(C.c_ulonglong)]),

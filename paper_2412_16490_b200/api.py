@@ -432,9 +432,14 @@ class SynthesisOutput:
 class Engine:
     """One CUDA device, one stream (grasp_ctx). Hand/object uploaded once."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, devices: Optional[List[int]] = None):
+        """devices: shard synthesize over these CUDA devices (grasp_ctx_create_devices)."""
         self._ctx = C.c_void_p()
-        N.check(N.lib().grasp_ctx_create(int(device), C.byref(self._ctx)))
+        if devices:
+            ids = np.ascontiguousarray(devices, dtype=np.int32)
+            N.check(N.lib().grasp_ctx_create_devices(iptr(ids), len(ids), C.byref(self._ctx)))
+        else:
+            N.check(N.lib().grasp_ctx_create(int(device), C.byref(self._ctx)))
         self.hand: Optional[HandModel] = None
         self.obj: Optional[ObjectModel] = None
 

@@ -21,6 +21,7 @@
 #include <numbers>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 using namespace gdev;
@@ -35,6 +36,12 @@ namespace {
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
+};
+
+// A shard's failure re-raised on the calling thread with its status code.
+struct ShardError : std::runtime_error {
+  int status;
+  ShardError(int s, const std::string& m) : std::runtime_error(m), status(s) {}
 };
 
 void ck(cudaError_t e, const char* what) {
@@ -84,6 +91,9 @@ std::vector<double> containing_boxes(const double* obb, const double* verts, con
 
 struct grasp_ctx {
   int device = 0;
+  // Multi-device group (grasp_ctx_create_devices): one single-device context
+  // per device; synthesize shards the batch over them.
+  std::vector<grasp_ctx*> shards;
   cudaStream_t stream = nullptr;
   bool has_hand = false, has_object = false;
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
@@ -948,6 +958,7 @@ struct grasp_ctx {
     });
     launch_qp(P, H.m, 1, 0);
     launch(6, [&] { k_squeeze<<<blocks(st.G, 128), 128, 0, stream>>>(H, st, x_s.p); });
+    launch(6, [&] { k_mask_failed<<<blocks(st.G, 128), 128, 0, stream>>>(H, st, p->n_edges); });
     ck(cudaGetLastError(), "kernel launch");
     collect_profile();
     if (tracing) trace_flush(nv, Mq);
@@ -963,6 +974,8 @@ int guard(F&& f) {
   try {
     f();
     return GRASP_OK;
+  } catch (const ShardError& e) {
+    return fail(e.status, e.what());
   } catch (const CudaError& e) {
     return fail(GRASP_ECUDA, e.what());
   } catch (const grasp::geom::GeometryError& e) {
@@ -975,6 +988,9 @@ int guard(F&& f) {
     return fail(GRASP_EINVAL, e.what());
   }
 }
+
+// Entry points other than synthesize run on a group context's first device.
+grasp_ctx* primary(grasp_ctx* c) { return c && !c->shards.empty() ? c->shards[0] : c; }
 
 void require_models(const grasp_ctx* ctx) {
   if (!ctx) throw std::invalid_argument("null context");
@@ -1003,25 +1019,6 @@ void emit_outputs(grasp_ctx* ctx, const grasp_run_params* p, int G, grasp_out* o
   ck(cudaStreamSynchronize(s), "output sync");
 }
 
-// Failed grasps report NaN energy and no QP fields (pipeline.cpp:312-314).
-void mask_failed_host(const grasp_ctx* ctx, const grasp_run_params* p, int G, grasp_out* out) {
-  if (!out->failed) return;
-  const double nan = std::numeric_limits<double>::quiet_NaN();
-  const int m = ctx->H.m, n = m * p->n_edges;
-  for (int g = 0; g < G; ++g) {
-    if (!out->failed[g]) continue;
-    if (out->energy_total) out->energy_total[g] = nan;
-    if (out->per_direction)
-      for (int j = 0; j < 6; ++j) out->per_direction[6 * g + j] = nan;
-    if (out->contact_forces)
-      for (int i = 0; i < n * 6; ++i) out->contact_forces[static_cast<size_t>(g) * n * 6 + i] = nan;
-    if (out->contacts)
-      for (int i = 0; i < m * 12; ++i) out->contacts[static_cast<size_t>(g) * m * 12 + i] = nan;
-    if (out->qp_converged)
-      for (int j = 0; j < 6; ++j) out->qp_converged[6 * g + j] = 0;
-  }
-}
-
 int synthesize_impl(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0, grasp_out* out,
                     bool device_ptrs) {
   return guard([&] {
@@ -1039,7 +1036,6 @@ int synthesize_impl(grasp_ctx* ctx, const grasp_run_params* p, int batch, const 
     ctx->run(p);
     ctx->check_errors();
     emit_outputs(ctx, p, batch, out, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
-    if (!device_ptrs) mask_failed_host(ctx, p, batch, out);
   });
 }
 
@@ -1058,8 +1054,10 @@ int grasp_ctx_create(int device, grasp_ctx** out) {
     try {
       ctx->set_device();
       ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
-      // Large per-thread stacks for the EPA scratch of k_pairs.
-      ck(cudaDeviceSetLimit(cudaLimitStackSize, 32 * 1024), "stack limit");
+      // No cudaDeviceSetLimit(cudaLimitStackSize): the EPA kernels' local
+      // polytopes are static frames (<= 11.8 KB/thread, ptxas), which the
+      // driver provisions per launch; a device-wide limit would reserve that
+      // for every resident thread of every kernel on the device.
     } catch (...) {
       delete ctx;
       throw;
@@ -1068,28 +1066,89 @@ int grasp_ctx_create(int device, grasp_ctx** out) {
   });
 }
 
-void grasp_ctx_destroy(grasp_ctx* ctx) { delete ctx; }
+int grasp_ctx_create_devices(const int* devices, int n, grasp_ctx** out) {
+  return guard([&] {
+    if (!out || !devices || n < 1) throw std::invalid_argument("need at least one device");
+    std::vector<grasp_ctx*> made;
+    for (int k = 0; k < n; ++k) {
+      grasp_ctx* c = nullptr;
+      const int st = grasp_ctx_create(devices[k], &c);
+      if (st != GRASP_OK) {
+        for (grasp_ctx* m : made) delete m;
+        throw CudaError(grasp::capi::g_last_error);
+      }
+      made.push_back(c);
+    }
+    auto* group = new grasp_ctx();
+    group->device = devices[0];
+    group->shards = made;
+    *out = group;
+  });
+}
+
+void grasp_ctx_destroy(grasp_ctx* ctx) {
+  if (!ctx) return;
+  for (grasp_ctx* s : ctx->shards) delete s;
+  delete ctx;
+}
 
 int grasp_ctx_set_hand(grasp_ctx* ctx, const grasp_hand_desc* hand) {
   return guard([&] {
     if (!ctx || !hand) throw std::invalid_argument("null argument");
-    ctx->set_hand(hand);
+    if (ctx->shards.empty()) ctx->set_hand(hand);
+    for (grasp_ctx* s : ctx->shards) s->set_hand(hand);
   });
 }
 
 int grasp_ctx_set_object(grasp_ctx* ctx, const grasp_object_desc* object) {
   return guard([&] {
     if (!ctx || !object) throw std::invalid_argument("null argument");
-    ctx->set_object(object);
+    if (ctx->shards.empty()) ctx->set_object(object);
+    for (grasp_ctx* s : ctx->shards) s->set_object(object);
   });
 }
 
 int grasp_synthesize(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0, grasp_out* out) {
-  return synthesize_impl(ctx, p, batch, x0, out, false);
+  if (!ctx || ctx->shards.empty()) return synthesize_impl(ctx, p, batch, x0, out, false);
+  return guard([&] {
+    // Contiguous shards [k B / G, (k + 1) B / G), one host thread + stream per
+    // device, results written straight into the caller's rows (pipeline.cpp:443-455
+    // with devices in place of worker threads; grasps are independent, so the
+    // records equal the single-device run's).
+    if (!p || !out || !x0) throw std::invalid_argument("null argument");
+    if (batch <= 0) throw std::invalid_argument("config: batch must be positive");
+    grasp::validate(grasp::capi::to_config(p));
+    const int G = static_cast<int>(ctx->shards.size());
+    const grasp_ctx* s0 = ctx->shards[0];
+    if (!s0->has_hand || !s0->has_object) require_models(s0);
+    const int D = s0->H.D, m = s0->H.m, nv = m * p->n_edges;
+    std::vector<int> status(G, GRASP_OK);
+    std::vector<std::string> message(G);
+    std::vector<std::thread> pool;
+    for (int k = 0; k < G; ++k) {
+      const int lo = static_cast<int>(static_cast<long long>(k) * batch / G);
+      const int hi = static_cast<int>(static_cast<long long>(k + 1) * batch / G);
+      if (hi <= lo) continue;
+      pool.emplace_back([&, k, lo, hi] {
+        auto at = [lo](auto* ptr, size_t per) { return ptr ? ptr + static_cast<size_t>(lo) * per : nullptr; };
+        grasp_out o{at(out->x_p, D), at(out->x, D), at(out->x_s, D), at(out->energy_total, 1),
+                    at(out->per_direction, 6), at(out->contact_forces, static_cast<size_t>(nv) * 6),
+                    at(out->contacts, static_cast<size_t>(m) * 12), at(out->stage_energy, 6), at(out->failed, 1),
+                    at(out->qp_converged, 6)};
+        status[k] = synthesize_impl(ctx->shards[k], p, hi - lo, x0 + static_cast<size_t>(lo) * D, &o, false);
+        if (status[k] != GRASP_OK) message[k] = grasp_last_error();
+      });
+    }
+    for (auto& t : pool) t.join();
+    for (int k = 0; k < G; ++k)
+      if (status[k] != GRASP_OK) throw ShardError(status[k], "device shard " + std::to_string(k) + ": " + message[k]);
+  });
 }
 
 int grasp_synthesize_device(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0_dev,
                             grasp_out* out_dev) {
+  if (ctx && !ctx->shards.empty())
+    return guard([] { throw std::invalid_argument("device-pointer synthesis needs a single-device context"); });
   return synthesize_impl(ctx, p, batch, x0_dev, out_dev, true);
 }
 
@@ -1106,6 +1165,7 @@ void grasp_eval_params_default(grasp_eval_params* e) {
 
 int grasp_eval(grasp_ctx* ctx, const grasp_run_params* p, const grasp_eval_params* e, int n, const double* x,
                const double* x_s, double* out_real, int* out_int) {
+  ctx = primary(ctx);
   return guard([&] {
     if (!p || !e || !x || !x_s || !out_real || !out_int) throw std::invalid_argument("null argument");
     require_models(ctx);
@@ -1124,9 +1184,21 @@ int grasp_eval(grasp_ctx* ctx, const grasp_run_params* p, const grasp_eval_param
     self_d.ensure(static_cast<size_t>(n) * std::max(ctx->H.ncp, 1));
     pd.ensure(n);
     spd.ensure(n);
-    if (ctx->H.ncp > 0)
-      k_eval_self_pairs<<<grasp_ctx::blocks(static_cast<long long>(n) * ctx->H.ncp, 128), 128, 0, s>>>(ctx->H, ctx->st,
+    if (ctx->H.ncp > 0) {
+      // Overflowing self pairs are queued in the pair-overflow list and redone with the
+      // full-capacity EPA scratch (the object pairs' queue is drained by now).
+      const size_t need = static_cast<size_t>(n) * ctx->H.ncp;
+      if (need > static_cast<size_t>(ctx->st.ovf_cap)) {
+        ctx->ovf_list.ensure(need);
+        ctx->st.ovf_list = ctx->ovf_list.p;
+        ctx->st.ovf_cap = static_cast<int>(need);
+      }
+      const DevState ss = ctx->st;
+      ck(cudaMemsetAsync(ctx->ovf_count.p, 0, sizeof(int), s), "memset");
+      k_eval_self_pairs<<<grasp_ctx::blocks(static_cast<long long>(n) * ctx->H.ncp, 128), 128, 0, s>>>(ctx->H, ss,
                                                                                                    self_d.p);
+      k_eval_self_pairs_big<<<grasp_ctx::kBigSlots / 128, 128, 0, s>>>(ctx->H, ss, self_d.p);
+    }
     k_eval_depths<<<grasp_ctx::blocks(n, 128), 128, 0, s>>>(ctx->H, ctx->O, ctx->st, self_d.p, pd.p, spd.p);
     ctx->launch_queries(true);
     ctx->launch_pairs(true);
@@ -1248,6 +1320,7 @@ int grasp_eval(grasp_ctx* ctx, const grasp_run_params* p, const grasp_eval_param
 int grasp_qp_batch(grasp_ctx* ctx, const grasp_run_params* p, int n_grasps, int m, const double* frames,
                    const double* warm_x, const double* warm_y, double* X, double* Y, double* Z, int* iters,
                    int* converged, double* per_direction, int device_ptrs) {
+  ctx = primary(ctx);
   return guard([&] {
     if (!ctx || !p || !frames) throw std::invalid_argument("null argument");
     if (m < 1 || m > kMaxTips) throw std::invalid_argument("grasp energy needs 1..5 contacts on device");
@@ -1287,6 +1360,7 @@ int grasp_qp_batch(grasp_ctx* ctx, const grasp_run_params* p, int n_grasps, int 
 }
 
 int grasp_point_to_mesh(grasp_ctx* ctx, int n, const double* points, double* out) {
+  ctx = primary(ctx);
   return guard([&] {
     if (!ctx || !ctx->has_object) throw std::invalid_argument("no object uploaded");
     ctx->set_device();
@@ -1303,6 +1377,7 @@ int grasp_point_to_mesh(grasp_ctx* ctx, int n, const double* points, double* out
 
 int grasp_signed_distance(grasp_ctx* ctx, int n, const int* link_ids, const int* part_ids, const double* poses,
                           double* out) {
+  ctx = primary(ctx);
   return guard([&] {
     require_models(ctx);
     ctx->set_device();
@@ -1324,6 +1399,7 @@ int grasp_signed_distance(grasp_ctx* ctx, int n, const int* link_ids, const int*
 
 int grasp_total_energy(grasp_ctx* ctx, const grasp_run_params* p, int stage, int n, const double* x,
                        const double* anchors, double* warm_x, double* warm_y, double* energy, double* grad) {
+  ctx = primary(ctx);
   return guard([&] {
     require_models(ctx);
     if (stage < 0 || stage > 2) throw std::invalid_argument("stage must be 0, 1 or 2");
@@ -1368,6 +1444,7 @@ int grasp_total_energy(grasp_ctx* ctx, const grasp_run_params* p, int stage, int
 }
 
 int grasp_device_forward_kinematics(grasp_ctx* ctx, int n, const double* x, double* out) {
+  ctx = primary(ctx);
   return guard([&] {
     if (!ctx || !ctx->has_hand) throw std::invalid_argument("no hand uploaded");
     if (n < 0 || (n > 0 && (!x || !out))) throw std::invalid_argument("null argument");
@@ -1394,7 +1471,39 @@ int grasp_device_forward_kinematics(grasp_ctx* ctx, int n, const double* x, doub
   });
 }
 
+int grasp_fine_contact_query_world(grasp_ctx* ctx, int n, const double* world, double* out) {
+  ctx = primary(ctx);
+  return guard([&] {
+    require_models(ctx);
+    if (n < 0 || (n > 0 && (!world || !out))) throw std::invalid_argument("null argument");
+    if (n == 0) return;
+    ctx->set_device();
+    ctx->ensure_state(n, ctx->H.m, 8);
+    ctx->reset_run_state(n);
+    cudaStream_t s = ctx->stream;
+    const int L = ctx->H.L;
+    // caller layout R column-major -> device layout R row-major
+    std::vector<double> w(static_cast<size_t>(n) * L * 12);
+    for (size_t t = 0; t < static_cast<size_t>(n) * L; ++t)
+      for (int i = 0; i < 3; ++i) {
+        for (int c = 0; c < 3; ++c) w[12 * t + 3 * i + c] = world[12 * t + 3 * c + i];
+        w[12 * t + 9 + i] = world[12 * t + 9 + i];
+      }
+    ck(cudaMemcpyAsync(ctx->world.p, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice, s), "world");
+    k_tip_points<<<grasp_ctx::blocks(static_cast<long long>(n) * ctx->H.m, 128), 128, 0, s>>>(ctx->H, ctx->st);
+    ctx->launch_queries(true);
+    ctx->launch_pairs(true);
+    k_final_frames<<<grasp_ctx::blocks(static_cast<long long>(n) * ctx->H.m, 128), 128, 0, s>>>(ctx->H, ctx->O, ctx->st,
+                                                                                              ctx->witness.p);
+    ck(cudaGetLastError(), "launch");
+    ctx->check_errors();
+    copy_out(out, ctx->witness.p, sizeof(double) * n * ctx->H.m * 11, cudaMemcpyDeviceToHost, s);
+    ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
 int grasp_fine_contact_query(grasp_ctx* ctx, int n, const double* x, double* out) {
+  ctx = primary(ctx);
   return guard([&] {
     require_models(ctx);
     ctx->set_device();
@@ -1542,9 +1651,13 @@ __global__ void k_fp64_peak(double* out, int iters) {
 
 extern "C" {
 
-void* grasp_ctx_stream(grasp_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+void* grasp_ctx_stream(grasp_ctx* ctx) {
+  ctx = primary(ctx);
+  return ctx ? static_cast<void*>(ctx->stream) : nullptr;
+}
 
 int grasp_ctx_set_profiling(grasp_ctx* ctx, int on) {
+  ctx = primary(ctx);
   return guard([&] {
     if (!ctx) throw std::invalid_argument("null context");
     ctx->set_device();
@@ -1562,6 +1675,7 @@ int grasp_ctx_set_profiling(grasp_ctx* ctx, int on) {
 }
 
 int grasp_ctx_profile(grasp_ctx* ctx, double* ms, long long* launches, unsigned long long* ops) {
+  ctx = primary(ctx);
   return guard([&] {
     if (!ctx) throw std::invalid_argument("null context");
     ctx->set_device();
@@ -1577,6 +1691,7 @@ int grasp_ctx_profile(grasp_ctx* ctx, double* ms, long long* launches, unsigned 
 }
 
 int grasp_ctx_set_trace(grasp_ctx* ctx, const grasp_trace* t) {
+  ctx = primary(ctx);
   return guard([&] {
     if (!ctx) throw std::invalid_argument("null context");
     ctx->tracing = false;
@@ -1601,6 +1716,8 @@ long long grasp_ctx_launch_count(grasp_ctx* ctx) {
   long long n = 0;
   if (ctx)
     for (long long v : ctx->launches) n += v;
+  if (ctx)
+    for (grasp_ctx* sh : ctx->shards) n += grasp_ctx_launch_count(sh);
   return n;
 }
 

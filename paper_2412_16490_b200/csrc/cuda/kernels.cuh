@@ -1188,10 +1188,12 @@ __global__ void k_pairs_raw(DevHand H, DevObject O, int n, const int* __restrict
 // Grasp evaluation (eval.cpp:51-89) on the state in st.x / st.world.
 // Self-penetration pairs: signed_distance(link a posed, link b posed)
 // (eval.cpp:63-72; geometry.cpp:500-525 with both poses), one thread per
-// (grasp, collision pair); d written to out[g * ncp + i].
-__global__ void __launch_bounds__(128) k_eval_self_pairs(DevHand H, DevState st, double* out) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)st.G * H.ncp) return;
+// (grasp, collision pair); d written to out[g * ncp + i]. Pairs whose EPA
+// polytope outgrows the small per-thread scratch are queued (st.ovf_list) and
+// redone by k_eval_self_pairs_big with the reference's full 512-iteration
+// capacity, like k_pairs_big for object pairs.
+template <class Scratch>
+__device__ PairResult self_pair_distance(const DevHand& H, const DevState& st, long long t, Scratch& scratch) {
   const int g = (int)(t / H.ncp), i = (int)(t % H.ncp);
   const int la = H.cp_a[i], lb = H.cp_b[i];
   Hull A, B;
@@ -1214,11 +1216,36 @@ __global__ void __launch_bounds__(128) k_eval_self_pairs(DevHand H, DevState st,
   double scale = 1.0;
   scale = fmax(scale, scale_of(mul(Ra, ld3(H.link_centroid + 3 * la)) + ta, H.link_halfnorm[la]));
   scale = fmax(scale, scale_of(mul(Rb, ld3(H.link_centroid + 3 * lb)) + tb, H.link_halfnorm[lb]));
+  return signed_distance(A, B, scale, scratch);
+}
+
+__global__ void __launch_bounds__(128) k_eval_self_pairs(DevHand H, DevState st, double* out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)st.G * H.ncp) return;
   EpaScratch scratch;
-  const PairResult r = signed_distance(A, B, scale, scratch);
+  const PairResult r = self_pair_distance(H, st, t, scratch);
+  if (r.flags & kPairOverflow) {
+    const int k = atomicAdd(st.ovf_count, 1);
+    if (k < st.ovf_cap) st.ovf_list[k] = (int)t;
+    else atomicAdd(st.err + 1, 1);
+    return;
+  }
   if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
-  if (r.flags & kPairOverflow) atomicAdd(st.err + 1, 1);
   out[t] = r.d;
+}
+
+__global__ void __launch_bounds__(128) k_eval_self_pairs_big(DevHand H, DevState st, double* out) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int count = min(*st.ovf_count, st.ovf_cap);
+  if (tid >= st.big_slots) return;
+  EpaScratchBig& scratch = static_cast<EpaScratchBig*>(st.big_scratch)[tid];
+  for (int i = tid; i < count; i += st.big_slots) {
+    const long long t = st.ovf_list[i];
+    const PairResult r = self_pair_distance(H, st, t, scratch);
+    if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
+    if (r.flags & kPairOverflow) atomicAdd(st.err + 1, 1);
+    out[t] = r.d;
+  }
 }
 
 // Per grasp: penetration depth over every (link, part) pair record and
@@ -1661,6 +1688,36 @@ __global__ void k_final_frames(DevHand H, DevObject O, DevState st, double* witn
     o[9] = wt.d;
     o[10] = l;
   }
+}
+
+// Failed grasps report NaN energy and no QP fields (pipeline.cpp:312-314):
+// the record buffers of failed rows are overwritten on the device, so host
+// and device outputs of grasp_synthesize carry the same values.
+__global__ void k_mask_failed(DevHand H, DevState st, int n_edges) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= st.G || !st.failed[g]) return;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  const int n = H.m * n_edges;
+  st.qp_energy[g] = nan;
+  for (int j = 0; j < 6; ++j) {
+    st.qp_perdir[(size_t)g * 6 + j] = nan;
+    st.qp_conv[(size_t)g * 6 + j] = 0;
+  }
+  for (int i = 0; i < n * 6; ++i) st.warm_x[(size_t)g * n * 6 + i] = nan;
+  for (int i = 0; i < H.m * 12; ++i) st.frames[(size_t)g * H.m * 12 + i] = nan;
+}
+
+// Fingertip-centre query points from given world link transforms (the
+// FkResult overload of fine_contact_query, pipeline.cpp:326-330).
+__global__ void k_tip_points(DevHand H, DevState st) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= st.G * H.m) return;
+  const int g = t / H.m, f = t % H.m;
+  const double* w = st.world + ((size_t)g * H.L + H.tip_link[f]) * 12;
+  M33 Rw;
+  for (int i = 0; i < 9; ++i) Rw.m[i] = w[i];
+  const D3 c = mul(Rw, ld3(H.proxy + 4 * H.tip_proxy[f])) + ld3(w + 9);
+  st3(st.qpts + ((size_t)g * st.NQ + H.tip_proxy[f]) * 3, c);
 }
 
 // x_p fallback and squeeze (pipeline.cpp:296-300, 426-434).

@@ -3,6 +3,8 @@
 #include <cctype>
 #include <cerrno>
 #include <charconv>
+#include <locale.h>
+#include <stdlib.h>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -237,8 +239,17 @@ class Parser {
       while (pos_ < s_.size() && std::isdigit(static_cast<unsigned char>(s_[pos_]))) ++pos_;
     }
     const std::string tok = s_.substr(start, pos_ - start);
-    errno = 0;
-    const double d = std::strtod(tok.c_str(), nullptr);
+    // Locale-free and correctly rounded (like nlohmann's lexer, whatever
+    // LC_NUMERIC the host application set); out-of-range magnitudes saturate
+    // like strtod in the "C" locale.
+    double d = 0.0;
+    const auto fr = std::from_chars(tok.data(), tok.data() + tok.size(), d);
+    if (fr.ec == std::errc::result_out_of_range) {
+      static const locale_t c_locale = newlocale(LC_ALL_MASK, "C", static_cast<locale_t>(0));
+      d = strtod_l(tok.c_str(), nullptr, c_locale);
+    } else if (fr.ec != std::errc()) {
+      fail("bad number");
+    }
     Value v = Value::make_number(d, false, 0);
     if (integral) {
       std::int64_t i = 0;

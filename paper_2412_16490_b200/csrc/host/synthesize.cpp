@@ -64,12 +64,17 @@ void check(int status) {
   }
 }
 
-CachedCtx& context_for(int device) {
-  thread_local std::map<int, CachedCtx> cache;
-  CachedCtx& c = cache[device];
+// One context per (thread, device list): a single device, or a multi-device
+// group (grasp_ctx_create_devices) for the sharded overload of synthesize.
+CachedCtx& context_for(const std::vector<int>& devices) {
+  thread_local std::map<std::vector<int>, CachedCtx> cache;
+  CachedCtx& c = cache[devices];
   if (!c.ctx) {
     grasp_ctx* raw = nullptr;
-    check(grasp_ctx_create(device, &raw));
+    if (devices.size() == 1)
+      check(grasp_ctx_create(devices[0], &raw));
+    else
+      check(grasp_ctx_create_devices(devices.data(), static_cast<int>(devices.size()), &raw));
     c.ctx.reset(raw);
   }
   return c;
@@ -77,8 +82,9 @@ CachedCtx& context_for(int device) {
 
 }  // namespace
 
-CachedCtx& bound_context(const hand::HandModel& model, const object::ObjectModel& object, int device) {
-  CachedCtx& c = context_for(device);
+CachedCtx& bound_context(const hand::HandModel& model, const object::ObjectModel& object,
+                         const std::vector<int>& devices) {
+  CachedCtx& c = context_for(devices);
   capi::PackedHand ph = capi::pack_hand(model);
   if (!c.has_hand || !same_content(ph, c.packed_hand)) {
     c.has_hand = false;
@@ -97,10 +103,17 @@ CachedCtx& bound_context(const hand::HandModel& model, const object::ObjectModel
   return c;
 }
 
-std::vector<records::GraspRecord> synthesize(const hand::HandModel& model, const object::ObjectModel& object,
-                                             const RunConfig& cfg, int device) {
+CachedCtx& bound_context(const hand::HandModel& model, const object::ObjectModel& object, int device) {
+  return bound_context(model, object, std::vector<int>{device});
+}
+
+namespace {
+
+std::vector<records::GraspRecord> synthesize_on(const hand::HandModel& model, const object::ObjectModel& object,
+                                                const RunConfig& cfg, const std::vector<int>& devices) {
   validate(cfg);
-  CachedCtx& c = bound_context(model, object, device);
+  if (devices.empty()) throw std::invalid_argument("synthesize: empty device list");
+  CachedCtx& c = bound_context(model, object, devices);
   const int B = cfg.batch, D = 12 + model.dof(), m = static_cast<int>(model.fingertip_links.size());
   const int n = m * cfg.contact.n_edges;
   const std::vector<VectorXd> starts = init_poses(model, object, B, cfg.seed, cfg.init);
@@ -159,7 +172,106 @@ std::vector<records::GraspRecord> synthesize(const hand::HandModel& model, const
   return recs;
 }
 
+}  // namespace
+
+std::vector<records::GraspRecord> synthesize(const hand::HandModel& model, const object::ObjectModel& object,
+                                             const RunConfig& cfg, int device) {
+  return synthesize_on(model, object, cfg, {device});
+}
+
+std::vector<records::GraspRecord> synthesize(const hand::HandModel& model, const object::ObjectModel& object,
+                                             const RunConfig& cfg, std::span<const int> devices) {
+  return synthesize_on(model, object, cfg, std::vector<int>(devices.begin(), devices.end()));
+}
+
+std::vector<ContactWitness> fine_contact_query(const hand::HandModel& model, const hand::FkResult& fk,
+                                               const object::ObjectModel& object, int device) {
+  const int L = static_cast<int>(model.links.size()), m = static_cast<int>(model.fingertip_links.size());
+  if (static_cast<int>(fk.world.size()) != L) throw std::invalid_argument("fine_contact_query: FkResult size");
+  CachedCtx& c = bound_context(model, object, device);
+  std::vector<double> world(static_cast<size_t>(L) * 12), out(static_cast<size_t>(m) * 11);
+  for (int l = 0; l < L; ++l) {
+    std::copy(fk.world[l].R.m, fk.world[l].R.m + 9, world.begin() + 12 * l);  // column-major
+    world[12 * l + 9] = fk.world[l].t.x;
+    world[12 * l + 10] = fk.world[l].t.y;
+    world[12 * l + 11] = fk.world[l].t.z;
+  }
+  check(grasp_fine_contact_query_world(c.ctx.get(), 1, world.data(), out.data()));
+  std::vector<ContactWitness> ws(m);
+  for (int f = 0; f < m; ++f) {
+    const double* o = out.data() + 11 * f;
+    ws[f].c_w = Vec3(o[0], o[1], o[2]);
+    ws[f].p_w = Vec3(o[3], o[4], o[5]);
+    ws[f].n = Vec3(o[6], o[7], o[8]);
+    ws[f].distance = o[9];
+    ws[f].link = static_cast<int>(o[10]);
+  }
+  return ws;
+}
+
+double coarse_distance_energy(const hand::HandModel& model, const VectorXd& x, const object::ObjectModel& object,
+                              double offset, double fd_step, VectorXd* grad, int device) {
+  const int D = 12 + model.dof();
+  if (static_cast<int>(x.size()) != D) throw hand::HandError("state vector has wrong size for this hand");
+  CachedCtx& c = bound_context(model, object, device);
+  // The coarse-stage total_energy with every weight but the distance term's at
+  // zero is exactly coarse_distance_energy (pipeline.cpp:133-163 vs :355-380):
+  // the other terms enter as 0 * finite = +0 and the tip force is 2 r (n - dp^T n).
+  grasp_run_params p;
+  grasp_run_params_default(&p);
+  p.w_grasp = p.w_joint_limit = p.w_self_penetration = p.w_object_penetration = 0.0;
+  p.w_distance = 1.0;
+  p.contact_offset = offset;
+  p.fd_step = fd_step;
+  double e = 0.0;
+  std::vector<double> g(D);
+  check(grasp_total_energy(c.ctx.get(), &p, 0, 1, x.data(), nullptr, nullptr, nullptr, &e, g.data()));
+  if (grad) *grad = g;
+  return e;
+}
+
+energy::SurrogateResult fine_grasp_surrogate(const hand::HandModel& model, const VectorXd& x,
+                                             std::span<const ContactWitness> witnesses,
+                                             std::span<const Vec3> anchors) {
+  Mat3 raw;
+  for (int i = 0; i < 9; ++i) raw.m[i] = x.at(i);
+  const hand::PoseState ps = hand::make_pose_state(raw);
+  const hand::HandPose pose = hand::pose_from_state(model, x);
+  const hand::FkResult fk = hand::forward_kinematics(model, pose);
+  std::vector<Vec3> points;
+  std::vector<MatrixXd> jac;
+  for (const ContactWitness& w : witnesses) {
+    points.push_back(w.c_w);
+    jac.push_back(hand::point_jacobian(model, ps, pose, fk, w.link, w.c_w));
+  }
+  return energy::fine_stage_surrogate(points, anchors, jac);
+}
+
 }  // namespace grasp::pipeline
+
+namespace grasp::energy {
+
+SurrogateResult fine_stage_surrogate(std::span<const Vec3> points, std::span<const Vec3> anchors,
+                                     std::span<const MatrixXd> jacobians) {
+  if (points.size() != anchors.size()) throw std::invalid_argument("point and anchor counts differ");
+  if (!jacobians.empty() && jacobians.size() != points.size())
+    throw std::invalid_argument("need one Jacobian per point when given");
+  SurrogateResult out;
+  const int dims = jacobians.empty() ? 0 : jacobians[0].cols();
+  out.gradient.assign(dims, 0.0);
+  for (size_t i = 0; i < points.size(); ++i) {
+    const Vec3 diff = points[i] - anchors[i];
+    out.value += squared_norm(diff);
+    if (jacobians.empty()) continue;
+    if (jacobians[i].rows() != 3 || jacobians[i].cols() != dims)
+      throw std::invalid_argument("point Jacobians must be 3 x dims");
+    for (int c = 0; c < dims; ++c)
+      out.gradient[c] += 2.0 * (jacobians[i](0, c) * diff.x + jacobians[i](1, c) * diff.y + jacobians[i](2, c) * diff.z);
+  }
+  return out;
+}
+
+}  // namespace grasp::energy
 
 namespace grasp::eval {
 namespace {

@@ -6,6 +6,8 @@
 #pragma once
 
 #include <cmath>
+#include <stdexcept>
+#include <vector>
 
 namespace grasp {
 
@@ -100,6 +102,32 @@ inline Mat3 outer(const Vec3& a, const Vec3& b) {
     for (int j = 0; j < 3; ++j) r(i, j) = a[i] * b[j];
   return r;
 }
+
+inline Mat3 skew(const Vec3& v) {
+  Mat3 m = Mat3::Zero();
+  m(0, 1) = -v.z;
+  m(0, 2) = v.y;
+  m(1, 0) = v.z;
+  m(1, 2) = -v.x;
+  m(2, 0) = -v.y;
+  m(2, 1) = v.x;
+  return m;
+}
+
+/// Dynamic dense matrix, column-major like Eigen::MatrixXd (Jacobians are
+/// 3 x (12 + dof), reference hand.hpp:111-121).
+struct MatrixXd {
+  int n_rows = 0, n_cols = 0;
+  std::vector<double> data;
+  MatrixXd() = default;
+  MatrixXd(int r, int c) : n_rows(r), n_cols(c), data(static_cast<size_t>(r) * c, 0.0) {}
+  static MatrixXd Zero(int r, int c) { return MatrixXd(r, c); }
+  int rows() const { return n_rows; }
+  int cols() const { return n_cols; }
+  double& operator()(int r, int c) { return data[static_cast<size_t>(c) * n_rows + r]; }
+  double operator()(int r, int c) const { return data[static_cast<size_t>(c) * n_rows + r]; }
+  Vec3 col3(int c) const { return {(*this)(0, c), (*this)(1, c), (*this)(2, c)}; }
+};
 
 /// Rigid transform p' = R p + t (reference: proj/include/grasp/geometry.hpp:17-28).
 struct RigidTransform {

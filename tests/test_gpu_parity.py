@@ -441,6 +441,42 @@ def test_eval_matches_oracle(G, O, engine):
     np.testing.assert_allclose(got["residuals"], ref["residuals"], atol=1e-6 * mg, rtol=1e-6)
 
 
+def ball_points(r, n=300):
+    golden = np.pi * (3.0 - np.sqrt(5.0))
+    k = np.arange(n)
+    z = 1.0 - 2.0 * (k + 0.5) / n
+    rr = np.sqrt(np.maximum(1.0 - z * z, 0.0))
+    return np.stack([r * rr * np.cos(golden * k), r * rr * np.sin(golden * k), r * z], 1)
+
+
+def test_eval_self_pairs_with_large_epa_polytopes(G, O, engine):
+    """Self-penetration depth (eval.cpp:63-72) between two deeply overlapping 300-vertex round
+    links: EPA needs far more than the 64-vertex per-thread polytope, so those pairs go through
+    the full-capacity retry (k_eval_self_pairs_big) and still match the oracle."""
+    import json
+    ball = ball_points(0.03).round(6).tolist()
+    tiny = [[x * 0.004, y * 0.004, z * 0.004] for x in (-1, 1) for y in (-1, 1) for z in (-1, 1)]
+    doc = {"format_version": 1, "name": "balls", "links": [
+        {"name": "palm", "vertices": ball, "proxies": [{"center": [0, 0, 0], "radius": 0.03}]},
+        {"name": "stem", "vertices": tiny, "joint": {"parent": "palm", "origin": [0, 0, 0.05], "axis": [1, 0, 0],
+                                                      "lower": -0.5, "upper": 0.5}},
+        {"name": "tip", "vertices": ball, "proxies": [{"center": [0, 0, 0], "radius": 0.03}], "tip_proxy": 0,
+         "joint": {"parent": "stem", "origin": [0, 0, -0.03], "axis": [1, 0, 0], "lower": -0.5, "upper": 0.5}}]}
+    hand = G.HandModel.from_json(json.dumps(doc))
+    assert hand.n_pairs == 1
+    obj = G.make_primitive("sphere", 0.1)
+    use(engine, hand, obj)
+    rng = np.random.default_rng(12)
+    x = np.zeros((64, hand.dims()))
+    x[:, [0, 4, 8]] = 1.0
+    x[:, 9:12] = [0.0, 0.0, 0.5]
+    x[:, 12:] = rng.uniform(-0.3, 0.3, size=(64, 2))
+    ref = O.evaluate(hand, obj, G.RunConfig(), x, x)
+    got = engine.evaluate(G.RunConfig(), x, x)
+    assert (ref["spd_mm"] > 30).all()
+    np.testing.assert_allclose(got["spd_mm"], ref["spd_mm"], atol=1e-6, rtol=0)
+
+
 def test_fine_contact_query_matches_oracle(G, O, trident, engine):
     obj = G.make_primitive("box", 0.1)
     use(engine, trident, obj)
@@ -694,6 +730,52 @@ def test_synthesis_deterministic_and_batch_prefix_independent(G, trident, engine
         p = engine.synthesize(cfg, np.ascontiguousarray(x0[:k]))
         for f in ("x", "x_p", "x_s", "energy_total", "failed"):
             assert np.array_equal(getattr(p, f), getattr(a, f)[:k], equal_nan=True), (k, f)
+
+
+def test_multi_device_context_equals_single_device(G, trident, engine):
+    """grasp_ctx_create_devices: contiguous shards on their own host threads
+    and streams (here three shards on cuda:0) give bitwise the single-context records."""
+    obj = G.make_primitive("capsule", 0.09)
+    use(engine, trident, obj)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 13, 9
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 40, 15, 15
+    x0 = G.init_poses(trident, obj, cfg.batch, cfg.seed, cfg.init)
+    one = engine.synthesize(cfg, x0)
+    multi = G.Engine(devices=[0, 0, 0])
+    multi.set_hand(trident)
+    multi.set_object(obj)
+    many = multi.synthesize(cfg, x0)
+    for f in ("x", "x_p", "x_s", "energy_total", "per_direction", "contact_forces", "contacts", "stage_energy",
+              "failed", "qp_converged"):
+        assert np.array_equal(getattr(one, f), getattr(many, f), equal_nan=True), f
+
+
+def test_failed_rows_masked_on_device_outputs(G, trident, engine):
+    """Failed grasps report NaN energy / forces / contacts and unconverged flags on the
+    device-pointer path too (pipeline.cpp:312-314), not stale buffer contents."""
+    import torch
+    sphere = G.make_primitive("sphere", 0.1)
+    use(engine, trident, sphere)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 4, 17
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 30, 10, 10
+    x0 = G.init_poses(trident, sphere, 4, 17, cfg.init)
+    engine.synthesize(cfg, x0)  # leaves finite values in the engine's buffers
+    cfg.pipeline.coarse.step_translation = 1e5
+    D, m, n = trident.dims(), trident.n_tips, trident.n_tips * cfg.contact.n_edges
+    dev = torch.device("cuda:0")
+    xd = torch.from_numpy(x0).to(dev)
+    outs = dict(energy_total=torch.zeros(4, dtype=torch.float64, device=dev),
+                contact_forces=torch.zeros(4 * n * 6, dtype=torch.float64, device=dev),
+                contacts=torch.zeros(4 * m * 12, dtype=torch.float64, device=dev),
+                failed=torch.zeros(4, dtype=torch.int32, device=dev),
+                qp_converged=torch.ones(4 * 6, dtype=torch.int32, device=dev))
+    engine.synthesize_device(cfg, xd.data_ptr(), 4, {k: v.data_ptr() for k, v in outs.items()})
+    torch.cuda.synchronize()
+    assert (outs["failed"].cpu().numpy() != 0).all()
+    assert torch.isnan(outs["energy_total"]).all() and torch.isnan(outs["contact_forces"]).all()
+    assert torch.isnan(outs["contacts"]).all() and (outs["qp_converged"] == 0).all()
 
 
 def test_diverging_grasps_are_flagged_on_device(G, O, trident, engine):
