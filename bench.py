@@ -123,59 +123,95 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def roofline(prof, hand, cfg, peak_tflops):
-    """Dominant kernel class by device time; achieved = algorithmic flops
-    (SURVEY.md 8(d) constants x op counters of this run) / its time."""
-    ms = prof["ms"]
-    dom = max(ms, key=ms.get)
-    ops = prof["ops"]
+# ncu --set full captures (profiles/) that give each kernel class's DRAM traffic per launch.
+NCU_CAPTURES = {
+    "pairs": "profiles/r02_ncu_pairs_list_full.json",
+    "qp": "profiles/r02_ncu_qp_full.json",
+    "point_query": "profiles/r02_ncu_point_query_full.json",
+}
+
+
+def class_flops(ops, hand, cfg, n_steps_iters):
+    """Algorithmic flops per kernel class: SURVEY.md 8(d) constants x this run's op counters
+    (FMA = 2). Step kernels: FK 160/link + proxy transform 20/proxy + self pair 10/pair +
+    apply_step 5D per grasp-iteration (their point-Jacobian work is replaced by wrench sums)."""
     m = hand.n_tips
     n = m * cfg.contact.n_edges
     M = m + 1 + n
-    flops = {
+    L, S, D = hand.n_links, len(hand.proxies), hand.dims()
+    nsp = int(getattr(hand, "n_sphere_pairs", 0))
+    per_grasp_iter = 160.0 * L + 20.0 * S + 10.0 * nsp + 5.0 * D
+    coarse_gi, mesh_gi = n_steps_iters
+    return {
         "point_query": 7.0 * ops["plane_tests"] + 64.0 * ops["triangle_tests"],
         "qp": (45.0 * n + 6.0 * M + 100.0 + 3.0 * n) * ops["qp_column_sweeps"] + (80.0 * n + 400.0) * ops["qp_solves"],
         "pairs": 6.0 * ops["support_verts"] + 200.0 * ops["gjk_iters"] + 200.0 * ops["epa_iters"],
+        "step_coarse": per_grasp_iter * coarse_gi,
+        "step_mesh": per_grasp_iter * mesh_gi,
     }
-    f = flops.get(dom)
+
+
+def roofline(prof, hand, cfg, peak_tflops, batch):
+    """Per kernel class: achieved = algorithmic flops / its CUDA-event time; the dominant class
+    (by device time) is the headline block, every class is listed under "kernels"."""
+    ms = prof["ms"]
+    ops = prof["ops"]
+    it = (cfg.pipeline.coarse.iters + 1, cfg.pipeline.fine.iters + cfg.pipeline.final_stage.iters + 2)
+    flops = class_flops(ops, hand, cfg, (batch * it[0], batch * it[1]))
     total_ms = sum(ms.values())
-    if f is None or ms[dom] <= 0:
-        return dom, None
-    achieved = f / (ms[dom] * 1e-3) / 1e12
-    # DRAM traffic per launch of the dominant kernel from the committed
-    # `ncu --set full` capture (profiles/), when one exists for it.
-    traffic, traffic_src = None, None
-    cap = {"qp": "profiles/r01_ncu_qp_full_v10.json", "pairs": "profiles/r01_ncu_pairs_list_full_v7.json"}.get(dom)
-    if cap and (ROOT / cap).exists():
-        traffic = json.loads((ROOT / cap).read_text()).get("traffic_bytes_per_launch")
-        traffic_src = cap + " (dram__bytes_read.sum + dram__bytes_write.sum, bytes per launch)"
+    kernels = {}
+    for cls, f in flops.items():
+        t = ms.get(cls, 0.0)
+        if t <= 0:
+            continue
+        achieved = f / (t * 1e-3) / 1e12
+        traffic = None
+        cap = NCU_CAPTURES.get(cls)
+        if cap and (ROOT / cap).exists():
+            traffic = json.loads((ROOT / cap).read_text()).get("traffic_bytes_per_launch")
+        kernels[cls] = {"achieved": round(achieved, 3), "frac": round(achieved / peak_tflops, 4),
+                        "ms": round(t, 2), "share_of_step": round(t / total_ms, 3), "traffic": traffic,
+                        "traffic_source": cap if traffic is not None else None}
+    dom = max((c for c in kernels), key=lambda c: kernels[c]["ms"])
+    k = kernels[dom]
     return dom, {
         "bound": "fp64",
         "kernel": dom,
-        "achieved": round(achieved, 3),
+        "achieved": k["achieved"],
         "peak": round(peak_tflops, 3),
         "unit": "TFLOP/s",
-        "frac": round(achieved / peak_tflops, 4),
-        "traffic": traffic,
-        "traffic_source": traffic_src,
-        "share_of_step": round(ms[dom] / total_ms, 3),
+        "frac": k["frac"],
+        "traffic": k["traffic"],
+        "traffic_source": (k["traffic_source"] + " (dram__bytes_read.sum + dram__bytes_write.sum, bytes per "
+                           "launch)") if k["traffic_source"] else None,
+        "share_of_step": k["share_of_step"],
         "peak_source": "measured fp64 FMA micro-benchmark on this GPU (MEASURED_PEAKS.json has no fp64 entry)",
         "flop_model": "SURVEY 8(d): plane test 7, closest-on-triangle 64, ADMM column-sweep 45n+6M+100+3n, "
-                      "QP setup 80n+400, support vertex 6, GJK/EPA iteration 200",
-        "kernel_ms": {k: round(v, 2) for k, v in ms.items()},
+                      "QP setup 80n+400, support vertex 6, GJK/EPA iteration 200; step kernels FK 160/link, "
+                      "proxy 20, self pair 10, apply_step 5D per grasp-iteration",
+        "kernels": kernels,
+        "kernel_ms": {c: round(v, 2) for c, v in ms.items()},
         "ops": ops,
     }
 
 
-def cpu_baseline(G, hand, obj, cfg, threads, n_grasps):
+def cpu_baseline(G, hand, obj, cfg, threads):
+    """The oracle port on the host: 4 grasps per host thread on all threads (the reference's
+    strided std::thread scheme, pipeline.cpp:443-455), plus a workers = 1 figure on 2 grasps."""
     from oracle import oracle as O
+    n_grasps = 4 * threads
     x0 = G.init_poses(hand, obj, n_grasps, SEED)
     t0 = time.perf_counter()
     O.synthesize(hand, obj, cfg, x0, workers=threads)
     dt = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    O.synthesize(hand, obj, cfg, x0[:2], workers=1)
+    dt1 = time.perf_counter() - t1
     return {"value": round(n_grasps / dt, 4), "unit": "grasps/s", "cores": threads, "kind": "port",
             "sample": "%d grasps (full schedule) of the same workload on %d host threads, %.1f s" % (
-                n_grasps, threads, dt)}
+                n_grasps, threads, dt),
+            "workers_1": {"value": round(2 / dt1, 4), "unit": "grasps/s", "cores": 1,
+                          "sample": "2 grasps (full schedule) on one host thread, %.1f s" % dt1}}
 
 
 def run_reference(args):
@@ -336,7 +372,7 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         prof = eng.profile()
         eng.set_profiling(False)
-        _, rl = roofline(prof, hand, shard_cfg, peak)
+        _, rl = roofline(prof, hand, shard_cfg, peak, B)
         if args.profile_json:
             Path(args.profile_json).write_text(json.dumps({"profile": prof, "fp64_peak_tflops": peak,
                                                             "step_ms": step_ms}, indent=1))
@@ -361,7 +397,7 @@ def run_ours(args):
             line["roofline"] = rl
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
-            line["cpu_baseline"] = cpu_baseline(G, hand, obj, cfg, threads, threads)
+            line["cpu_baseline"] = cpu_baseline(G, hand, obj, cfg, threads)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -201,6 +201,9 @@ class HandModel:
         self.collision_pairs = _arr(d.collision_pairs, 2 * d.n_pairs, np.int32).reshape(-1, 2)
         self.link_parent_joint = _arr(d.link_parent_joint, d.n_links, np.int32)
         self.link_tip_proxy = _arr(d.link_tip_proxy, d.n_links, np.int32)
+        per_link = np.diff(self.link_proxy_begin)
+        # sphere pairs the self-penetration term visits (hand.cpp:225-231)
+        self.n_sphere_pairs = int(sum(per_link[a] * per_link[b] for a, b in self.collision_pairs))
 
     @staticmethod
     def builtin() -> "HandModel":
