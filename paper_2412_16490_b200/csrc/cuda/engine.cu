@@ -11,6 +11,7 @@
 #include "../../../include/grasp_b200.h"
 #include "../host/capi_common.hpp"
 #include "kernels.cuh"
+#include "support_map.cuh"
 
 #include <cuda_runtime.h>
 
@@ -107,6 +108,8 @@ struct grasp_ctx {
   DevBuf<unsigned> h_subtree;
   DevBuf<double> h_jorigin, h_jaxis, h_jlo, h_jhi, h_proxy, h_envelope, h_lverts, h_lcentroid, h_lhalf,
       h_link_bsphere, h_link_box;
+  DevBuf<int> h_link_cm, h_cm_off, o_part_cm, o_cm_off;
+  DevBuf<unsigned short> h_cm_idx, o_cm_idx;
   // object
   DevObject O{};
   DevBuf<int> o_fbeg, o_vbeg;
@@ -388,7 +391,18 @@ struct grasp_ctx {
     h_link_tip.upload(link_tip, s);
     h_link_bsphere.upload(bsphere, s);
     h_link_box.upload(containing_boxes(d->link_obb, d->verts, d->link_vert_begin, L), s);
-    ck(cudaStreamSynchronize(s), "hand upload");
+    {
+      std::vector<int> base, off;
+      std::vector<unsigned short> idx;
+      build_support_maps(d->verts, d->link_vert_begin, L, base, off, idx);
+      h_link_cm.upload(base, s);
+      h_cm_off.upload(off, s);
+      h_cm_idx.upload(idx, s);
+      ck(cudaStreamSynchronize(s), "hand upload");
+    }
+    H.link_cm = h_link_cm.p;
+    H.cm_off = h_cm_off.p;
+    H.cm_idx = h_cm_idx.p;
     H.link_tip = h_link_tip.p;
     H.link_bsphere = h_link_bsphere.p;
     H.link_box = (std::getenv("GRASP_SAT") && std::string(std::getenv("GRASP_SAT")) == "0") ? nullptr : h_link_box.p;
@@ -665,7 +679,18 @@ struct grasp_ctx {
     o_cluster_fbeg.upload(cluster_fbeg, s);
     o_cluster_sphere32.upload(cluster32, s);
     o_cluster_box32.upload(cbox32, s);
-    ck(cudaStreamSynchronize(s), "object upload");
+    {
+      std::vector<int> base, off;
+      std::vector<unsigned short> idx;
+      build_support_maps(d->verts, d->part_vert_begin, P, base, off, idx);
+      o_part_cm.upload(base, s);
+      o_cm_off.upload(off, s);
+      o_cm_idx.upload(idx, s);
+      ck(cudaStreamSynchronize(s), "object upload");
+    }
+    O.part_cm = o_part_cm.p;
+    O.cm_off = o_cm_off.p;
+    O.cm_idx = o_cm_idx.p;
     O.part_sphere = o_part_sphere.p;
     O.part_box = o_part_box.p;
     O.face_sphere = o_face_sphere.p;

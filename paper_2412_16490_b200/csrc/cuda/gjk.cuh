@@ -8,6 +8,7 @@
 #pragma once
 
 #include "dmath.cuh"
+#include "model.cuh"
 
 namespace gdev {
 
@@ -28,6 +29,8 @@ struct Hull {
   bool posed;  // false: identity pose (object frame)
   M33 R;       // row-major
   D3 t;
+  const int* cm_off = nullptr;             // support map of this hull (kSupportCells + 1 offsets), or none
+  const unsigned short* cm_idx = nullptr;  // candidate lists (model.cuh)
 };
 
 struct SP {
@@ -39,6 +42,23 @@ GDEV_FN D3 support(const Hull& h, D3 dir, int& arg_out) {
   double best = -INFINITY;
   int arg = 0;
   const double* __restrict__ V = h.verts;
+  const int cell = h.cm_off ? support_cell(dl.x, dl.y, dl.z) : -1;
+  if (cell >= 0) {
+    // Candidates of the direction's cell, ascending: every vertex that can be
+    // the computed maximum is listed, so the first maximum is the full scan's.
+    const int k1 = GDEV_LDG(h.cm_off + cell + 1);
+    for (int k = GDEV_LDG(h.cm_off + cell); k < k1; ++k) {
+      const int i = GDEV_LDG(h.cm_idx + k);
+      const double s = dl.x * GDEV_LDG(V + 3 * i) + dl.y * GDEV_LDG(V + 3 * i + 1) + dl.z * GDEV_LDG(V + 3 * i + 2);
+      if (s > best) {
+        best = s;
+        arg = i;
+      }
+    }
+    const D3 v = ldg3(h.verts + 3 * arg);
+    arg_out = arg;
+    return h.posed ? mul(h.R, v) + h.t : v;
+  }
   int i = 0;
   // Four independent dot products per step for ILP; the compares stay in
   // index order, so the first maximum still wins (geometry.cpp:404-409).

@@ -752,6 +752,25 @@ __global__ void k_points_raw(DevObject O, int n, const double* __restrict__ pts,
 }
 
 // ------------------------------------------------------------ GJK pairs
+// Vertex range and support map of a link hull (link frame) / object part.
+__device__ __forceinline__ void set_link_hull(const DevHand& H, int link, Hull& A) {
+  A.verts = H.link_verts + 3 * (size_t)H.link_vbeg[link];
+  A.nv = H.link_vbeg[link + 1] - H.link_vbeg[link];
+  const int cm = H.link_cm[link];
+  A.cm_off = cm >= 0 ? H.cm_off + cm : nullptr;
+  A.cm_idx = H.cm_idx;
+}
+__device__ __forceinline__ void set_part_hull(const DevObject& O, int part, Hull& B) {
+  B.verts = O.verts + 3 * (size_t)O.part_vbeg[part];
+  B.nv = O.part_vbeg[part + 1] - O.part_vbeg[part];
+  B.posed = false;
+  B.R = eye();
+  B.t = mk(0, 0, 0);
+  const int cm = O.part_cm[part];
+  B.cm_off = cm >= 0 ? O.cm_off + cm : nullptr;
+  B.cm_idx = O.cm_idx;
+}
+
 __device__ __forceinline__ double scale_of(D3 centroid_world, double halfnorm) {
   return nrm(centroid_world) + 2.0 * halfnorm;
 }
@@ -760,17 +779,12 @@ template <class Scratch>
 __device__ inline PairResult link_part_distance(const DevHand& H, const DevObject& O, int link, int part,
                                                 const M33& Rw, D3 tw, Scratch& scratch) {
   Hull A;
-  A.verts = H.link_verts + 3 * (size_t)H.link_vbeg[link];
-  A.nv = H.link_vbeg[link + 1] - H.link_vbeg[link];
+  set_link_hull(H, link, A);
   A.posed = true;
   A.R = Rw;
   A.t = tw;
   Hull B;
-  B.verts = O.verts + 3 * (size_t)O.part_vbeg[part];
-  B.nv = O.part_vbeg[part + 1] - O.part_vbeg[part];
-  B.posed = false;
-  B.R = eye();
-  B.t = mk(0, 0, 0);
+  set_part_hull(O, part, B);
   // cloud_scale (geometry.cpp:17-23).
   double scale = 1.0;
   scale = fmax(scale, scale_of(mul(Rw, ld3(H.link_centroid + 3 * link)) + tw, H.link_halfnorm[link]));
@@ -991,16 +1005,11 @@ __device__ __forceinline__ void slot_hulls(const DevHand& H, const DevObject& O,
   const int g = slot / st.NP, lp = slot % st.NP;
   const int link = lp / O.P, part = lp % O.P;
   const double* w = st.world + ((size_t)g * H.L + link) * 12;
-  A.verts = H.link_verts + 3 * (size_t)H.link_vbeg[link];
-  A.nv = H.link_vbeg[link + 1] - H.link_vbeg[link];
+  set_link_hull(H, link, A);
   A.posed = true;
   for (int k = 0; k < 9; ++k) A.R.m[k] = w[k];
   A.t = ld3(w + 9);
-  B.verts = O.verts + 3 * (size_t)O.part_vbeg[part];
-  B.nv = O.part_vbeg[part + 1] - O.part_vbeg[part];
-  B.posed = false;
-  B.R = eye();
-  B.t = mk(0, 0, 0);
+  set_part_hull(O, part, B);
   scale = 1.0;
   scale = fmax(scale, scale_of(mul(A.R, ld3(H.link_centroid + 3 * link)) + A.t, H.link_halfnorm[link]));
   scale = fmax(scale, scale_of(ld3(O.part_centroid + 3 * part), O.part_halfnorm[part]));
@@ -1202,13 +1211,11 @@ __device__ PairResult self_pair_distance(const DevHand& H, const DevState& st, l
   const double* wb = st.world + ((size_t)g * H.L + lb) * 12;
   for (int k = 0; k < 9; ++k) Ra.m[k] = wa[k], Rb.m[k] = wb[k];
   const D3 ta = ld3(wa + 9), tb = ld3(wb + 9);
-  A.verts = H.link_verts + 3 * (size_t)H.link_vbeg[la];
-  A.nv = H.link_vbeg[la + 1] - H.link_vbeg[la];
+  set_link_hull(H, la, A);
   A.posed = true;
   A.R = Ra;
   A.t = ta;
-  B.verts = H.link_verts + 3 * (size_t)H.link_vbeg[lb];
-  B.nv = H.link_vbeg[lb + 1] - H.link_vbeg[lb];
+  set_link_hull(H, lb, B);
   B.posed = true;
   B.R = Rb;
   B.t = tb;

@@ -53,6 +53,9 @@ struct DevHand {
   const int* link_tip;              // [L] fingertip index of the link, -1 if none
   const double* link_bsphere;       // [L*4] bounding sphere of the link hull (link frame): center, radius
   const double* link_box;           // [L*15] box containing the link hull (link frame): center, half, axes (col-major)
+  const int* link_cm;               // [L] base of the link hull's support map in cm_off, -1 = full scan
+  const int* cm_off;                // support-map cell offsets into cm_idx (kSupportCells + 1 per map)
+  const unsigned short* cm_idx;     // candidate vertex indices per cell, ascending
 };
 
 struct DevObject {
@@ -74,7 +77,52 @@ struct DevObject {
   const int* cluster_fbeg;      // [NC+1] first face of each cluster (consecutive indices)
   const float4* cluster_sphere32;  // [NC] fp32 sphere bounding the cluster's face spheres
   const float4* cluster_box32;     // [NC*4] fp32 oriented box of the cluster's vertices (face-box layout)
+  const int* part_cm;              // [P] base of the part hull's support map in cm_off, -1 = full scan
+  const int* cm_off;
+  const unsigned short* cm_idx;
 };
+
+// Support maps (cube map of directions -> candidate support vertices). A hull
+// with at least kSupportMapMinVerts vertices gets, for each of the 6 * N * N
+// cells of a cube map of directions, the ascending list of every vertex that
+// can be the fp64-computed argmax of dir . v for some direction in the cell
+// (exclusion needs a provable margin over the rounding of the dot products),
+// so scanning the list in index order returns exactly the full scan's first
+// maximum (geometry.cpp:399-412). Built on the host at upload.
+#ifndef GDEV_SUPPORT_MAP_N
+#define GDEV_SUPPORT_MAP_N 16
+#endif
+#ifndef GDEV_SUPPORT_MAP_MIN_VERTS
+#define GDEV_SUPPORT_MAP_MIN_VERTS 24
+#endif
+constexpr int kSupportMapN = GDEV_SUPPORT_MAP_N;
+constexpr int kSupportCells = 6 * kSupportMapN * kSupportMapN;
+constexpr int kSupportMapMinVerts = GDEV_SUPPORT_MAP_MIN_VERTS;
+
+// Cell of direction d: face = dominant axis and sign (x+, x-, y+, y-, z+, z-),
+// (u, v) = the other two components in axis order over |d_face|, binned in
+// [-1, 1]. Returns -1 for zero, tiny, huge or NaN directions (full scan).
+__host__ __device__ __forceinline__ int support_cell(double dx, double dy, double dz) {
+  const double ax = fabs(dx), ay = fabs(dy), az = fabs(dz);
+  int face;
+  double m, pu, pv;
+  if (ax >= ay && ax >= az) {
+    face = dx >= 0 ? 0 : 1;
+    m = ax, pu = dy, pv = dz;
+  } else if (ay >= az) {
+    face = dy >= 0 ? 2 : 3;
+    m = ay, pu = dx, pv = dz;
+  } else {
+    face = dz >= 0 ? 4 : 5;
+    m = az, pu = dx, pv = dy;
+  }
+  if (!(m > 1e-200 && m < 1e200)) return -1;
+  const double sc = 0.5 * kSupportMapN / m;
+  int iu = (int)((pu + m) * sc), iv = (int)((pv + m) * sc);
+  iu = iu < 0 ? 0 : (iu >= kSupportMapN ? kSupportMapN - 1 : iu);
+  iv = iv < 0 ? 0 : (iv >= kSupportMapN ? kSupportMapN - 1 : iv);
+  return (face * kSupportMapN + iv) * kSupportMapN + iu;
+}
 
 #ifndef GDEV_FACE_CLUSTER
 #define GDEV_FACE_CLUSTER 16  // 8 and 32 measured slower (point queries 284 / 292 vs 282 ms)
