@@ -303,6 +303,9 @@ struct grasp_ctx {
     if (d->dof > kMaxDof) throw std::invalid_argument("hand has more than 32 joints");
     if (d->n_tips < 1 || d->n_tips > kMaxTips) throw std::invalid_argument("hand needs 1..5 fingertips");
     if (d->n_proxies > kMaxProxies) throw std::invalid_argument("hand has more than 128 sphere proxies");
+    for (int l = 0; l < d->n_links; ++l)
+      if (d->link_vert_begin[l + 1] - d->link_vert_begin[l] > 65535)
+        throw std::invalid_argument("link hull has more than 65535 vertices");
     const int L = d->n_links, dof = d->dof, m = d->n_tips, S = d->n_proxies;
     std::vector<int> depth(L), path(static_cast<size_t>(L) * kMaxDepth, 0);
     for (int l = 0; l < L; ++l) {
@@ -443,6 +446,9 @@ struct grasp_ctx {
     set_device();
     if (d->n_parts < 1) throw std::invalid_argument("point query against an empty part list");
     if (d->n_parts > kMaxParts) throw std::invalid_argument("object has more than 64 parts");
+    for (int p = 0; p < d->n_parts; ++p)
+      if (d->part_vert_begin[p + 1] - d->part_vert_begin[p] > 65535)
+        throw std::invalid_argument("object part has more than 65535 vertices");
     const int P = d->n_parts;
     std::vector<double> faces(static_cast<size_t>(d->n_faces) * kFaceStride, 0.0);
     for (int p = 0; p < P; ++p) {
@@ -1614,8 +1620,7 @@ __global__ void k_cos_debug(int n, const double* w, double* out) {
   SP tri[3];
   for (int i = 0; i < 3; ++i) {
     tri[i].w = ld3(w + 9 * t + 3 * i);
-    tri[i].a = tri[i].w;
-    tri[i].b = mk(0, 0, 0);
+    tri[i].key = 0;
   }
   const Simplex s = closest_on_simplex(tri, 3);
   double* o = out + 8 * t;

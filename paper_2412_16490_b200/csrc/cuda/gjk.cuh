@@ -33,8 +33,13 @@ struct Hull {
   const unsigned short* cm_idx = nullptr;  // candidate lists (model.cuh)
 };
 
+// A Minkowski-difference point w = a - b with its support vertices as a key
+// (ia | ib << 16). The points a and b themselves are rebuilt from the key
+// (hull_point, the same operations support() used), so simplices, EPA
+// polytopes and EPA job records carry 4 bytes instead of 48 per point.
 struct SP {
-  D3 w, a, b;
+  D3 w;
+  unsigned key;
 };
 
 GDEV_FN D3 support(const Hull& h, D3 dir, int& arg_out) {
@@ -84,27 +89,21 @@ GDEV_FN D3 support(const Hull& h, D3 dir, int& arg_out) {
   return h.posed ? mul(h.R, v) + h.t : v;
 }
 
-GDEV_FN D3 support(const Hull& h, D3 dir) {
-  int arg;
-  return support(h, dir, arg);
+// Vertex i of a hull in the world frame, exactly as support() returns it.
+GDEV_FN D3 hull_point(const Hull& h, int i) {
+  const D3 v = ldg3(h.verts + 3 * i);
+  return h.posed ? mul(h.R, v) + h.t : v;
 }
+GDEV_FN D3 sp_a(const Hull& A, const SP& p) { return hull_point(A, (int)(p.key & 0xffffu)); }
+GDEV_FN D3 sp_b(const Hull& B, const SP& p) { return hull_point(B, (int)(p.key >> 16)); }
 
 GDEV_FN SP support_pair(const Hull& A, const Hull& B, D3 dir) {
   SP s;
-  s.a = support(A, dir);
-  s.b = support(B, -dir);
-  s.w = s.a - s.b;
-  return s;
-}
-
-// Same, also returning the support vertices as a key (ia | ib << 16).
-GDEV_FN SP support_pair(const Hull& A, const Hull& B, D3 dir, unsigned& key) {
-  SP s;
   int ia, ib;
-  s.a = support(A, dir, ia);
-  s.b = support(B, -dir, ib);
-  s.w = s.a - s.b;
-  key = (unsigned)ia | ((unsigned)ib << 16);
+  const D3 a = support(A, dir, ia);
+  const D3 b = support(B, -dir, ib);
+  s.w = a - b;
+  s.key = (unsigned)ia | ((unsigned)ib << 16);
   return s;
 }
 
@@ -130,11 +129,11 @@ GDEV_FN void cycle_init(GjkCycle& c, int nva, int nvb) {
 }
 
 // Returns the number of iterations to jump (0 when no cycle was closed).
-GDEV_FN int cycle_step(GjkCycle& c, const unsigned (&key)[4], int ns, int iter) {
+GDEV_FN int cycle_step(GjkCycle& c, const SP (&simp)[4], int ns, int iter) {
   if (!c.on) return 0;
   unsigned k[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) k[i] = i < ns ? key[i] : ~0u;
+  for (int i = 0; i < 4; ++i) k[i] = i < ns ? simp[i].key : ~0u;
   const unsigned long long a = (unsigned long long)k[0] | ((unsigned long long)k[1] << 32);
   const unsigned long long b = (unsigned long long)k[2] | ((unsigned long long)k[3] << 32);
   if (a == c.s0 && b == c.s1) {
@@ -808,16 +807,17 @@ GDEV_FN bool epa(const SP (&simp)[4], int ns, const Hull& A, const Hull& B, doub
   D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
   double wsum = 0.0;
   for (int i = 0; i < sx.nkeep; ++i) {
-    wa += sx.wts[i] * tri[sx.keep[i]].a;
-    wb += sx.wts[i] * tri[sx.keep[i]].b;
+    const SP& p = tri[sx.keep[i]];
+    wa += sx.wts[i] * sp_a(A, p);
+    wb += sx.wts[i] * sp_b(B, p);
     wsum += sx.wts[i];
   }
   if (wsum > 0.5) {
     out.pa = wa;
     out.pb = wb;
   } else {
-    out.pa = tri[0].a;
-    out.pb = tri[0].b;
+    out.pa = sp_a(A, tri[0]);
+    out.pb = sp_b(B, tri[0]);
   }
   out.flags |= kPairEpa;
   if (dbg) {
@@ -826,7 +826,7 @@ GDEV_FN bool epa(const SP (&simp)[4], int ns, const Hull& A, const Hull& B, doub
     dbg->v[0] = best_copy.v0; dbg->v[1] = best_copy.v1; dbg->v[2] = best_copy.v2;
     st3(dbg->n, best_copy.n);
     dbg->d = best_copy.d;
-    for (int i = 0; i < 3; ++i) { st3(dbg->tri_w + 3 * i, tri[i].w); st3(dbg->tri_a + 3 * i, tri[i].a); }
+    for (int i = 0; i < 3; ++i) { st3(dbg->tri_w + 3 * i, tri[i].w); st3(dbg->tri_a + 3 * i, sp_a(A, tri[i])); }
     dbg->nkeep = sx.nkeep;
     for (int i = 0; i < sx.nkeep; ++i) { dbg->keep[i] = sx.keep[i]; dbg->wts[i] = sx.wts[i]; }
   }
@@ -845,10 +845,8 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
   // loops with predicates) so it stays in registers.
   out.gjk_skipped = 0;
   ns = 1;
-  unsigned key[4];
-  simp[0] = support_pair(A, B, mk(1, 0, 0), key[0]);
+  simp[0] = support_pair(A, B, mk(1, 0, 0));
   simp[1] = simp[2] = simp[3] = simp[0];
-  key[1] = key[2] = key[3] = key[0];
   GjkCycle cyc;
   cycle_init(cyc, A.nv, B.nv);
   bool overlap = false;
@@ -856,7 +854,7 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
   // One closest_on_simplex call site (code size): call kGjkMaxIters is the
   // iteration-cap estimate on the unreduced simplex (geometry.cpp:136-149).
   for (int iter = 0;; ++iter) {
-    const int jump = cycle_step(cyc, key, ns, iter);
+    const int jump = cycle_step(cyc, simp, ns, iter);
     iter += jump;
     out.gjk_skipped += jump;
     sx = closest_on_simplex(simp, ns);
@@ -876,8 +874,8 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
           if (src == 1) p = simp[1];
           if (src == 2) p = simp[2];
           if (src == 3) p = simp[3];
-          wa += sx.wts[i] * p.a;
-          wb += sx.wts[i] * p.b;
+          wa += sx.wts[i] * sp_a(A, p);
+          wb += sx.wts[i] * sp_b(B, p);
         }
       }
       const double d = sqrt(sx.dist2);
@@ -888,25 +886,22 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
       return false;
     }
     SP red[4];
-    unsigned rkey[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int src = sx.keep[i];
       red[i] = simp[0];
-      rkey[i] = key[0];
-      if (src == 1) red[i] = simp[1], rkey[i] = key[1];
-      if (src == 2) red[i] = simp[2], rkey[i] = key[2];
-      if (src == 3) red[i] = simp[3], rkey[i] = key[3];
+      if (src == 1) red[i] = simp[1];
+      if (src == 2) red[i] = simp[2];
+      if (src == 3) red[i] = simp[3];
     }
     ns = sx.nkeep;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) simp[i] = red[i], key[i] = rkey[i];
+    for (int i = 0; i < 4; ++i) simp[i] = red[i];
     if (sx.contains || sqrt(sx.dist2) < kTouchTol * scale) {
       overlap = true;
       break;
     }
-    unsigned wkey;
-    const SP w = support_pair(A, B, -sx.v, wkey);
+    const SP w = support_pair(A, B, -sx.v);
     ++out.n_support;
     ++out.gjk_iters;
     const double gap = sx.dist2 - dot(sx.v, w.w);
@@ -917,7 +912,7 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
     if (gap <= kGjkRelTol * sx.dist2 + 1e-300 || repeat || ns == 4) break;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (i == ns) simp[i] = w, key[i] = wkey;
+      if (i == ns) simp[i] = w;
     ++ns;
   }
   if (!overlap) {
@@ -925,8 +920,8 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (i < ns) {
-        wa += sx.wts[i] * simp[i].a;
-        wb += sx.wts[i] * simp[i].b;
+        wa += sx.wts[i] * sp_a(A, simp[i]);
+        wb += sx.wts[i] * sp_b(B, simp[i]);
       }
     }
     const double d = sqrt(sx.dist2);

@@ -1050,37 +1050,10 @@ __device__ __forceinline__ void write_epa_job(const DevState& st, int slot, cons
   jb[1] = ns;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    st3(jb + 2 + 9 * k, simp[k].w);
-    st3(jb + 5 + 9 * k, simp[k].a);
-    st3(jb + 8 + 9 * k, simp[k].b);
+    st3(jb + 2 + 4 * k, simp[k].w);
+    jb[5 + 4 * k] = simp[k].key;
   }
 }
-
-// Separated-pair result (geometry.cpp:136-164): weights sx.wts over
-// simp[i] when simp is already reduced to sx's keep set, else over
-// simp[sx.keep[i]] (iteration cap).
-__device__ __forceinline__ void store_separated(double* o, const Simplex& sx, const SP (&simp)[4], bool reduced) {
-  D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (i < sx.nkeep) {
-      const int src = reduced ? i : sx.keep[i];
-      SP p = simp[0];
-      if (src == 1) p = simp[1];
-      if (src == 2) p = simp[2];
-      if (src == 3) p = simp[3];
-      wa += sx.wts[i] * p.a;
-      wb += sx.wts[i] * p.b;
-    }
-  }
-  const double d = sqrt(sx.dist2);
-  o[0] = d;
-  st3(o + 1, wa);
-  st3(o + 4, wb);
-  st3(o + 7, d > 1e-14 ? (wa - wb) / d : mk(0, 0, 1));
-  o[10] = 0;
-}
-
 
 // Pass 2 (default): GJK, one thread per listed pair from start to end.
 __global__ void __launch_bounds__(GDEV_PAIRS_BLOCK, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHand H, DevObject O, DevState st) {
@@ -1125,9 +1098,8 @@ __global__ void __launch_bounds__(32, GDEV_EPA_MIN_BLOCKS) k_pairs_epa(DevHand H
   SP simp[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    simp[k].w = ld3(jb + 2 + 9 * k);
-    simp[k].a = ld3(jb + 5 + 9 * k);
-    simp[k].b = ld3(jb + 8 + 9 * k);
+    simp[k].w = ld3(jb + 2 + 4 * k);
+    simp[k].key = (unsigned)jb[5 + 4 * k];
   }
   Hull A, B;
   double scale;

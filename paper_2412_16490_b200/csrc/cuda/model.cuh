@@ -207,7 +207,7 @@ struct DevState {
   int epa_cap;
 };
 
-constexpr int kEpaJobStride = 40;
+constexpr int kEpaJobStride = 18;  // slot, ns, 4 x (w, support key)
 // The GJK list is segmented by (link, part) and, inside a segment, by the
 // slot's previous GJK length (kPairBuckets buckets), so a warp's pairs tend
 // to need the same number of iterations.

@@ -19,13 +19,15 @@ from pathlib import Path
 def main() -> None:
     rep, obj, fun = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+    short = re.sub(r"^_ZN4gdev\d+", "", fun)
+    short = re.match(r"[A-Za-z_0-9]+?(?=E|I|N|$)", short).group(0) if short else fun
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
+                          "regex:" + short], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[1]
     ia, isrc = hdr.index("Address"), hdr.index("Source")
     ist, iex = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
-    data = [r for r in rows[2:] if len(r) > iex]
+    data = [r for r in rows[2:] if len(r) > iex and r[ia].startswith("0x")]
     base = int(data[0][ia], 16)
     samples = {int(r[ia], 16) - base: (int(r[ist] or 0), int(r[iex] or 0), r[isrc].strip()) for r in data}
     with tempfile.TemporaryDirectory() as td:
