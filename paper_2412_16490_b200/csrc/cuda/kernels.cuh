@@ -1029,7 +1029,7 @@ __device__ __forceinline__ void queue_overflow(const DevState& st, int slot) {
 #define GDEV_PAIRS_BLOCK 128
 #endif
 #ifndef GDEV_PAIRS_MIN_BLOCKS
-#define GDEV_PAIRS_MIN_BLOCKS 2  // 255 registers (measured: 2 > 3 > 4 > 5 > 6 since the bucketed list)
+#define GDEV_PAIRS_MIN_BLOCKS 3  // 168 registers: 376 vs 382 ms at 2 blocks (232 registers) since SP keys; before them 2 > 3 > 4 > 5 > 6
 #endif
 // Jobs whose slot needed more than kEpaLongPred EPA iterations last time go
 // to a second region (launched first, packed into their own warps): a
