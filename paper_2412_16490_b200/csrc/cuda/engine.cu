@@ -98,6 +98,10 @@ struct grasp_ctx {
   cudaStream_t stream = nullptr;
   bool has_hand = false, has_object = false;
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
+  DevBuf<int> pq_key, pq_list, pq_total, pq_count;
+  // Bucket the all-slot point queries by their last closest face's cluster
+  // (GRASP_PQ_BUCKETS=0: slot order).
+  bool bucket_queries = !(std::getenv("GRASP_PQ_BUCKETS") && std::string(std::getenv("GRASP_PQ_BUCKETS")) == "0");
   DevBuf<unsigned char> pair_need, pair_hist, epa_hist;
 
   // hand
@@ -116,7 +120,7 @@ struct grasp_ctx {
   DevBuf<double> o_faces, o_verts, o_centroid, o_half, o_obb, o_part_sphere, o_face_sphere, o_part_box;
   DevBuf<float4> o_face_sphere32, o_cluster_sphere32, o_face_box32, o_cluster_box32;
   DevBuf<double4> o_face_plane;
-  DevBuf<int> o_part_cbeg, o_cluster_fbeg;
+  DevBuf<int> o_part_cbeg, o_cluster_fbeg, o_face_cluster;
 
   // Bounding sphere (AABB center, max vertex distance, relative slack) of
   // each vertex range [begin[i], begin[i+1]).
@@ -686,6 +690,12 @@ struct grasp_ctx {
     o_cluster_sphere32.upload(cluster32, s);
     o_cluster_box32.upload(cbox32, s);
     {
+      std::vector<int> fc(d->n_faces, 0);
+      for (size_t c = 0; c + 1 < cluster_fbeg.size(); ++c)
+        for (int f = cluster_fbeg[c]; f < cluster_fbeg[c + 1]; ++f) fc[f] = static_cast<int>(c);
+      o_face_cluster.upload(fc, s);
+    }
+    {
       std::vector<int> base, off;
       std::vector<unsigned short> idx;
       build_support_maps(d->verts, d->part_vert_begin, P, base, off, idx);
@@ -707,6 +717,8 @@ struct grasp_ctx {
     O.cluster_fbeg = o_cluster_fbeg.p;
     O.cluster_box32 = o_cluster_box32.p;
     O.cluster_sphere32 = o_cluster_sphere32.p;
+    O.NC = static_cast<int>(cluster32.size());
+    O.face_cluster = o_face_cluster.p;
     O.P = P;
     O.F = d->n_faces;
     O.part_fbeg = o_fbeg.p;
@@ -753,6 +765,14 @@ struct grasp_ctx {
     qp_conv.ensure(g * 6);
     qp_ready.ensure(g);
     qface.ensure(g * NQ);
+    pq_key.ensure(g * NQ);
+    pq_list.ensure(g * NQ);
+    pq_total.ensure(1);
+    pq_count.ensure(static_cast<size_t>(has_object ? O.NC + O.P + 1 : 1));
+    st.pq_key = pq_key.p;
+    st.pq_list = pq_list.p;
+    st.pq_total = pq_total.p;
+    st.pq_count = pq_count.p;
     ck(cudaMemsetAsync(qface.p, 0xff, sizeof(int) * g * NQ, stream), "memset");
     st.qface = qface.p;
     failed.ensure(g);
@@ -880,6 +900,17 @@ struct grasp_ctx {
     };
     const int L = tips_only ? lanes("GRASP_QGROUP_TIPS", 4) : lanes("GRASP_QGROUP", 1);
     const int* sl = tips_only ? h_tip_slots.p : nullptr;
+    if (!tips_only && L == 1 && bucket_queries) {
+      launch(0, [&] {
+        const int nb = O.NC + O.P + 1;
+        ck(cudaMemsetAsync(pq_count.p, 0, sizeof(int) * nb, stream), "memset");
+        k_pq_count<<<blocks(n, 128), 128, 0, stream>>>(O, st);
+        k_exclusive_scan<<<1, 1024, 0, stream>>>(pq_count.p, nb, pq_total.p);
+        k_pq_scatter<<<blocks(n, 128), 128, 0, stream>>>(st);
+        k_point_query_list<<<blocks(n, GDEV_PQ_BLOCK), GDEV_PQ_BLOCK, 0, stream>>>(O, st);
+      });
+      return;
+    }
     launch(0, [&] {
       switch (L) {
         case 2: k_point_query_group<2><<<blocks(n * 2, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, stream>>>(O, st, sl, per); break;

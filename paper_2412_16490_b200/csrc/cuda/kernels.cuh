@@ -999,6 +999,92 @@ __global__ void __launch_bounds__(128) k_pairs_scatter(DevState st, const int* _
   }
 }
 
+// Spatially bucketed all-slot point queries. A slot's query of the last
+// iteration tells where its point is now: near the cluster of its last
+// closest face, or inside a part. Listing the queries by that bucket puts
+// queries with the same path through point_to_mesh (same parts culled, same
+// clusters scanned, same inside test) into the same warps. Which thread runs
+// a query does not change its result, so the order is free.
+__device__ __forceinline__ int pq_bucket(const DevObject& O, const DevState& st, size_t t) {
+  const int f = st.qface[t];
+  if (f >= 0 && f < O.F) return __ldg(O.face_cluster + f);
+  const double d = st.qres[t * 8];
+  const double pd = st.qres[t * 8 + 7];
+  if (d < 0.0 && pd >= 0.0 && pd < O.P) return O.NC + (int)pd;
+  return O.NC + O.P;
+}
+
+__global__ void __launch_bounds__(128) k_pq_count(DevObject O, DevState st) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = (long long)st.G * st.NQ;
+  bool active = false;
+  int key = 0;
+  if (t < n) {
+    active = !st.failed[t / st.NQ];
+    if (active) key = pq_bucket(O, st, (size_t)t);
+    st.pq_key[t] = active ? key : -1;
+  }
+  warp_segment_add(st.pq_count, key, active);
+}
+
+// Exclusive scan of n counts in place (one block); *total = their sum.
+__global__ void __launch_bounds__(1024) k_exclusive_scan(int* counts, int n, int* total) {
+  __shared__ int part_sum[1024];
+  const int tid = threadIdx.x;
+  const int per = (n + 1023) / 1024;
+  const int b = tid * per, e = min(n, b + per);
+  int s = 0;
+  for (int i = b; i < e; ++i) s += counts[i];
+  part_sum[tid] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const int v = tid >= off ? part_sum[tid - off] : 0;
+    __syncthreads();
+    part_sum[tid] += v;
+    __syncthreads();
+  }
+  int run = part_sum[tid] - s;
+  for (int i = b; i < e; ++i) {
+    const int c = counts[i];
+    counts[i] = run;
+    run += c;
+  }
+  if (tid == 1023) *total = part_sum[1023];
+}
+
+__global__ void __launch_bounds__(128) k_pq_scatter(DevState st) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = (long long)st.G * st.NQ;
+  const int key = t < n ? st.pq_key[t] : -1;
+  const bool active = key >= 0;
+  const int pos = warp_segment_add(st.pq_count, active ? key : 0, active);
+  if (active) st.pq_list[pos] = (int)t;
+}
+
+// k_point_query over the bucketed list.
+__global__ void __launch_bounds__(GDEV_PQ_BLOCK, 768 / GDEV_PQ_BLOCK) k_point_query_list(DevObject O, DevState st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *st.pq_total) return;
+  const int t = st.pq_list[i];
+  const int g = t / st.NQ;
+  const D3 p = ld3(st.qpts + (size_t)t * 3);
+  unsigned planes, tris;
+  int* qf = st.qface + t;
+  const PointHit h = point_to_mesh(O, p, *qf, &planes, &tris);
+  *qf = h.face;
+  if (st.ops) {
+    atomicAdd(st.ops + kOpPlaneTests, (unsigned long long)planes);
+    atomicAdd(st.ops + kOpTriangleTests, (unsigned long long)tris);
+    atomicAdd(st.ops + kOpPointQueries, 1ull);
+  }
+  double* o = st.qres + (size_t)t * 8;
+  o[0] = h.d;
+  st3(o + 1, h.pb);
+  st3(o + 4, h.n);
+  o[7] = h.part;
+  (void)g;
+}
+
 // Hulls and cloud_scale (geometry.cpp:17-23) of a pair slot.
 __device__ __forceinline__ void slot_hulls(const DevHand& H, const DevObject& O, const DevState& st, int slot, Hull& A,
                                            Hull& B, double& scale) {

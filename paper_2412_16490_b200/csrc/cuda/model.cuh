@@ -80,6 +80,8 @@ struct DevObject {
   const int* part_cm;              // [P] base of the part hull's support map in cm_off, -1 = full scan
   const int* cm_off;
   const unsigned short* cm_idx;
+  int NC;                          // face clusters
+  const int* face_cluster;         // [F] cluster of each face (point-query bucketing)
 };
 
 // Support maps (cube map of directions -> candidate support vertices). A hull
@@ -169,6 +171,10 @@ struct DevState {
   double* qpts;     // [G*NQ*3]
   double* qres;     // [G*NQ*8]: d, pb(3), n(3), part
   int* qface;       // [G*NQ] closest face of the slot's last query (warm-start seed), -1 if none
+  int* pq_key;      // [G*NQ] bucket of each query slot (its last closest face's cluster, ...)
+  int* pq_count;    // [NC + P + 1] queries per bucket, then the fill cursor
+  int* pq_total;    // [1] listed queries
+  int* pq_list;     // [G*NQ] query slots (g * NQ + slot) grouped by bucket
   double* pairs;    // [G*NP*12]: d, pa(3), pb(3), n(3), flags, pad
   double* warm_x;   // [G*n*6] column-major n x 6
   double* warm_y;   // [G*M*6]

@@ -711,6 +711,32 @@ def test_group_point_queries_bitwise_equal_thread_queries(G, monkeypatch):
         assert np.array_equal(o.contacts, ref.contacts, equal_nan=True), k
 
 
+@pytest.mark.parametrize("case", ["shadow_drill", "trident_box"])
+def test_bucketed_point_queries_bitwise(G, monkeypatch, case):
+    """The coarse stage's point queries listed by spatial bucket (k_pq_count / k_pq_scatter /
+    k_point_query_list) give bitwise the records of the slot-order launch (GRASP_PQ_BUCKETS=0)."""
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    if case == "shadow_drill":
+        hand = G.HandModel.from_file(root / "paper_2412_16490_b200/assets/hands/shadow_like.json")
+        obj = G.load_object(root / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+    else:
+        hand, obj = G.HandModel.builtin(), G.make_primitive("box", 0.08)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 256, 31
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 300, 5, 5
+    x0 = G.init_poses(hand, obj, cfg.batch, cfg.seed, cfg.init)
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("GRASP_PQ_BUCKETS", flag)
+        eng = G.Engine(0)
+        eng.set_hand(hand)
+        eng.set_object(obj)
+        outs.append(eng.synthesize(cfg, x0))
+    for f in ("x", "x_p", "x_s", "energy_total", "stage_energy", "failed", "contact_forces"):
+        assert np.array_equal(getattr(outs[0], f), getattr(outs[1], f), equal_nan=True), f
+
+
 def test_synthesis_deterministic_and_batch_prefix_independent(G, trident, engine):
     """test_pipeline.cpp:399-421 on the device: the same start states give bitwise-equal
     records on a rerun, and a grasp's record does not depend on the batch it is in

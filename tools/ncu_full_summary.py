@@ -1,6 +1,7 @@
 """Summarise one kernel of an `ncu --set full` report into the profiles/ JSON layout (dev tool).
 
-usage: python tools/ncu_full_summary.py report.ncu-rep "source note" > profiles/<name>.json
+usage: python tools/ncu_full_summary.py report.ncu-rep "source note" [kernel-substring] > profiles/<name>.json
+(the first profiled launch whose name contains the substring; default the first launch)
 """
 import csv
 import io
@@ -23,9 +24,12 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 def main() -> None:
     rep, note = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else ""
+    want = sys.argv[3] if len(sys.argv) > 3 else ""
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    ik = hdr.index("Kernel Name")
+    vals = next(r for r in rows[2:] if want in r[ik])
     d = {k: (v, u) for k, u, v in zip(hdr, units, vals)}
     metrics = {k: {"value": d[k][0], "unit": d[k][1]} for k in KEYS if k in d}
     stalls = {}
