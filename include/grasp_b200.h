@@ -167,6 +167,11 @@ void grasp_ctx_destroy(grasp_ctx* ctx);
 int grasp_ctx_set_hand(grasp_ctx* ctx, const grasp_hand_desc* hand);
 int grasp_ctx_set_object(grasp_ctx* ctx, const grasp_object_desc* object);
 
+/* Several objects in one context (object.hpp:19-25): their convex parts are
+ * packed back to back on the device, replacing the context's object(s).
+ * grasp_ctx_set_object(ctx, o) is grasp_ctx_set_objects(ctx, 1, &o). */
+int grasp_ctx_set_objects(grasp_ctx* ctx, int n, const grasp_object_desc* const* objects);
+
 /* Caller-owned per-grasp outputs of synthesize (records.hpp:29-44 as SoA).
  * D = 12 + dof, m = n_tips, n = m * n_edges. Any pointer may be NULL. */
 typedef struct grasp_out {
@@ -186,6 +191,13 @@ typedef struct grasp_out {
  * caller produced with grasp_init_poses (the reference's single RNG stream).
  * Per-grasp failure is reported in out->failed, never as an error. */
 int grasp_synthesize(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0, grasp_out* out);
+
+/* One synthesis over grasps of several objects (the objects of grasp_ctx_set_objects):
+ * grasp g grasps object object_index[g] from start state x0[g] (grasp_init_poses of that
+ * object). Every kernel launch covers the whole batch; each record equals the one a
+ * single-object grasp_synthesize of that grasp gives. Single-device contexts only. */
+int grasp_synthesize_objects(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0,
+                             const int* object_index, grasp_out* out);
 
 /* Same, but x0 and every output pointer are DEVICE pointers on ctx's device
  * (no host copies; used to time the kernels with inputs resident in HBM). */

@@ -115,6 +115,8 @@ SIGNATURES = {
     "grasp_ctx_set_object": (C.c_int, [C.c_void_p, C.POINTER(ObjectDesc)]),
     "grasp_synthesize": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.c_int, _dp, C.POINTER(Out)]),
     "grasp_synthesize_device": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.c_int, _dp, C.POINTER(Out)]),
+    "grasp_ctx_set_objects": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.POINTER(ObjectDesc))]),
+    "grasp_synthesize_objects": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.c_int, _dp, _ip, C.POINTER(Out)]),
     "grasp_eval_params_default": (None, [C.POINTER(EvalParamsStruct)]),
     "grasp_eval": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.POINTER(EvalParamsStruct), C.c_int, _dp, _dp, _dp,
                              C.POINTER(C.c_int)]),

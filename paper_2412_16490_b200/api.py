@@ -410,6 +410,14 @@ class SynthesisOutput:
                      dptr(self.per_direction), dptr(self.contact_forces), dptr(self.contacts),
                      dptr(self.stage_energy), iptr(self.failed), iptr(self.qp_converged))
 
+    def subset(self, lo: int, hi: int) -> "SynthesisOutput":
+        """Rows [lo, hi) as their own output (views)."""
+        out = SynthesisOutput.__new__(SynthesisOutput)
+        for k in ("x_p", "x", "x_s", "energy_total", "per_direction", "contact_forces", "contacts", "stage_energy",
+                  "failed", "qp_converged"):
+            setattr(out, k, getattr(self, k)[lo:hi])
+        return out
+
     def records(self, cfg: RunConfig, obj: ObjectModel, index_offset: int = 0) -> List[GraspRecord]:
         names = ("coarse", "fine", "final")
         iters = (cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters)
@@ -460,6 +468,24 @@ class Engine:
         out = SynthesisOutput(batch, self.hand.dims(), self.hand.n_tips, cfg.contact.n_edges)
         s = out.as_struct()
         N.check(N.lib().grasp_synthesize(self._ctx, C.byref(cfg.to_params()), batch, dptr(x0), C.byref(s)))
+        return out
+
+    def set_objects(self, objects: List[ObjectModel]):
+        """Several objects in this context (grasp_ctx_set_objects)."""
+        arr = (C.POINTER(N.ObjectDesc) * len(objects))(*[C.pointer(o.desc) for o in objects])
+        N.check(N.lib().grasp_ctx_set_objects(self._ctx, len(objects), arr))
+        self.objects = list(objects)
+        self.obj = objects[0]
+
+    def synthesize_objects(self, cfg: RunConfig, x0: np.ndarray, object_index) -> SynthesisOutput:
+        """One batch over grasps of the objects of set_objects (grasp_synthesize_objects)."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        idx = np.ascontiguousarray(object_index, dtype=np.int32)
+        batch = x0.shape[0]
+        out = SynthesisOutput(batch, self.hand.dims(), self.hand.n_tips, cfg.contact.n_edges)
+        s = out.as_struct()
+        N.check(N.lib().grasp_synthesize_objects(self._ctx, C.byref(cfg.to_params()), batch, dptr(x0), iptr(idx),
+                                                 C.byref(s)))
         return out
 
     def synthesize_traced(self, cfg: RunConfig, x0: np.ndarray, snaps) -> tuple:
@@ -570,11 +596,14 @@ def synthesize(model: HandModel, obj: ObjectModel, cfg: RunConfig, device: int =
 
 
 def synthesize_objects(model: HandModel, objects: List[ObjectModel], configs, device: int = 0,
-                       streams: int = 8) -> List[List[GraspRecord]]:
-    """Many objects on one GPU (BASELINE config 3): one synthesize per
-    object (pipeline.cpp:436-457 each, so results equal per-object runs), issued from `streams`
-    host threads, each driving its own engine context and CUDA stream, so several objects'
-    batches share the GPU concurrently. `configs` is one RunConfig or one per object."""
+                       streams: int = 8, single_launch: bool = True) -> List[List[GraspRecord]]:
+    """Many objects on one GPU (BASELINE config 3). `configs` is one RunConfig
+    or one per object (each object's start states come from its own init_poses stream,
+    pipeline.cpp:388-424). When the configs differ only in seed and batch (config 3), all
+    objects run as ONE batch in one context (grasp_synthesize_objects: object id per grasp,
+    parts packed on the device, one set of launches); otherwise one synthesize per object is
+    issued from `streams` host threads on their own contexts and streams. Either way each
+    object's records equal a plain per-object synthesize."""
     import threading
     from .errors import InvalidArgument
     if isinstance(configs, RunConfig):
@@ -583,6 +612,20 @@ def synthesize_objects(model: HandModel, objects: List[ObjectModel], configs, de
         raise InvalidArgument("one RunConfig per object")
     for c in configs:
         validate(c)
+    shared = all(dataclasses.replace(c, seed=0, batch=0) == dataclasses.replace(configs[0], seed=0, batch=0)
+                 for c in configs)
+    if single_launch and shared:
+        eng = Engine(device)
+        eng.set_hand(model)
+        eng.set_objects(list(objects))
+        x0 = np.concatenate([init_poses(model, o, c.batch, c.seed, c.init) for o, c in zip(objects, configs)])
+        idx = np.concatenate([np.full(c.batch, k, np.int32) for k, c in enumerate(configs)])
+        res = eng.synthesize_objects(configs[0], x0, idx)
+        recs, lo = [], 0
+        for o, c in zip(objects, configs):
+            recs.append(res.subset(lo, lo + c.batch).records(c, o))
+            lo += c.batch
+        return recs
     S = max(1, min(int(streams), len(objects)))
     engines = [Engine(device) for _ in range(S)]
     for e in engines:

@@ -120,7 +120,7 @@ struct grasp_ctx {
   DevBuf<double> o_faces, o_verts, o_centroid, o_half, o_obb, o_part_sphere, o_face_sphere, o_part_box;
   DevBuf<float4> o_face_sphere32, o_cluster_sphere32, o_face_box32, o_cluster_box32;
   DevBuf<double4> o_face_plane;
-  DevBuf<int> o_part_cbeg, o_cluster_fbeg, o_face_cluster;
+  DevBuf<int> o_part_cbeg, o_cluster_fbeg, o_face_cluster, o_obj_pbeg, obj_ids;
 
   // Bounding sphere (AABB center, max vertex distance, relative slack) of
   // each vertex range [begin[i], begin[i+1]).
@@ -446,10 +446,57 @@ struct grasp_ctx {
     has_hand = true;
   }
 
-  void set_object(const grasp_object_desc* d) {
+  // Several objects in one context: their parts are packed
+  // back to back (faces, vertices, clusters, support maps indexed globally),
+  // obj_pbeg[o] is object o's first part, and each grasp of a synthesis names
+  // its object (st.obj). Pair slots keep a stride of Pmax parts per link.
+  void set_objects(const grasp_object_desc* const* ds, int n) {
+    if (n < 1) throw std::invalid_argument("no objects");
+    std::vector<int> pbeg(1, 0);
+    int pmax = 0;
+    for (int o = 0; o < n; ++o) {
+      if (!ds[o]) throw std::invalid_argument("null object");
+      if (ds[o]->n_parts < 1) throw std::invalid_argument("point query against an empty part list");
+      if (ds[o]->n_parts > kMaxParts) throw std::invalid_argument("object has more than 64 parts");
+      pbeg.push_back(pbeg.back() + ds[o]->n_parts);
+      pmax = std::max(pmax, ds[o]->n_parts);
+    }
+    if (n == 1) {
+      set_object(ds[0], pbeg, pmax);
+      return;
+    }
+    // concatenate the packed descriptors (face indices stay local to their part's vertices)
+    std::vector<int> vb(1, 0), fb(1, 0), faces;
+    std::vector<double> verts, obb, centroid, volume;
+    for (int o = 0; o < n; ++o) {
+      const grasp_object_desc* d = ds[o];
+      for (int p = 0; p < d->n_parts; ++p) {
+        vb.push_back(vb.back() + d->part_vert_begin[p + 1] - d->part_vert_begin[p]);
+        fb.push_back(fb.back() + d->part_face_begin[p + 1] - d->part_face_begin[p]);
+      }
+      verts.insert(verts.end(), d->verts, d->verts + 3 * static_cast<size_t>(d->n_verts));
+      faces.insert(faces.end(), d->faces, d->faces + 3 * static_cast<size_t>(d->n_faces));
+      obb.insert(obb.end(), d->part_obb, d->part_obb + 15 * static_cast<size_t>(d->n_parts));
+      centroid.insert(centroid.end(), d->part_centroid, d->part_centroid + 3 * static_cast<size_t>(d->n_parts));
+      volume.insert(volume.end(), d->part_volume, d->part_volume + d->n_parts);
+    }
+    grasp_object_desc m{};
+    m.n_parts = pbeg.back();
+    m.n_verts = static_cast<int>(verts.size() / 3);
+    m.n_faces = static_cast<int>(faces.size() / 3);
+    m.part_vert_begin = vb.data();
+    m.part_face_begin = fb.data();
+    m.verts = verts.data();
+    m.faces = faces.data();
+    m.part_obb = obb.data();
+    m.part_centroid = centroid.data();
+    m.part_volume = volume.data();
+    set_object(&m, pbeg, pmax);
+  }
+
+  void set_object(const grasp_object_desc* d, const std::vector<int>& obj_part_begin, int pmax) {
     set_device();
     if (d->n_parts < 1) throw std::invalid_argument("point query against an empty part list");
-    if (d->n_parts > kMaxParts) throw std::invalid_argument("object has more than 64 parts");
     for (int p = 0; p < d->n_parts; ++p)
       if (d->part_vert_begin[p + 1] - d->part_vert_begin[p] > 65535)
         throw std::invalid_argument("object part has more than 65535 vertices");
@@ -720,6 +767,11 @@ struct grasp_ctx {
     O.NC = static_cast<int>(cluster32.size());
     O.face_cluster = o_face_cluster.p;
     O.P = P;
+    O.Pmax = pmax;
+    O.NO = static_cast<int>(obj_part_begin.size()) - 1;
+    o_obj_pbeg.upload(obj_part_begin, s);
+    ck(cudaStreamSynchronize(s), "object upload");
+    O.obj_pbeg = o_obj_pbeg.p;
     O.F = d->n_faces;
     O.part_fbeg = o_fbeg.p;
     O.part_vbeg = o_vbeg.p;
@@ -737,7 +789,7 @@ struct grasp_ctx {
     const int mq = std::max(m, m_qp);
     const int D = 12 + dof;
     const int NQ = has_hand ? H.S + 6 * H.m : 1;
-    const int NP = L * (has_object ? O.P : 1);
+    const int NP = L * (has_object ? O.Pmax : 1);
     const int n = mq * k, M = mq + 1 + n;
     const size_t g = static_cast<size_t>(G);
     x.ensure(g * D);
@@ -924,15 +976,15 @@ struct grasp_ctx {
   }
   void launch_pairs(bool tips_only) {
     const int nl = tips_only ? H.m : H.L;
-    const long long n = static_cast<long long>(st.G) * nl * O.P;
+    const long long n = static_cast<long long>(st.G) * nl * O.Pmax;
     launch(3, [&] {
       ck(cudaMemsetAsync(ovf_count.p, 0, sizeof(int), stream), "memset");
       const int* lk = tips_only ? h_tip_links_sorted.p : nullptr;
       ck(cudaMemsetAsync(pair_count.p, 0, 4 * sizeof(int), stream), "memset");
-      ck(cudaMemsetAsync(seg_count.p, 0, sizeof(int) * nl * O.P * kPairBuckets, stream), "memset");
+      ck(cudaMemsetAsync(seg_count.p, 0, sizeof(int) * nl * O.Pmax * kPairBuckets, stream), "memset");
       k_pairs_cull<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
-      k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.P * kPairBuckets);
-      k_pairs_scatter<<<blocks(n, 128), 128, 0, stream>>>(st, lk, nl, O.P);
+      k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.Pmax * kPairBuckets);
+      k_pairs_scatter<<<blocks(n, 128), 128, 0, stream>>>(st, lk, nl, O.Pmax);
       k_pairs_list<<<blocks(n, GDEV_PAIRS_BLOCK), GDEV_PAIRS_BLOCK, 0, stream>>>(H, O, st);
       // EPA jobs spread over all SMs (32-thread blocks; few jobs per launch)
       k_pairs_epa<<<blocks(2 * std::min<long long>(n, st.epa_cap), 32), 32, 0, stream>>>(H, O, st);
@@ -1082,7 +1134,7 @@ void emit_outputs(grasp_ctx* ctx, const grasp_run_params* p, int G, grasp_out* o
 }
 
 int synthesize_impl(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0, grasp_out* out,
-                    bool device_ptrs) {
+                    bool device_ptrs, const int* object_index = nullptr) {
   return guard([&] {
     require_models(ctx);
     if (!p || !out) throw std::invalid_argument("null argument");
@@ -1092,11 +1144,25 @@ int synthesize_impl(grasp_ctx* ctx, const grasp_run_params* p, int batch, const 
     ctx->set_device();
     ctx->ensure_state(batch, ctx->H.m, p->n_edges);
     ctx->reset_run_state(batch);
+    ctx->st.obj = nullptr;
+    if (object_index) {
+      for (int g = 0; g < batch; ++g)
+        if (object_index[g] < 0 || object_index[g] >= ctx->O.NO)
+          throw std::invalid_argument("object index out of range");
+      ctx->obj_ids.upload(std::vector<int>(object_index, object_index + batch), ctx->stream);
+      ctx->st.obj = ctx->obj_ids.p;
+    }
     ck(cudaMemcpyAsync(ctx->x.p, x0, sizeof(double) * batch * ctx->H.D,
                        device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream),
        "x0 copy");
-    ctx->run(p);
-    ctx->check_errors();
+    try {
+      ctx->run(p);
+      ctx->check_errors();
+    } catch (...) {
+      ctx->st.obj = nullptr;
+      throw;
+    }
+    ctx->st.obj = nullptr;
     emit_outputs(ctx, p, batch, out, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
   });
 }
@@ -1165,8 +1231,8 @@ int grasp_ctx_set_hand(grasp_ctx* ctx, const grasp_hand_desc* hand) {
 int grasp_ctx_set_object(grasp_ctx* ctx, const grasp_object_desc* object) {
   return guard([&] {
     if (!ctx || !object) throw std::invalid_argument("null argument");
-    if (ctx->shards.empty()) ctx->set_object(object);
-    for (grasp_ctx* s : ctx->shards) s->set_object(object);
+    if (ctx->shards.empty()) ctx->set_objects(&object, 1);
+    for (grasp_ctx* s : ctx->shards) s->set_objects(&object, 1);
   });
 }
 
@@ -1205,6 +1271,22 @@ int grasp_synthesize(grasp_ctx* ctx, const grasp_run_params* p, int batch, const
     for (int k = 0; k < G; ++k)
       if (status[k] != GRASP_OK) throw ShardError(status[k], "device shard " + std::to_string(k) + ": " + message[k]);
   });
+}
+
+int grasp_ctx_set_objects(grasp_ctx* ctx, int n, const grasp_object_desc* const* objects) {
+  return guard([&] {
+    if (!ctx || !objects) throw std::invalid_argument("null argument");
+    if (ctx->shards.empty()) ctx->set_objects(objects, n);
+    for (grasp_ctx* s : ctx->shards) s->set_objects(objects, n);
+  });
+}
+
+int grasp_synthesize_objects(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0,
+                             const int* object_index, grasp_out* out) {
+  if (!object_index) return guard([] { throw std::invalid_argument("null object index"); });
+  if (ctx && !ctx->shards.empty())
+    return guard([] { throw std::invalid_argument("multi-object synthesis needs a single-device context"); });
+  return synthesize_impl(ctx, p, batch, x0, out, false, object_index);
 }
 
 int grasp_synthesize_device(grasp_ctx* ctx, const grasp_run_params* p, int batch, const double* x0_dev,

@@ -257,7 +257,16 @@ __device__ __forceinline__ bool cluster_box_far(const DevObject& O, int c, float
   return eu * eu + ev * ev + en * en > reach * reach;
 }
 
-__device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int warm_face = -1,
+// Part range [p0, p1) of grasp g's object (multi-object contexts; st.obj == nullptr: object 0).
+__device__ __forceinline__ void obj_parts(const DevObject& O, const DevState& st, int g, int& p0, int& p1) {
+  const int o = st.obj ? __ldg(st.obj + g) : 0;
+  p0 = __ldg(O.obj_pbeg + o);
+  p1 = __ldg(O.obj_pbeg + o + 1);
+}
+
+// point_to_mesh(p, parts [p0, p1)) (geometry.cpp:527-542); the part index
+// returned is global (p0 + the object's part index).
+__device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p1, int warm_face = -1,
                                          unsigned* plane_tests = nullptr, unsigned* tri_tests = nullptr) {
   PointHit best;
   best.d = INFINITY;
@@ -277,7 +286,7 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int warm_face
     const double* F = O.faces + (size_t)warm_face * kFaceStride;
     ub_warm = nrm(p - closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6)));
   }
-  for (int part = 0; part < O.P; ++part) {
+  for (int part = p0; part < p1; ++part) {
     const int f0 = __ldg(O.part_fbeg + part), f1 = __ldg(O.part_fbeg + part + 1);
     // Part-level cull: every point of the part is at least |p - c| - r
     // away; a part that cannot reach below the current best cannot win the
@@ -497,7 +506,7 @@ __device__ __forceinline__ float group_fmin(unsigned gmask, float v) {
 }
 
 template <int L>
-__device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int warm_face, int gl, unsigned gmask,
+__device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int p0, int p1, int warm_face, int gl, unsigned gmask,
                                         unsigned* plane_tests, unsigned* tri_tests) {
   PointHit best;
   best.d = INFINITY;
@@ -513,7 +522,7 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int warm_face,
     const double* F = O.faces + (size_t)warm_face * kFaceStride;
     ub_warm = nrm(p - closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6)));
   }
-  for (int part = 0; part < O.P; ++part) {
+  for (int part = p0; part < p1; ++part) {
     const int f0 = __ldg(O.part_fbeg + part), f1 = __ldg(O.part_fbeg + part + 1);
     {
       const double* S = O.part_sphere + 4 * part;
@@ -690,7 +699,9 @@ __global__ void __launch_bounds__(GDEV_PQG_BLOCK) k_point_query_group(DevObject 
   const D3 p = ld3(st.qpts + ((size_t)g * st.NQ + slot) * 3);
   unsigned planes, tris;
   int* qf = st.qface + (size_t)g * st.NQ + slot;
-  const PointHit h = point_to_mesh_group<L>(O, p, *qf, gl, gmask, &planes, &tris);
+  int p0, p1;
+  obj_parts(O, st, g, p0, p1);
+  const PointHit h = point_to_mesh_group<L>(O, p, p0, p1, *qf, gl, gmask, &planes, &tris);
   __syncwarp(gmask);
   if (st.ops) {
     atomicAdd(st.ops + kOpPlaneTests, (unsigned long long)planes);
@@ -724,7 +735,9 @@ __global__ void __launch_bounds__(GDEV_PQ_BLOCK, 768 / GDEV_PQ_BLOCK) k_point_qu
   const D3 p = ld3(st.qpts + ((size_t)g * st.NQ + slot) * 3);
   unsigned planes, tris;
   int* qf = st.qface + (size_t)g * st.NQ + slot;
-  const PointHit h = point_to_mesh(O, p, *qf, &planes, &tris);
+  int p0, p1;
+  obj_parts(O, st, g, p0, p1);
+  const PointHit h = point_to_mesh(O, p, p0, p1, *qf, &planes, &tris);
   *qf = h.face;
   if (st.ops) {
     atomicAdd(st.ops + kOpPlaneTests, (unsigned long long)planes);
@@ -743,7 +756,8 @@ __global__ void k_points_raw(DevObject O, int n, const double* __restrict__ pts,
                              const int* __restrict__ warm = nullptr) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  const PointHit h = point_to_mesh(O, ld3(pts + 3 * t), warm ? warm[t] : -1);
+  // standalone surface: the context's first object
+  const PointHit h = point_to_mesh(O, ld3(pts + 3 * t), 0, O.obj_pbeg[1], warm ? warm[t] : -1);
   double* o = out + 8 * t;
   o[0] = h.d;
   st3(o + 1, h.pb);
@@ -930,25 +944,28 @@ __device__ __forceinline__ int warp_segment_add(int* counters, int seg, bool act
 __global__ void __launch_bounds__(128) k_pairs_cull(DevHand H, DevObject O, DevState st,
                                                     const int* __restrict__ links, int n_links) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long n = (long long)st.G * n_links * O.P;
+  const long long n = (long long)st.G * n_links * O.Pmax;
   bool need = false;
   int lp = 0, b = 0;
   if (t < n) {
     const int g = (int)(t % st.G);
     lp = (int)(t / st.G);
-    const int link = links ? links[lp / O.P] : lp / O.P;
-    const int part = lp % O.P;
+    const int link = links ? links[lp / O.Pmax] : lp / O.Pmax;
+    const int part = lp % O.Pmax;  // the grasp's object's part index
     if (!st.failed[g]) {
+      int p0, p1;
+      obj_parts(O, st, g, p0, p1);
       const double* w = st.world + ((size_t)g * H.L + link) * 12;
       M33 Rw;
       for (int i = 0; i < 9; ++i) Rw.m[i] = w[i];
-      need = pair_needed(H, O, st, g, link, part, Rw, ld3(w + 9));
+      // slots past the object's parts (multi-object contexts) hold +inf and are never read as pairs
+      need = part < p1 - p0 && pair_needed(H, O, st, g, link, p0 + part, Rw, ld3(w + 9));
       if (!need) {
-        double* o = st.pairs + ((size_t)g * st.NP + link * O.P + part) * 12;
+        double* o = st.pairs + ((size_t)g * st.NP + link * O.Pmax + part) * 12;
         o[0] = INFINITY;
         o[10] = kPairCulled;
       } else {
-        b = pair_bucket(st.pair_hist[(size_t)g * st.NP + link * O.P + part]);
+        b = pair_bucket(st.pair_hist[(size_t)g * st.NP + link * O.Pmax + part]);
       }
     }
     st.pair_need[t] = need ? (unsigned char)(1 + b) : 0;
@@ -1070,7 +1087,9 @@ __global__ void __launch_bounds__(GDEV_PQ_BLOCK, 768 / GDEV_PQ_BLOCK) k_point_qu
   const D3 p = ld3(st.qpts + (size_t)t * 3);
   unsigned planes, tris;
   int* qf = st.qface + t;
-  const PointHit h = point_to_mesh(O, p, *qf, &planes, &tris);
+  int p0, p1;
+  obj_parts(O, st, g, p0, p1);
+  const PointHit h = point_to_mesh(O, p, p0, p1, *qf, &planes, &tris);
   *qf = h.face;
   if (st.ops) {
     atomicAdd(st.ops + kOpPlaneTests, (unsigned long long)planes);
@@ -1082,14 +1101,15 @@ __global__ void __launch_bounds__(GDEV_PQ_BLOCK, 768 / GDEV_PQ_BLOCK) k_point_qu
   st3(o + 1, h.pb);
   st3(o + 4, h.n);
   o[7] = h.part;
-  (void)g;
 }
 
 // Hulls and cloud_scale (geometry.cpp:17-23) of a pair slot.
 __device__ __forceinline__ void slot_hulls(const DevHand& H, const DevObject& O, const DevState& st, int slot, Hull& A,
                                            Hull& B, double& scale) {
   const int g = slot / st.NP, lp = slot % st.NP;
-  const int link = lp / O.P, part = lp % O.P;
+  int p0, p1;
+  obj_parts(O, st, g, p0, p1);
+  const int link = lp / O.Pmax, part = p0 + lp % O.Pmax;
   const double* w = st.world + ((size_t)g * H.L + link) * 12;
   set_link_hull(H, link, A);
   A.posed = true;
@@ -1223,7 +1243,9 @@ __global__ void __launch_bounds__(128) k_pairs_big(DevHand H, DevObject O, DevSt
   for (int i = tid; i < count; i += st.big_slots) {
     const int slot = st.ovf_list[i];
     const int g = slot / st.NP, lp = slot % st.NP;
-    const int link = lp / O.P, part = lp % O.P;
+    int p0, p1;
+    obj_parts(O, st, g, p0, p1);
+    const int link = lp / O.Pmax, part = p0 + lp % O.Pmax;
     const double* w = st.world + ((size_t)g * H.L + link) * 12;
     M33 Rw;
     for (int k = 0; k < 9; ++k) Rw.m[k] = w[k];
@@ -1320,7 +1342,7 @@ __global__ void k_eval_depths(DevHand H, DevObject O, DevState st, const double*
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= st.G) return;
   double depth = 0.0;
-  const int np = H.L * O.P;
+  const int np = H.L * O.Pmax;  // slots past the object's parts hold +inf
   for (int i = 0; i < np; ++i) depth = fmax(depth, -st.pairs[((size_t)g * st.NP + i) * 12]);
   pd[g] = 1000.0 * depth;
   depth = 0.0;
@@ -1609,9 +1631,11 @@ __device__ inline Witness select_witness(const DevHand& H, const DevObject& O, c
   w.d = INFINITY;
   w.c_w = w.p_w = mk(0, 0, 0);
   w.n = mk(0, 0, 1);
-  for (int p = 0; p < O.P; ++p) {
-    if (!(obb_sphere(O.part_obb + 15 * p, center, env) < reference + 1e-9)) continue;
-    const double* r = st.pairs + ((size_t)g * st.NP + link * O.P + p) * 12;
+  int p0, p1;
+  obj_parts(O, st, g, p0, p1);
+  for (int p = 0; p < p1 - p0; ++p) {
+    if (!(obb_sphere(O.part_obb + 15 * (p0 + p), center, env) < reference + 1e-9)) continue;
+    const double* r = st.pairs + ((size_t)g * st.NP + link * O.Pmax + p) * 12;
     if (r[0] < w.d) {
       w.d = r[0];
       w.c_w = ld3(r + 1);
@@ -1637,7 +1661,7 @@ __global__ void __launch_bounds__(64) k_step_mesh(DevHand H, DevObject O, DevPar
   double e_lim, e_self;
   limit_and_self(H, P, s, lane, acc, with_grad, e_lim, e_self);
 
-  const int npairs = H.L * O.P;
+  const int npairs = H.L * O.Pmax;  // slots past the object's parts hold +inf (no hinge)
   const double* pr = st.pairs + (size_t)g * st.NP * 12;
   double total = P.w_limit * e_lim;
   total += P.w_self * e_self;
@@ -1651,7 +1675,7 @@ __global__ void __launch_bounds__(64) k_step_mesh(DevHand H, DevObject O, DevPar
       if (d < 0.0) {
         term = P.w_pen * d * d;
         active = true;
-        if (with_grad) put_item(s, lane, t / O.P, ld3(pr + (size_t)t * 12 + 1), (P.w_pen * 2.0 * d) * ld3(pr + (size_t)t * 12 + 7));
+        if (with_grad) put_item(s, lane, t / O.Pmax, ld3(pr + (size_t)t * 12 + 1), (P.w_pen * 2.0 * d) * ld3(pr + (size_t)t * 12 + 7));
       }
     }
     s.red[lane] = term;

@@ -59,7 +59,9 @@ struct DevHand {
 };
 
 struct DevObject {
-  int P, F;
+  int P, F;                   // parts and faces of all objects in the context
+  int NO, Pmax;               // objects; most parts of one object (pair-slot stride per link)
+  const int* obj_pbeg;        // [NO+1] first part of each object
   const int* part_fbeg;       // [P+1]
   const int* part_vbeg;       // [P+1]
   const double* faces;        // [F*kFaceStride]
@@ -171,6 +173,7 @@ struct DevState {
   double* qpts;     // [G*NQ*3]
   double* qres;     // [G*NQ*8]: d, pb(3), n(3), part
   int* qface;       // [G*NQ] closest face of the slot's last query (warm-start seed), -1 if none
+  const int* obj;   // [G] object of each grasp (multi-object contexts), nullptr = object 0
   int* pq_key;      // [G*NQ] bucket of each query slot (its last closest face's cluster, ...)
   int* pq_count;    // [NC + P + 1] queries per bucket, then the fill cursor
   int* pq_total;    // [1] listed queries

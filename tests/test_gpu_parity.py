@@ -634,22 +634,30 @@ def test_config1_allegro_end_to_end_statistics(G, O, engine, shape):
     assert abs(np.median(eg["pd_mm"]) - np.median(ec["pd_mm"])) <= 0.25 * np.median(ec["pd_mm"]) + 0.5
 
 
-def test_synthesize_objects_equals_per_object_runs(G, trident, engine):
-    """Multi-object synthesis on concurrent engine contexts (config 3 path) returns, per
-    object, exactly the records of a plain per-object synthesize."""
+@pytest.mark.parametrize("single_launch", [True, False])
+def test_synthesize_objects_equals_per_object_runs(G, trident, engine, single_launch):
+    """Multi-object synthesis (config 3 path): one batch over several objects in
+    one context (object id per grasp, parts packed, one set of launches) -- including a
+    multi-part mesh next to single-part primitives of different batch sizes -- and the
+    concurrent-context fallback both return, per object, bitwise the records of a plain
+    per-object synthesize."""
     import dataclasses
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
     objs = [G.make_primitive(n, 0.09) for n in ("sphere", "box", "cylinder")]
+    objs.insert(1, G.load_object(root / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10))
     cfg = G.RunConfig()
     cfg.batch, cfg.seed = 8, 3
     cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 30, 10, 10
-    cfgs = [dataclasses.replace(cfg, seed=i) for i in range(len(objs))]
-    many = G.synthesize_objects(trident, objs, cfgs, streams=3)
+    cfgs = [dataclasses.replace(cfg, seed=i, batch=6 + 3 * i) for i in range(len(objs))]
+    many = G.synthesize_objects(trident, objs, cfgs, streams=3, single_launch=single_launch)
     for obj, c, recs in zip(objs, cfgs, many):
         one = G.synthesize(trident, obj, c)
-        assert len(one) == len(recs)
+        assert len(one) == len(recs) == c.batch
         for a, b in zip(one, recs):
-            assert np.array_equal(a.x, b.x) and np.array_equal(a.x_s, b.x_s)
+            assert np.array_equal(a.x, b.x) and np.array_equal(a.x_s, b.x_s) and np.array_equal(a.x_p, b.x_p)
             assert a.energy_total == b.energy_total or (np.isnan(a.energy_total) and np.isnan(b.energy_total))
+            assert a.failed == b.failed and a.object_id == b.object_id
 
 
 def test_optional_pair_cull_runs_and_agrees(tmp_path):
