@@ -44,6 +44,7 @@ def parse_args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--batch", type=int, default=4096, help="grasps per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true", help="skip the config-3 / config-5 sub-results")
     ap.add_argument("--profile-json", default="", help="also dump the per-kernel profile here")
     return ap.parse_args()
 
@@ -398,10 +399,34 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             line["cpu_baseline"] = cpu_baseline(G, hand, obj, cfg, threads)
+        if world == 1 and not args.no_other_configs:
+            line["other_configs"] = other_configs(not args.no_cpu_baseline)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def other_configs(cpu=True):
+    """The other BASELINE configs measured in the same run (not the headline): config 3 (Leap-like,
+    16 objects x 1024 in one multi-object batch, bench_multi.py) and config 5 (batched lower-level
+    QP at 256k columns, cold as BASELINE defines it and warm-started, bench_qp.py)."""
+    import bench_multi
+    import bench_qp
+    out = {}
+    c3 = bench_multi.run(steps=2, warmup=1, mode="single", cpu=cpu)
+    out["config3"] = {k: c3[k] for k in ("metric", "value", "unit", "ms_per_step", "gpu_launches_per_step",
+                                         "failed_grasps") if k in c3}
+    out["config3"]["config"] = c3["config"]
+    if "cpu_baseline" in c3:
+        out["config3"]["cpu_baseline"] = c3["cpu_baseline"]
+    for name, warm in (("config5", False), ("config5_warm", True)):
+        q = bench_qp.run(sizes=(256000,), steps=3, warmup=2, warm=warm, cpu=cpu and not warm)
+        out[name] = {"metric": q["metric"], "value": q["value"], "unit": q["unit"], "result": q["results"][-1],
+                     "config": q["config"]}
+        if "cpu_baseline" in q:
+            out[name]["cpu_baseline"] = q["cpu_baseline"]
+    return out
 
 
 def C_double_fp64_peak(N, device):
