@@ -267,6 +267,16 @@ void* grasp_ctx_stream(grasp_ctx* ctx);
 int grasp_ctx_set_profiling(grasp_ctx* ctx, int on);
 int grasp_ctx_profile(grasp_ctx* ctx, double* ms /*[8]*/, long long* launches /*[8]*/,
                       unsigned long long* ops /*[20]*/);
+/* Engine options (defaults are the product settings; results never depend on
+ * them except "pair_cull"): "query_buckets" (1: the coarse stage's point
+ * queries listed by spatial bucket, 0: slot order), "query_lanes" (lanes per
+ * point query in all-slot launches, 1 = thread per query; 2..32) and
+ * "tip_query_lanes" (tip-only launches, default 4), "pair_cull" (0: every
+ * (link, part) pair through GJK like the reference; 1: the opt-in separation
+ * cull, exact for the true geometry only) with "pair_sat" (its
+ * link-box vs part-box test, default 1). GRASP_EINVAL for unknown names. */
+int grasp_ctx_set_option(grasp_ctx* ctx, const char* name, int value);
+
 /* Kernels launched by this context so far. */
 long long grasp_ctx_launch_count(grasp_ctx* ctx);
 

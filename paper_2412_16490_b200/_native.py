@@ -133,6 +133,7 @@ SIGNATURES = {
     "grasp_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "grasp_ctx_profile": (C.c_int, [C.c_void_p, _dp, C.POINTER(C.c_longlong), C.POINTER(C.c_ulonglong)]),
     "grasp_ctx_launch_count": (C.c_longlong, [C.c_void_p]),
+    "grasp_ctx_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int]),
     "grasp_ctx_set_trace": (C.c_int, [C.c_void_p, C.POINTER(Trace)]),
     "grasp_measure_fp64_peak": (C.c_int, [C.c_int, _dp]),
 }

@@ -531,6 +531,10 @@ class Engine:
     def stream_handle(self) -> int:
         return N.lib().grasp_ctx_stream(self._ctx) or 0
 
+    def set_option(self, name: str, value: int) -> None:
+        """grasp_ctx_set_option: "query_buckets", "query_lanes", "tip_query_lanes", "pair_cull", "pair_sat"."""
+        N.check(N.lib().grasp_ctx_set_option(self._ctx, name.encode(), int(value)))
+
     def set_profiling(self, on: bool) -> None:
         N.check(N.lib().grasp_ctx_set_profiling(self._ctx, int(bool(on))))
 

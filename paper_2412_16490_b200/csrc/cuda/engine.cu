@@ -99,9 +99,17 @@ struct grasp_ctx {
   bool has_hand = false, has_object = false;
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
   DevBuf<int> pq_key, pq_list, pq_total, pq_count;
-  // Bucket the all-slot point queries by their last closest face's cluster
-  // (GRASP_PQ_BUCKETS=0: slot order).
-  bool bucket_queries = !(std::getenv("GRASP_PQ_BUCKETS") && std::string(std::getenv("GRASP_PQ_BUCKETS")) == "0");
+  // Engine options (grasp_ctx_set_option; defaults = the product settings).
+  bool bucket_queries = true;  // "query_buckets": coarse queries listed by spatial bucket
+  bool opt_cull = false;       // "pair_cull": opt-in separation cull of (link, part) pairs
+  bool opt_sat = true;         // "pair_sat": link-box vs part-box SAT inside that cull
+  int query_lanes = 1;         // "query_lanes": lanes per query in all-slot launches
+  int tip_query_lanes = 4;     // "tip_query_lanes": lanes per query in tip-only launches
+
+  void apply_hand_options() {
+    H.link_box = opt_sat ? h_link_box.p : nullptr;
+    H.cull = opt_cull ? 1 : 0;
+  }
   DevBuf<unsigned char> pair_need, pair_hist, epa_hist;
 
   // hand
@@ -412,8 +420,7 @@ struct grasp_ctx {
     H.cm_idx = h_cm_idx.p;
     H.link_tip = h_link_tip.p;
     H.link_bsphere = h_link_bsphere.p;
-    H.link_box = (std::getenv("GRASP_SAT") && std::string(std::getenv("GRASP_SAT")) == "0") ? nullptr : h_link_box.p;
-    H.cull = std::getenv("GRASP_CULL") && std::string(std::getenv("GRASP_CULL")) == "1";
+    apply_hand_options();
     H.L = L;
     H.dof = dof;
     H.m = m;
@@ -943,14 +950,8 @@ struct grasp_ctx {
   void launch_queries(bool tips_only) {
     const int per = tips_only ? H.m : st.NQ;
     const long long n = static_cast<long long>(st.G) * per;
-    // Lanes per query: GRASP_QGROUP_TIPS (tip-only launches, default 4) and
-    // GRASP_QGROUP (full launches, default 1 = thread per query).
-    auto lanes = [](const char* var, int dflt) {
-      const char* v = std::getenv(var);
-      const int l = v ? std::atoi(v) : dflt;
-      return (l == 2 || l == 4 || l == 8 || l == 16 || l == 32) ? l : 1;
-    };
-    const int L = tips_only ? lanes("GRASP_QGROUP_TIPS", 4) : lanes("GRASP_QGROUP", 1);
+    // Lanes per query (options "tip_query_lanes" / "query_lanes").
+    const int L = tips_only ? tip_query_lanes : query_lanes;
     const int* sl = tips_only ? h_tip_slots.p : nullptr;
     if (!tips_only && L == 1 && bucket_queries) {
       launch(0, [&] {
@@ -1672,6 +1673,10 @@ int grasp_fine_contact_query(grasp_ctx* ctx, int n, const double* x, double* out
 
 }  // extern "C"
 
+// Debug surfaces (EPA internals, warm-start point queries, simplex solves): built
+// only into libgrasp_b200_debug.so (cuda/debug_surfaces.cu defines
+// GRASP_DEBUG_SURFACES and includes this file), never into the product library.
+#ifdef GRASP_DEBUG_SURFACES
 // Debug-only (not in the public header): EPA internals for pair queries.
 namespace {
 __global__ void k_pairs_debug(DevHand H, DevObject O, int n, const int* links, const int* parts, const double* poses,
@@ -1777,6 +1782,8 @@ extern "C" int grasp_debug_cos(int n, const double* w, double* out) {
   });
 }
 
+#endif  // GRASP_DEBUG_SURFACES
+
 // ---------------------------------------------------------------- instrumentation
 namespace {
 __global__ void k_fp64_peak(double* out, int iters) {
@@ -1852,6 +1859,33 @@ int grasp_ctx_set_trace(grasp_ctx* ctx, const grasp_trace* t) {
     ctx->trace_stage.assign(t->stage, t->stage + t->n_snap);
     ctx->trace_iter.assign(t->iter, t->iter + t->n_snap);
     ctx->tracing = t->n_snap > 0;
+  });
+}
+
+int grasp_ctx_set_option(grasp_ctx* ctx, const char* name, int value) {
+  return guard([&] {
+    if (!ctx || !name) throw std::invalid_argument("null argument");
+    const std::string n(name);
+    auto lanes_ok = [](int l) { return l == 1 || l == 2 || l == 4 || l == 8 || l == 16 || l == 32; };
+    std::vector<grasp_ctx*> targets = ctx->shards;
+    targets.push_back(ctx);
+    for (grasp_ctx* c : targets) {
+      if (n == "query_buckets") {
+        c->bucket_queries = value != 0;
+      } else if (n == "pair_cull") {
+        c->opt_cull = value != 0;
+        c->apply_hand_options();
+      } else if (n == "pair_sat") {
+        c->opt_sat = value != 0;
+        c->apply_hand_options();
+      } else if (n == "query_lanes" && lanes_ok(value)) {
+        c->query_lanes = value;
+      } else if (n == "tip_query_lanes" && lanes_ok(value)) {
+        c->tip_query_lanes = value;
+      } else {
+        throw std::invalid_argument("unknown option or value: " + n);
+      }
+    }
   });
 }
 

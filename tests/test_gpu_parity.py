@@ -122,10 +122,40 @@ def test_point_queries_multipart(G, O, trident, engine):
     np.testing.assert_allclose(got[:, :7], ref[:, :7], atol=1e-9, rtol=0)
 
 
-def test_point_queries_warm_start_exact(G, O, engine, trident):
-    """Warm-start seeds (the slot's previous closest face, used as an exact upper
-    bound) must not change any result: random and nearest-face seeds vs no seed,
-    bitwise, and vs the oracle, on the multi-part drill mesh."""
+WARM_START_SCRIPT = r'''
+import ctypes as C, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import paper_2412_16490_b200 as G
+from paper_2412_16490_b200 import _native as N
+from oracle import oracle as O
+from test_gpu_parity import gpu_points, warm_start_checks
+assert N.LIB_PATH.name == "libgrasp_b200_debug.so"
+eng = G.Engine(0)
+warm_start_checks(G, O, eng, G.HandModel.builtin())
+print("warm start ok")
+'''
+
+
+def test_point_queries_warm_start_exact(tmp_path):
+    """Warm-start seeds (the slot's previous closest face, used as an exact upper bound) must not
+    change any result. Runs in a subprocess on the debug library (libgrasp_b200_debug.so: the
+    engine plus grasp_debug_point_to_mesh_warm; the product library carries no debug surface)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    lib = root / "paper_2412_16490_b200/_lib/libgrasp_b200_debug.so"
+    script = tmp_path / "warm.py"
+    script.write_text(WARM_START_SCRIPT)
+    r = subprocess.run([sys.executable, str(script), str(root)], capture_output=True, text=True,
+                       env=dict(os.environ, GRASP_LIB=str(lib)), timeout=600)
+    assert r.returncode == 0 and "warm start ok" in r.stdout, r.stdout + r.stderr
+
+
+def warm_start_checks(G, O, engine, trident):
+    """Random and nearest-face seeds vs no seed, bitwise, and vs the oracle, on the drill mesh."""
     from pathlib import Path
     from paper_2412_16490_b200 import _native as N
     from paper_2412_16490_b200.api import dptr, iptr
@@ -133,7 +163,6 @@ def test_point_queries_warm_start_exact(G, O, engine, trident):
     obj = G.load_object(root / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
     use(engine, trident, obj)
     rng = np.random.default_rng(11)
-    lo, hi = obj.desc.verts[0:1], None
     pts = rng.normal(size=(6000, 3)) * 0.06 + np.array([0.02, 0.0, 0.0])
     nf = int(obj.desc.n_faces)
     cold = gpu_points(engine, pts)
@@ -660,38 +689,29 @@ def test_synthesize_objects_equals_per_object_runs(G, trident, engine, single_la
             assert a.failed == b.failed and a.object_id == b.object_id
 
 
-def test_optional_pair_cull_runs_and_agrees(tmp_path):
-    """The opt-in separation cull (GRASP_CULL=1) runs and, on well-separated
+def test_optional_pair_cull_runs_and_agrees(G):
+    """The opt-in separation cull (option "pair_cull") runs and, on well-separated
     starts, gives the reference-exact default's results except for the grasps where the
     reference's spurious GJK overlaps matter (most grasps identical)."""
-    import subprocess
-    import sys
-    from pathlib import Path
-    root = Path(__file__).resolve().parents[1]
-    script = tmp_path / "cull.py"
-    script.write_text(f"""
-import sys, numpy as np
-sys.path.insert(0, {str(root)!r})
-import paper_2412_16490_b200 as G
-hand = G.HandModel.builtin()
-obj = G.make_primitive('box', 0.1)
-cfg = G.RunConfig(); cfg.batch, cfg.seed = 32, 5
-cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 40, 20, 20
-x0 = G.init_poses(hand, obj, cfg.batch, cfg.seed, cfg.init)
-eng = G.Engine(0); eng.set_hand(hand); eng.set_object(obj)
-np.save(sys.argv[1], eng.synthesize(cfg, x0).x)
-""")
-    import os
-    env0 = dict(os.environ, GRASP_CULL="0")
-    env1 = dict(os.environ, GRASP_CULL="1")
-    subprocess.run([sys.executable, str(script), str(tmp_path / "a.npy")], check=True, env=env0)
-    subprocess.run([sys.executable, str(script), str(tmp_path / "b.npy")], check=True, env=env1)
-    a, b = np.load(tmp_path / "a.npy"), np.load(tmp_path / "b.npy")
+    hand = G.HandModel.builtin()
+    obj = G.make_primitive("box", 0.1)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 32, 5
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 40, 20, 20
+    x0 = G.init_poses(hand, obj, cfg.batch, cfg.seed, cfg.init)
+    eng = G.Engine(0)
+    eng.set_hand(hand)
+    eng.set_object(obj)
+    a = eng.synthesize(cfg, x0).x
+    eng.set_option("pair_cull", 1)
+    b = eng.synthesize(cfg, x0).x
     same = (a == b).all(axis=1)
     assert same.mean() >= 0.75, same.mean()
+    with pytest.raises(G.InvalidArgument):
+        eng.set_option("no_such_option", 1)
 
 
-def test_group_point_queries_bitwise_equal_thread_queries(G, monkeypatch):
+def test_group_point_queries_bitwise_equal_thread_queries(G):
     """The lane-group point query (tip-centre queries of the fine/final stages, 4 lanes per query by
     default) merges its split scans with order-free reductions; any group size must give
     the thread-per-query kernel's results bit for bit, on the tips and on all query slots."""
@@ -707,11 +727,11 @@ def test_group_point_queries_bitwise_equal_thread_queries(G, monkeypatch):
     eng.set_hand(hand)
     eng.set_object(obj)
     outs = {}
-    for tips, full in (("1", "1"), ("4", "1"), ("8", "2"), ("32", "4")):
-        monkeypatch.setenv("GRASP_QGROUP_TIPS", tips)
-        monkeypatch.setenv("GRASP_QGROUP", full)
+    for tips, full in ((1, 1), (4, 1), (8, 2), (32, 4)):
+        eng.set_option("tip_query_lanes", tips)
+        eng.set_option("query_lanes", full)
         outs[(tips, full)] = eng.synthesize(cfg, x0)
-    ref = outs[("1", "1")]
+    ref = outs[(1, 1)]
     for k, o in outs.items():
         assert np.array_equal(o.x, ref.x), k
         assert np.array_equal(o.x_s, ref.x_s), k
@@ -720,9 +740,9 @@ def test_group_point_queries_bitwise_equal_thread_queries(G, monkeypatch):
 
 
 @pytest.mark.parametrize("case", ["shadow_drill", "trident_box"])
-def test_bucketed_point_queries_bitwise(G, monkeypatch, case):
+def test_bucketed_point_queries_bitwise(G, case):
     """The coarse stage's point queries listed by spatial bucket (k_pq_count / k_pq_scatter /
-    k_point_query_list) give bitwise the records of the slot-order launch (GRASP_PQ_BUCKETS=0)."""
+    k_point_query_list) give bitwise the records of the slot-order launch (query_buckets = 0)."""
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
     if case == "shadow_drill":
@@ -735,11 +755,11 @@ def test_bucketed_point_queries_bitwise(G, monkeypatch, case):
     cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 300, 5, 5
     x0 = G.init_poses(hand, obj, cfg.batch, cfg.seed, cfg.init)
     outs = []
-    for flag in ("0", "1"):
-        monkeypatch.setenv("GRASP_PQ_BUCKETS", flag)
+    for flag in (0, 1):
         eng = G.Engine(0)
         eng.set_hand(hand)
         eng.set_object(obj)
+        eng.set_option("query_buckets", flag)
         outs.append(eng.synthesize(cfg, x0))
     for f in ("x", "x_p", "x_s", "energy_total", "stage_energy", "failed", "contact_forces"):
         assert np.array_equal(getattr(outs[0], f), getattr(outs[1], f), equal_nan=True), f
