@@ -129,6 +129,9 @@ struct grasp_ctx {
   DevBuf<float4> o_face_sphere32, o_cluster_sphere32, o_face_box32, o_cluster_box32;
   DevBuf<double4> o_face_plane;
   DevBuf<int> o_part_cbeg, o_cluster_fbeg, o_face_cluster, o_obj_pbeg, obj_ids;
+  DevBuf<int> o_part_gbeg, o_grp_beg, o_grp_face;
+  DevBuf<float4> o_grp_bound;
+  DevBuf<double4> o_grp_plane;
 
   // Bounding sphere (AABB center, max vertex distance, relative slack) of
   // each vertex range [begin[i], begin[i+1]).
@@ -748,6 +751,99 @@ struct grasp_ctx {
       for (size_t c = 0; c + 1 < cluster_fbeg.size(); ++c)
         for (int f = cluster_fbeg[c]; f < cluster_fbeg[c + 1]; ++f) fc[f] = static_cast<int>(c);
       o_face_cluster.upload(fc, s);
+    }
+    // Plane groups for the inside test: per part, the non-degenerate faces
+    // ordered by the cube-map cell of their normal (6 x 8 x 8 cells), then
+    // by index; each cell's faces split into groups of at most kPlaneGroup.
+    // Degenerate faces are left out: their plane (0, 0, 0, +inf) never
+    // separates and never holds the minimum depth.
+    {
+      constexpr int kPlaneGroup = 16, kCellN = 8;
+      auto normal_cell = [](const double* n) {
+        const double ax = std::fabs(n[0]), ay = std::fabs(n[1]), az = std::fabs(n[2]);
+        int face;
+        double m, pu, pv;
+        if (ax >= ay && ax >= az) {
+          face = n[0] >= 0 ? 0 : 1, m = ax, pu = n[1], pv = n[2];
+        } else if (ay >= az) {
+          face = n[1] >= 0 ? 2 : 3, m = ay, pu = n[0], pv = n[2];
+        } else {
+          face = n[2] >= 0 ? 4 : 5, m = az, pu = n[0], pv = n[1];
+        }
+        const int iu = std::min(kCellN - 1, std::max(0, static_cast<int>((pu / m + 1.0) * 0.5 * kCellN)));
+        const int iv = std::min(kCellN - 1, std::max(0, static_cast<int>((pv / m + 1.0) * 0.5 * kCellN)));
+        return (face * kCellN + iu) * kCellN + iv;
+      };
+      std::vector<int> part_gbeg(P + 1, 0), grp_beg, grp_face;
+      std::vector<float4> grp_bound;
+      std::vector<double4> grp_plane;
+      for (int p = 0; p < P; ++p) {
+        part_gbeg[p] = static_cast<int>(grp_beg.size());
+        std::vector<std::pair<int, int>> order;  // (cell, face)
+        for (int f = fbeg[p]; f < fbeg[p + 1]; ++f) {
+          const double* F = faces.data() + static_cast<size_t>(f) * kFaceStride;
+          if (F[13] != 0.0) order.emplace_back(normal_cell(F + 9), f);
+        }
+        std::sort(order.begin(), order.end());
+        size_t a = 0;
+        while (a < order.size()) {
+          size_t b = a;
+          while (b < order.size() && order[b].first == order[a].first) ++b;
+          const size_t cnt = b - a, ng = (cnt + kPlaneGroup - 1) / kPlaneGroup;
+          for (size_t gi = 0; gi < ng; ++gi) {
+            const size_t g0 = a + cnt * gi / ng, g1 = a + cnt * (gi + 1) / ng;
+            double nc[3] = {0, 0, 0}, C[3] = {0, 0, 0};
+            for (size_t q = g0; q < g1; ++q) {
+              const double* F = faces.data() + static_cast<size_t>(order[q].second) * kFaceStride;
+              for (int k = 0; k < 3; ++k) {
+                nc[k] += F[9 + k];
+                C[k] += face_sphere[4 * order[q].second + k] / static_cast<double>(g1 - g0);
+              }
+            }
+            const double ln = std::sqrt(nc[0] * nc[0] + nc[1] * nc[1] + nc[2] * nc[2]);
+            // the bound is evaluated in fp32: n_g and C_g are rounded first and
+            // h_g, delta_g measured from the rounded values (then rounded
+            // outward)
+            for (int k = 0; k < 3; ++k) {
+              nc[k] = static_cast<float>(nc[k] / ln);
+              C[k] = static_cast<float>(C[k]);
+            }
+            double delta = 0.0, h = INFINITY;
+            grp_beg.push_back(static_cast<int>(grp_plane.size()));
+            for (size_t q = g0; q < g1; ++q) {
+              const int f = order[q].second;
+              const double* F = faces.data() + static_cast<size_t>(f) * kFaceStride;
+              const double dn[3] = {F[9] - nc[0], F[10] - nc[1], F[11] - nc[2]};
+              delta = std::max(delta, std::sqrt(dn[0] * dn[0] + dn[1] * dn[1] + dn[2] * dn[2]));
+              h = std::min(h, F[12] - (F[9] * C[0] + F[10] * C[1] + F[11] * C[2]));
+              grp_plane.push_back(planes[f]);
+              grp_face.push_back(f);
+            }
+            grp_bound.push_back(make_float4(static_cast<float>(nc[0]), static_cast<float>(nc[1]),
+                                            static_cast<float>(nc[2]), std::nextafter(static_cast<float>(h), -1e30f)));
+            grp_bound.push_back(make_float4(static_cast<float>(C[0]), static_cast<float>(C[1]), static_cast<float>(C[2]),
+                                            std::nextafter(static_cast<float>(delta * (1.0 + 1e-6) + 1e-9), 1e30f)));
+          }
+          a = b;
+        }
+      }
+      part_gbeg[P] = static_cast<int>(grp_beg.size());
+      grp_beg.push_back(static_cast<int>(grp_plane.size()));
+      if (grp_plane.empty()) {  // keep the buffers non-empty
+        grp_plane.push_back(make_double4(0, 0, 0, INFINITY));
+        grp_face.push_back(0);
+        grp_bound.assign(2, make_float4(0, 0, 0, 0));
+      }
+      o_part_gbeg.upload(part_gbeg, s);
+      o_grp_beg.upload(grp_beg, s);
+      o_grp_face.upload(grp_face, s);
+      o_grp_bound.upload(grp_bound, s);
+      o_grp_plane.upload(grp_plane, s);
+      O.part_gbeg = o_part_gbeg.p;
+      O.grp_beg = o_grp_beg.p;
+      O.grp_face = o_grp_face.p;
+      O.grp_bound = o_grp_bound.p;
+      O.grp_plane = o_grp_plane.p;
     }
     {
       std::vector<int> base, off;

@@ -207,7 +207,7 @@ struct PointHit {
   double d;
   D3 pb, n;
   int part;
-  int face;  // closest face when the winning part was outside, else -1
+  int face;  // winning part's closest face (outside) or shallowest face (inside); -1 if none
 };
 
 // point_to_mesh (geometry.cpp:527-542) with query_part (:355-395): inside
@@ -301,11 +301,13 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p
     }
     // Face clusters (runs of consecutive faces with fp32 bounding spheres):
     // an upper bound on the part distance (min |p-C| + R) and a seed face,
-    // the smallest sphere lower bound in the nearest cluster.
+    // the smallest sphere lower bound in the nearest cluster. The warm face,
+    // when it is one of this part's, is the seed instead (its exact distance
+    // is already the bound).
     const int c0 = __ldg(O.part_cbeg + part), c1 = __ldg(O.part_cbeg + part + 1);
     float ubA = INFINITY;
-    int seed_f;
-    {
+    int seed_f = warm_face;
+    if (!(warm_face >= f0 && warm_face < f1)) {
       float lb_seed = INFINITY;
       int seed_c = c0;
       for (int c = c0; c < c1; ++c) {
@@ -333,47 +335,60 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p
     }
     // Inside test (query_part, geometry.cpp:369-383): inside iff no face
     // plane has depth < -1e-12; then the shallowest face in index order
-    // (strict '<'). Whether some plane separates does not depend on the
-    // order the planes are tried, so the seed face's plane (usually a
-    // separating one for outside points) is tried first. Plane records are
-    // (n, n.a) with degenerate faces stored as (0, +inf), which neither
-    // separates nor wins the minimum, i.e. is skipped as in the reference.
+    // (strict '<'), i.e. the lexicographic minimum of (depth, face). Neither
+    // depends on the order the planes are tried, so the seed face's plane
+    // (usually a separating one for outside points) and the warm face's are
+    // tried first, and the planes are then visited by normal group (model.cuh
+    // grp_*): a group whose depth lower bound h_g + n_g.(C_g - p) -
+    // delta_g |C_g - p| exceeds a known depth can neither separate nor hold
+    // the minimum, so it is skipped. Plane records are (n, n.a) with
+    // degenerate faces stored as (0, +inf), which neither separates nor wins
+    // the minimum, i.e. is skipped as in the reference.
     bool inside;
     double min_depth = INFINITY;
     D3 best_n = mk(0, 0, 1);
+    int min_f = -1;
+    double ub_depth;  // a depth of some plane of the part (>= the minimum)
     {
       const double4 Q = ld_plane(O, seed_f);
       ++planes;
-      inside = !((Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z)) < -1e-12);
+      ub_depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
+      inside = !(ub_depth < -1e-12);
+    }
+    if (inside && warm_face >= f0 && warm_face < f1 && warm_face != seed_f) {
+      const double4 Q = ld_plane(O, warm_face);
+      ++planes;
+      const double depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
+      inside = !(depth < -1e-12);
+      ub_depth = fmin(ub_depth, depth);
     }
     if (inside) {
-      int f = f0;
-      for (; f + 4 <= f1 && inside; f += 4) {
-        double4 Q[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) Q[i] = ld_plane(O, f + i);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (!inside) break;
+      const int q1 = __ldg(O.part_gbeg + part + 1);
+      for (int q = __ldg(O.part_gbeg + part); q < q1 && inside; ++q) {
+        {
+          // fp32 with |r| <= |r|_1 (a weaker bound, no square root); the
+          // rounding (~1e-8 m) is far inside kCullSlack32
+          const float4 B0 = __ldg(O.grp_bound + 2 * q), B1 = __ldg(O.grp_bound + 2 * q + 1);
+          const float rx = B1.x - px, ry = B1.y - py, rz = B1.z - pz;
+          const float lb = (B0.w + (B0.x * rx + B0.y * ry + B0.z * rz)) - B1.w * (fabsf(rx) + fabsf(ry) + fabsf(rz));
+          if (lb > (float)fmin(ub_depth, min_depth) + kCullSlack32) continue;
+        }
+        const int k1 = __ldg(O.grp_beg + q + 1);
+        for (int k = __ldg(O.grp_beg + q); k < k1; ++k) {
+          const double2* qq = reinterpret_cast<const double2*>(O.grp_plane + k);
+          const double2 qa = __ldg(qq), qb = __ldg(qq + 1);
           ++planes;
-          const double depth = Q[i].w - (Q[i].x * p.x + Q[i].y * p.y + Q[i].z * p.z);
+          const double depth = qb.y - (qa.x * p.x + qa.y * p.y + qb.x * p.z);
           if (depth < -1e-12) {
             inside = false;
-          } else if (depth < min_depth) {
-            min_depth = depth;
-            best_n = mk(Q[i].x, Q[i].y, Q[i].z);
+            break;
           }
-        }
-      }
-      for (; f < f1 && inside; ++f) {
-        const double4 Q = ld_plane(O, f);
-        ++planes;
-        const double depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
-        if (depth < -1e-12) {
-          inside = false;
-        } else if (depth < min_depth) {
-          min_depth = depth;
-          best_n = mk(Q.x, Q.y, Q.z);
+          const int f = __ldg(O.grp_face + k);
+          if (depth < min_depth || (depth == min_depth && f < min_f)) {
+            min_depth = depth;
+            best_n = mk(qa.x, qa.y, qb.x);
+            min_f = f;
+          }
         }
       }
     }
@@ -384,6 +399,7 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p
       sd = -min_depth;
       nn = best_n;
       pt = p + best_n * min_depth;
+      sf = min_f;  // the shallowest face: the next query's warm start
     } else {
       // Brute-force closest point over the faces in index order with strict
       // '<' (geometry.cpp:384-392), evaluated exactly only where it can
@@ -396,9 +412,12 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p
       // kCullSlack32 (conservative).
       float bound;
       {
-        ++tris;
-        const double* F = O.faces + (size_t)seed_f * kFaceStride;
-        const double d_seed = nrm(p - closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6)));
+        double d_seed = ub_warm;
+        if (seed_f != warm_face) {
+          ++tris;
+          const double* F = O.faces + (size_t)seed_f * kFaceStride;
+          d_seed = nrm(p - closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6)));
+        }
         bound = fminf(fminf(ubA, __double2float_ru(d_seed)), __double2float_ru(ub_warm)) + kCullSlack32;
       }
       sd = INFINITY;
@@ -605,6 +624,7 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int p0, int p1
       sd = -min_depth;
       nn = best_n;
       pt = p + best_n * min_depth;
+      sf = min_face;
     } else {
       float bound;
       {
@@ -724,7 +744,10 @@ __global__ void __launch_bounds__(GDEV_PQG_BLOCK) k_point_query_group(DevObject 
 #ifndef GDEV_PQ_BLOCK
 #define GDEV_PQ_BLOCK 64  // 64 and 32 measured 3% faster than 128 (finer tail)
 #endif
-__global__ void __launch_bounds__(GDEV_PQ_BLOCK, 768 / GDEV_PQ_BLOCK) k_point_query(DevObject O, DevState st, const int* __restrict__ slots,
+#ifndef GDEV_PQ_THREADS_PER_SM
+#define GDEV_PQ_THREADS_PER_SM 768
+#endif
+__global__ void __launch_bounds__(GDEV_PQ_BLOCK, GDEV_PQ_THREADS_PER_SM / GDEV_PQ_BLOCK) k_point_query(DevObject O, DevState st, const int* __restrict__ slots,
                                                         int n_slots) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int per = slots ? n_slots : st.NQ;
@@ -1079,7 +1102,7 @@ __global__ void __launch_bounds__(128) k_pq_scatter(DevState st) {
 }
 
 // k_point_query over the bucketed list.
-__global__ void __launch_bounds__(GDEV_PQ_BLOCK, 768 / GDEV_PQ_BLOCK) k_point_query_list(DevObject O, DevState st) {
+__global__ void __launch_bounds__(GDEV_PQ_BLOCK, GDEV_PQ_THREADS_PER_SM / GDEV_PQ_BLOCK) k_point_query_list(DevObject O, DevState st) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *st.pq_total) return;
   const int t = st.pq_list[i];

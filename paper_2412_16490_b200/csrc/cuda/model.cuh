@@ -84,7 +84,15 @@ struct DevObject {
   const unsigned short* cm_idx;
   int NC;                          // face clusters
   const int* face_cluster;         // [F] cluster of each face (point-query bucketing)
+  // Plane groups (inside test): each part's non-degenerate face planes grouped
+  // by normal direction, with a lower bound on the group's plane depths.
+  const int* part_gbeg;            // [P+1] plane groups of each part
+  const int* grp_beg;              // [NG+1] first entry of each group in grp_plane / grp_face
+  const float4* grp_bound;         // [NG*2] (n_g, h_g), (C_g, delta_g): fp32, h_g <= min (w_f - n_f.C_g), delta_g >= max |n_f - n_g|
+  const double4* grp_plane;        // planes in group order (copies of face_plane)
+  const int* grp_face;             // face index of each entry
 };
+
 
 // Support maps (cube map of directions -> candidate support vertices). A hull
 // with at least kSupportMapMinVerts vertices gets, for each of the 6 * N * N

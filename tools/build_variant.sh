@@ -12,5 +12,5 @@ $NV --fmad=false -c cuda/engine.cu -o $OUT/$NAME/engine.o 2> $OUT/$NAME/ptxas_en
 $NV -c cuda/qp.cu -o $OUT/$NAME/qp.o 2> $OUT/$NAME/ptxas_qp.log &
 wait
 /usr/local/cuda/bin/nvcc -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -o $OUT/libgrasp_b200_$NAME.so \
-  $(ls $OBJ/*.o | grep -v -e engine.o -e qp.o) $OUT/$NAME/engine.o $OUT/$NAME/qp.o -lpthread
+  $(ls $OBJ/*.o | grep -v -e engine.o -e qp.o -e engine_debug.o) $OUT/$NAME/engine.o $OUT/$NAME/qp.o -lpthread
 echo built $OUT/libgrasp_b200_$NAME.so
