@@ -129,8 +129,8 @@ struct grasp_ctx {
   DevBuf<float4> o_face_sphere32, o_cluster_sphere32, o_face_box32, o_cluster_box32;
   DevBuf<double4> o_face_plane;
   DevBuf<int> o_part_cbeg, o_cluster_fbeg, o_face_cluster, o_obj_pbeg, obj_ids;
-  DevBuf<int> o_part_gbeg, o_grp_beg, o_grp_face;
-  DevBuf<float4> o_grp_bound;
+  DevBuf<int> o_part_gbeg, o_grp_beg, o_grp_face, o_sup_gbeg;
+  DevBuf<float4> o_grp_bound, o_sup_bound;
   DevBuf<double4> o_grp_plane;
 
   // Bounding sphere (AABB center, max vertex distance, relative slack) of
@@ -162,7 +162,7 @@ struct grasp_ctx {
   DevState st{};
   DevBuf<double> x, pose, world, joints, qpts, qres, pairs, warm_x, warm_y, out_z, qp_force, qp_energy, qp_perdir,
       frames, anchors, energy, grad, stage_energy, x_p, x_s, witness;
-  DevBuf<int> qp_iters, qp_conv, qp_ready, failed, have_pregrasp, err, ovf_count, ovf_list, qface;
+  DevBuf<int> qp_iters, qp_conv, qp_ready, failed, have_pregrasp, err, ovf_count, ovf_list, qface, qsep;
   DevBuf<EpaScratchBig> big_scratch;
   static constexpr int kBigSlots = 1024;
   DevBuf<double> epa_jobs;  // EPA jobs handed from k_pairs_list to k_pairs_epa
@@ -753,10 +753,12 @@ struct grasp_ctx {
       o_face_cluster.upload(fc, s);
     }
     // Plane groups for the inside test: per part, the non-degenerate faces
-    // ordered by the cube-map cell of their normal (6 x 8 x 8 cells), then
-    // by index; each cell's faces split into groups of at most kPlaneGroup.
-    // Degenerate faces are left out: their plane (0, 0, 0, +inf) never
-    // separates and never holds the minimum depth.
+    // ordered by the cube-map cell of their normal (6 x 8 x 8 cells, ordered
+    // so that each 4 x 4 block of a cube face is contiguous), then by index;
+    // each cell's faces split into groups of at most kPlaneGroup, and each
+    // 4 x 4 block's groups form a super-group with its own bound. Degenerate
+    // faces are left out: their plane (0, 0, 0, +inf) never separates and
+    // never holds the minimum depth.
     {
       constexpr int kPlaneGroup = 16, kCellN = 8;
       auto normal_cell = [](const double* n) {
@@ -772,13 +774,43 @@ struct grasp_ctx {
         }
         const int iu = std::min(kCellN - 1, std::max(0, static_cast<int>((pu / m + 1.0) * 0.5 * kCellN)));
         const int iv = std::min(kCellN - 1, std::max(0, static_cast<int>((pv / m + 1.0) * 0.5 * kCellN)));
-        return (face * kCellN + iu) * kCellN + iv;
+        return (((face * 2 + iu / 4) * 2 + iv / 4) * 4 + iu % 4) * 4 + iv % 4;  // super-group = cell / 16
       };
-      std::vector<int> part_gbeg(P + 1, 0), grp_beg, grp_face;
-      std::vector<float4> grp_bound;
+      // Bound of the faces order[g0, g1): fp32 (n_g, h_g), (C_g, delta_g). The
+      // bound is evaluated in fp32: n_g and C_g are rounded first and h_g,
+      // delta_g measured from the rounded values (then rounded outward).
+      auto group_bound = [&](const std::vector<std::pair<int, int>>& order, size_t g0, size_t g1,
+                             std::vector<float4>& out) {
+        double nc[3] = {0, 0, 0}, C[3] = {0, 0, 0};
+        for (size_t q = g0; q < g1; ++q) {
+          const double* F = faces.data() + static_cast<size_t>(order[q].second) * kFaceStride;
+          for (int k = 0; k < 3; ++k) {
+            nc[k] += F[9 + k];
+            C[k] += face_sphere[4 * order[q].second + k] / static_cast<double>(g1 - g0);
+          }
+        }
+        const double ln = std::sqrt(nc[0] * nc[0] + nc[1] * nc[1] + nc[2] * nc[2]);
+        for (int k = 0; k < 3; ++k) {
+          nc[k] = ln > 0 ? static_cast<float>(nc[k] / ln) : 0.0f;
+          C[k] = static_cast<float>(C[k]);
+        }
+        double delta = 0.0, h = INFINITY;
+        for (size_t q = g0; q < g1; ++q) {
+          const double* F = faces.data() + static_cast<size_t>(order[q].second) * kFaceStride;
+          const double dn[3] = {F[9] - nc[0], F[10] - nc[1], F[11] - nc[2]};
+          delta = std::max(delta, std::sqrt(dn[0] * dn[0] + dn[1] * dn[1] + dn[2] * dn[2]));
+          h = std::min(h, F[12] - (F[9] * C[0] + F[10] * C[1] + F[11] * C[2]));
+        }
+        out.push_back(make_float4(static_cast<float>(nc[0]), static_cast<float>(nc[1]), static_cast<float>(nc[2]),
+                                  std::nextafter(static_cast<float>(h), -1e30f)));
+        out.push_back(make_float4(static_cast<float>(C[0]), static_cast<float>(C[1]), static_cast<float>(C[2]),
+                                  std::nextafter(static_cast<float>(delta * (1.0 + 1e-6) + 1e-9), 1e30f)));
+      };
+      std::vector<int> part_gbeg(P + 1, 0), grp_beg, grp_face, sup_gbeg;
+      std::vector<float4> grp_bound, sup_bound;
       std::vector<double4> grp_plane;
       for (int p = 0; p < P; ++p) {
-        part_gbeg[p] = static_cast<int>(grp_beg.size());
+        part_gbeg[p] = static_cast<int>(sup_gbeg.size());
         std::vector<std::pair<int, int>> order;  // (cell, face)
         for (int f = fbeg[p]; f < fbeg[p + 1]; ++f) {
           const double* F = faces.data() + static_cast<size_t>(f) * kFaceStride;
@@ -787,53 +819,42 @@ struct grasp_ctx {
         std::sort(order.begin(), order.end());
         size_t a = 0;
         while (a < order.size()) {
-          size_t b = a;
-          while (b < order.size() && order[b].first == order[a].first) ++b;
-          const size_t cnt = b - a, ng = (cnt + kPlaneGroup - 1) / kPlaneGroup;
-          for (size_t gi = 0; gi < ng; ++gi) {
-            const size_t g0 = a + cnt * gi / ng, g1 = a + cnt * (gi + 1) / ng;
-            double nc[3] = {0, 0, 0}, C[3] = {0, 0, 0};
-            for (size_t q = g0; q < g1; ++q) {
-              const double* F = faces.data() + static_cast<size_t>(order[q].second) * kFaceStride;
-              for (int k = 0; k < 3; ++k) {
-                nc[k] += F[9 + k];
-                C[k] += face_sphere[4 * order[q].second + k] / static_cast<double>(g1 - g0);
+          size_t e = a;  // super-group [a, e)
+          while (e < order.size() && order[e].first / 16 == order[a].first / 16) ++e;
+          sup_gbeg.push_back(static_cast<int>(grp_beg.size()));
+          group_bound(order, a, e, sup_bound);
+          size_t c = a;
+          while (c < e) {
+            size_t b = c;
+            while (b < e && order[b].first == order[c].first) ++b;
+            const size_t cnt = b - c, ng = (cnt + kPlaneGroup - 1) / kPlaneGroup;
+            for (size_t gi = 0; gi < ng; ++gi) {
+              const size_t g0 = c + cnt * gi / ng, g1 = c + cnt * (gi + 1) / ng;
+              grp_beg.push_back(static_cast<int>(grp_plane.size()));
+              group_bound(order, g0, g1, grp_bound);
+              for (size_t q = g0; q < g1; ++q) {
+                grp_plane.push_back(planes[order[q].second]);
+                grp_face.push_back(order[q].second);
               }
             }
-            const double ln = std::sqrt(nc[0] * nc[0] + nc[1] * nc[1] + nc[2] * nc[2]);
-            // the bound is evaluated in fp32: n_g and C_g are rounded first and
-            // h_g, delta_g measured from the rounded values (then rounded
-            // outward)
-            for (int k = 0; k < 3; ++k) {
-              nc[k] = static_cast<float>(nc[k] / ln);
-              C[k] = static_cast<float>(C[k]);
-            }
-            double delta = 0.0, h = INFINITY;
-            grp_beg.push_back(static_cast<int>(grp_plane.size()));
-            for (size_t q = g0; q < g1; ++q) {
-              const int f = order[q].second;
-              const double* F = faces.data() + static_cast<size_t>(f) * kFaceStride;
-              const double dn[3] = {F[9] - nc[0], F[10] - nc[1], F[11] - nc[2]};
-              delta = std::max(delta, std::sqrt(dn[0] * dn[0] + dn[1] * dn[1] + dn[2] * dn[2]));
-              h = std::min(h, F[12] - (F[9] * C[0] + F[10] * C[1] + F[11] * C[2]));
-              grp_plane.push_back(planes[f]);
-              grp_face.push_back(f);
-            }
-            grp_bound.push_back(make_float4(static_cast<float>(nc[0]), static_cast<float>(nc[1]),
-                                            static_cast<float>(nc[2]), std::nextafter(static_cast<float>(h), -1e30f)));
-            grp_bound.push_back(make_float4(static_cast<float>(C[0]), static_cast<float>(C[1]), static_cast<float>(C[2]),
-                                            std::nextafter(static_cast<float>(delta * (1.0 + 1e-6) + 1e-9), 1e30f)));
+            c = b;
           }
-          a = b;
+          a = e;
         }
       }
-      part_gbeg[P] = static_cast<int>(grp_beg.size());
+      part_gbeg[P] = static_cast<int>(sup_gbeg.size());
+      sup_gbeg.push_back(static_cast<int>(grp_beg.size()));
       grp_beg.push_back(static_cast<int>(grp_plane.size()));
       if (grp_plane.empty()) {  // keep the buffers non-empty
         grp_plane.push_back(make_double4(0, 0, 0, INFINITY));
         grp_face.push_back(0);
         grp_bound.assign(2, make_float4(0, 0, 0, 0));
+        sup_bound.assign(2, make_float4(0, 0, 0, 0));
       }
+      o_sup_gbeg.upload(sup_gbeg, s);
+      o_sup_bound.upload(sup_bound, s);
+      O.sup_gbeg = o_sup_gbeg.p;
+      O.sup_bound = o_sup_bound.p;
       o_part_gbeg.upload(part_gbeg, s);
       o_grp_beg.upload(grp_beg, s);
       o_grp_face.upload(grp_face, s);
@@ -930,6 +951,9 @@ struct grasp_ctx {
     st.pq_count = pq_count.p;
     ck(cudaMemsetAsync(qface.p, 0xff, sizeof(int) * g * NQ, stream), "memset");
     st.qface = qface.p;
+    qsep.ensure(g * NQ);
+    ck(cudaMemsetAsync(qsep.p, 0xff, sizeof(int) * g * NQ, stream), "memset");
+    st.qsep = qsep.p;
     failed.ensure(g);
     have_pregrasp.ensure(g);
     err.ensure(4);

@@ -208,6 +208,7 @@ struct PointHit {
   D3 pb, n;
   int part;
   int face;  // winning part's closest face (outside) or shallowest face (inside); -1 if none
+  int sep;   // face whose plane separated the point from the winning part, -1 if inside / none
 };
 
 // point_to_mesh (geometry.cpp:527-542) with query_part (:355-395): inside
@@ -267,13 +268,15 @@ __device__ __forceinline__ void obj_parts(const DevObject& O, const DevState& st
 // point_to_mesh(p, parts [p0, p1)) (geometry.cpp:527-542); the part index
 // returned is global (p0 + the object's part index).
 __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p1, int warm_face = -1,
-                                         unsigned* plane_tests = nullptr, unsigned* tri_tests = nullptr) {
+                                         unsigned* plane_tests = nullptr, unsigned* tri_tests = nullptr,
+                                         int warm_sep = -1) {
   PointHit best;
   best.d = INFINITY;
   best.pb = mk(0, 0, 0);
   best.n = mk(0, 0, 1);
   best.part = -1;
   best.face = -1;
+  best.sep = -1;
   unsigned planes = 0, tris = 0;
   const float px = (float)p.x, py = (float)p.y, pz = (float)p.z;
   // Warm start: the exact distance to any face (here the slot's closest face
@@ -337,8 +340,9 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p
     // plane has depth < -1e-12; then the shallowest face in index order
     // (strict '<'), i.e. the lexicographic minimum of (depth, face). Neither
     // depends on the order the planes are tried, so the seed face's plane
-    // (usually a separating one for outside points) and the warm face's are
-    // tried first, and the planes are then visited by normal group (model.cuh
+    // (usually a separating one for outside points), the warm face's and the
+    // plane that separated the slot's last query are tried first, and the
+    // planes are then visited by normal group (model.cuh
     // grp_*): a group whose depth lower bound h_g + n_g.(C_g - p) -
     // delta_g |C_g - p| exceeds a known depth can neither separate nor hold
     // the minimum, so it is skipped. Plane records are (n, n.a) with
@@ -348,46 +352,63 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p
     double min_depth = INFINITY;
     D3 best_n = mk(0, 0, 1);
     int min_f = -1;
+    int sep_f = -1;
     double ub_depth;  // a depth of some plane of the part (>= the minimum)
     {
       const double4 Q = ld_plane(O, seed_f);
       ++planes;
       ub_depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
       inside = !(ub_depth < -1e-12);
+      sep_f = inside ? -1 : seed_f;
+    }
+    if (inside && warm_sep >= f0 && warm_sep < f1 && warm_sep != seed_f) {
+      const double4 Q = ld_plane(O, warm_sep);
+      ++planes;
+      const double depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
+      inside = !(depth < -1e-12);
+      sep_f = inside ? -1 : warm_sep;
+      ub_depth = fmin(ub_depth, depth);
     }
     if (inside && warm_face >= f0 && warm_face < f1 && warm_face != seed_f) {
       const double4 Q = ld_plane(O, warm_face);
       ++planes;
       const double depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
       inside = !(depth < -1e-12);
+      sep_f = inside ? -1 : warm_face;
       ub_depth = fmin(ub_depth, depth);
     }
     if (inside) {
-      const int q1 = __ldg(O.part_gbeg + part + 1);
-      for (int q = __ldg(O.part_gbeg + part); q < q1 && inside; ++q) {
-        {
-          // fp32 with |r| <= |r|_1 (a weaker bound, no square root); the
-          // rounding (~1e-8 m) is far inside kCullSlack32
-          const float4 B0 = __ldg(O.grp_bound + 2 * q), B1 = __ldg(O.grp_bound + 2 * q + 1);
-          const float rx = B1.x - px, ry = B1.y - py, rz = B1.z - pz;
-          const float lb = (B0.w + (B0.x * rx + B0.y * ry + B0.z * rz)) - B1.w * (fabsf(rx) + fabsf(ry) + fabsf(rz));
-          if (lb > (float)fmin(ub_depth, min_depth) + kCullSlack32) continue;
-        }
-        const int k1 = __ldg(O.grp_beg + q + 1);
-        for (int k = __ldg(O.grp_beg + q); k < k1; ++k) {
-          const double2* qq = reinterpret_cast<const double2*>(O.grp_plane + k);
-          const double2 qa = __ldg(qq), qb = __ldg(qq + 1);
-          ++planes;
-          const double depth = qb.y - (qa.x * p.x + qa.y * p.y + qb.x * p.z);
-          if (depth < -1e-12) {
-            inside = false;
-            break;
-          }
-          const int f = __ldg(O.grp_face + k);
-          if (depth < min_depth || (depth == min_depth && f < min_f)) {
-            min_depth = depth;
-            best_n = mk(qa.x, qa.y, qb.x);
-            min_f = f;
+      // fp32 bound with |r| <= |r|_1 (weaker, no square root); the rounding
+      // (~1e-8 m) is far inside kCullSlack32
+      auto group_far = [&](const float4* B) {
+        const float4 B0 = __ldg(B), B1 = __ldg(B + 1);
+        const float rx = B1.x - px, ry = B1.y - py, rz = B1.z - pz;
+        const float lb = (B0.w + (B0.x * rx + B0.y * ry + B0.z * rz)) - B1.w * (fabsf(rx) + fabsf(ry) + fabsf(rz));
+        return lb > (float)fmin(ub_depth, min_depth) + kCullSlack32;
+      };
+      const int s1 = __ldg(O.part_gbeg + part + 1);
+      for (int sg = __ldg(O.part_gbeg + part); sg < s1 && inside; ++sg) {
+        if (group_far(O.sup_bound + 2 * sg)) continue;
+        const int q1 = __ldg(O.sup_gbeg + sg + 1);
+        for (int q = __ldg(O.sup_gbeg + sg); q < q1 && inside; ++q) {
+          if (group_far(O.grp_bound + 2 * q)) continue;
+          const int k1 = __ldg(O.grp_beg + q + 1);
+          for (int k = __ldg(O.grp_beg + q); k < k1; ++k) {
+            const double2* qq = reinterpret_cast<const double2*>(O.grp_plane + k);
+            const double2 qa = __ldg(qq), qb = __ldg(qq + 1);
+            ++planes;
+            const double depth = qb.y - (qa.x * p.x + qa.y * p.y + qb.x * p.z);
+            const int f = __ldg(O.grp_face + k);
+            if (depth < -1e-12) {
+              inside = false;
+              sep_f = f;
+              break;
+            }
+            if (depth < min_depth || (depth == min_depth && f < min_f)) {
+              min_depth = depth;
+              best_n = mk(qa.x, qa.y, qb.x);
+              min_f = f;
+            }
           }
         }
       }
@@ -478,6 +499,7 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p
       best.n = nn;
       best.part = part;
       best.face = sf;
+      best.sep = sep_f;
     }
   }
   if (plane_tests) *plane_tests = planes;
@@ -533,6 +555,7 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int p0, int p1
   best.n = mk(0, 0, 1);
   best.part = -1;
   best.face = -1;
+  best.sep = -1;
   unsigned planes = 0, tris = 0;
   const float px = (float)p.x, py = (float)p.y, pz = (float)p.z;
   double ub_warm = INFINITY;
@@ -758,10 +781,12 @@ __global__ void __launch_bounds__(GDEV_PQ_BLOCK, GDEV_PQ_THREADS_PER_SM / GDEV_P
   const D3 p = ld3(st.qpts + ((size_t)g * st.NQ + slot) * 3);
   unsigned planes, tris;
   int* qf = st.qface + (size_t)g * st.NQ + slot;
+  int* qs = st.qsep + (size_t)g * st.NQ + slot;
   int p0, p1;
   obj_parts(O, st, g, p0, p1);
-  const PointHit h = point_to_mesh(O, p, p0, p1, *qf, &planes, &tris);
+  const PointHit h = point_to_mesh(O, p, p0, p1, *qf, &planes, &tris, *qs);
   *qf = h.face;
+  *qs = h.sep;
   if (st.ops) {
     atomicAdd(st.ops + kOpPlaneTests, (unsigned long long)planes);
     atomicAdd(st.ops + kOpTriangleTests, (unsigned long long)tris);
@@ -1110,10 +1135,12 @@ __global__ void __launch_bounds__(GDEV_PQ_BLOCK, GDEV_PQ_THREADS_PER_SM / GDEV_P
   const D3 p = ld3(st.qpts + (size_t)t * 3);
   unsigned planes, tris;
   int* qf = st.qface + t;
+  int* qs = st.qsep + t;
   int p0, p1;
   obj_parts(O, st, g, p0, p1);
-  const PointHit h = point_to_mesh(O, p, p0, p1, *qf, &planes, &tris);
+  const PointHit h = point_to_mesh(O, p, p0, p1, *qf, &planes, &tris, *qs);
   *qf = h.face;
+  *qs = h.sep;
   if (st.ops) {
     atomicAdd(st.ops + kOpPlaneTests, (unsigned long long)planes);
     atomicAdd(st.ops + kOpTriangleTests, (unsigned long long)tris);

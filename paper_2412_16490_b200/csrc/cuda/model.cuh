@@ -85,8 +85,11 @@ struct DevObject {
   int NC;                          // face clusters
   const int* face_cluster;         // [F] cluster of each face (point-query bucketing)
   // Plane groups (inside test): each part's non-degenerate face planes grouped
-  // by normal direction, with a lower bound on the group's plane depths.
-  const int* part_gbeg;            // [P+1] plane groups of each part
+  // by normal direction, with a lower bound on the group's plane depths;
+  // groups of neighbouring directions form super-groups with their own bound.
+  const int* part_gbeg;            // [P+1] plane super-groups of each part
+  const int* sup_gbeg;             // [NS+1] first group of each super-group
+  const float4* sup_bound;         // [NS*2] super-group bounds (grp_bound layout)
   const int* grp_beg;              // [NG+1] first entry of each group in grp_plane / grp_face
   const float4* grp_bound;         // [NG*2] (n_g, h_g), (C_g, delta_g): fp32, h_g <= min (w_f - n_f.C_g), delta_g >= max |n_f - n_g|
   const double4* grp_plane;        // planes in group order (copies of face_plane)
@@ -181,6 +184,7 @@ struct DevState {
   double* qpts;     // [G*NQ*3]
   double* qres;     // [G*NQ*8]: d, pb(3), n(3), part
   int* qface;       // [G*NQ] closest face of the slot's last query (warm-start seed), -1 if none
+  int* qsep;        // [G*NQ] face whose plane put the last query outside its winning part, -1 if none
   const int* obj;   // [G] object of each grasp (multi-object contexts), nullptr = object 0
   int* pq_key;      // [G*NQ] bucket of each query slot (its last closest face's cluster, ...)
   int* pq_count;    // [NC + P + 1] queries per bucket, then the fill cursor
