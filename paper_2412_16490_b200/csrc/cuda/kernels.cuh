@@ -181,6 +181,15 @@ __device__ inline void load_fk(const DevHand& H, const DevState& st, int g, int 
   __syncwarp();
 }
 
+// Profiling op counter, aggregated over the warp's active lanes first (one
+// atomic per warp instead of one per thread: per-thread atomics on the same
+// few counters serialised and inflated the profiled kernel times).
+__device__ __forceinline__ void op_add(unsigned long long* ops, int k, unsigned v) {
+  const unsigned mask = __activemask();
+  const unsigned s = __reduce_add_sync(mask, v);
+  if ((int)(threadIdx.x & 31) == __ffs(mask) - 1 && s) atomicAdd(ops + k, (unsigned long long)s);
+}
+
 // --------------------------------------------------------- point queries
 // Ericson closest point on a triangle (geometry.cpp:327-347).
 __device__ __forceinline__ D3 closest_on_triangle(D3 p, D3 a, D3 b, D3 c) {
@@ -747,9 +756,9 @@ __global__ void __launch_bounds__(GDEV_PQG_BLOCK) k_point_query_group(DevObject 
   const PointHit h = point_to_mesh_group<L>(O, p, p0, p1, *qf, gl, gmask, &planes, &tris);
   __syncwarp(gmask);
   if (st.ops) {
-    atomicAdd(st.ops + kOpPlaneTests, (unsigned long long)planes);
-    atomicAdd(st.ops + kOpTriangleTests, (unsigned long long)tris);
-    if (gl == 0) atomicAdd(st.ops + kOpPointQueries, 1ull);
+    op_add(st.ops, kOpPlaneTests, planes);
+    op_add(st.ops, kOpTriangleTests, tris);
+    op_add(st.ops, kOpPointQueries, gl == 0 ? 1u : 0u);
   }
   if (gl != 0) return;
   *qf = h.face;
@@ -788,9 +797,9 @@ __global__ void __launch_bounds__(GDEV_PQ_BLOCK, GDEV_PQ_THREADS_PER_SM / GDEV_P
   *qf = h.face;
   *qs = h.sep;
   if (st.ops) {
-    atomicAdd(st.ops + kOpPlaneTests, (unsigned long long)planes);
-    atomicAdd(st.ops + kOpTriangleTests, (unsigned long long)tris);
-    atomicAdd(st.ops + kOpPointQueries, 1ull);
+    op_add(st.ops, kOpPlaneTests, planes);
+    op_add(st.ops, kOpTriangleTests, tris);
+    op_add(st.ops, kOpPointQueries, 1u);
   }
   double* o = st.qres + ((size_t)g * st.NQ + slot) * 8;
   o[0] = h.d;
@@ -856,13 +865,12 @@ __device__ inline PairResult link_part_distance(const DevHand& H, const DevObjec
 
 // Profiling: GJK closest-point calls of one pair, total and histogram.
 __device__ __forceinline__ void count_gjk(unsigned long long* ops, unsigned calls, unsigned skipped) {
-  atomicAdd(ops + kOpGjkIters, (unsigned long long)calls);
-  if (skipped) {
-    atomicAdd(ops + kOpGjkCycleJumps, 1ull);
-    atomicAdd(ops + kOpGjkItersSkipped, (unsigned long long)skipped);
-  }
+  op_add(ops, kOpGjkIters, calls);
+  op_add(ops, kOpGjkCycleJumps, skipped ? 1u : 0u);
+  op_add(ops, kOpGjkItersSkipped, skipped);
   const int b = calls <= 4 ? 0 : calls <= 8 ? 1 : calls <= 16 ? 2 : calls <= 32 ? 3 : calls <= 64 ? 4 : 5;
-  atomicAdd(ops + kOpGjkHist + b, 1ull);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) op_add(ops, kOpGjkHist + k, b == k ? 1u : 0u);
 }
 
 __device__ __forceinline__ void store_pair(double* o, const PairResult& r) {
@@ -1142,9 +1150,9 @@ __global__ void __launch_bounds__(GDEV_PQ_BLOCK, GDEV_PQ_THREADS_PER_SM / GDEV_P
   *qf = h.face;
   *qs = h.sep;
   if (st.ops) {
-    atomicAdd(st.ops + kOpPlaneTests, (unsigned long long)planes);
-    atomicAdd(st.ops + kOpTriangleTests, (unsigned long long)tris);
-    atomicAdd(st.ops + kOpPointQueries, 1ull);
+    op_add(st.ops, kOpPlaneTests, planes);
+    op_add(st.ops, kOpTriangleTests, tris);
+    op_add(st.ops, kOpPointQueries, 1u);
   }
   double* o = st.qres + (size_t)t * 8;
   o[0] = h.d;
@@ -1225,9 +1233,9 @@ __global__ void __launch_bounds__(GDEV_PAIRS_BLOCK, GDEV_PAIRS_MIN_BLOCKS) k_pai
   const bool overlap = gjk_phase(A, B, scale, r, simp, ns);
   st.pair_hist[slot] = (unsigned char)min(255u, r.gjk_iters + 1);
   if (st.ops) {
-    atomicAdd(st.ops + kOpSupportVerts, (unsigned long long)r.n_support * (A.nv + B.nv));
+    op_add(st.ops, kOpSupportVerts, r.n_support * (A.nv + B.nv));
     count_gjk(st.ops, r.gjk_iters + 1, r.gjk_skipped);
-    atomicAdd(st.ops + kOpPairsNeeded, 1ull);
+    op_add(st.ops, kOpPairsNeeded, 1u);
   }
   if (!overlap) {
     store_pair(st.pairs + (size_t)slot * 12, r);

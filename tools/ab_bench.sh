@@ -7,5 +7,7 @@ for lib in default "$@"; do
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-other-configs > gpurun_out/ab_$lib.json 2>&1
   python -c "
 import json,sys; d=json.loads(open('gpurun_out/ab_$lib.json').read().strip().splitlines()[-1])
-print('$lib', d['value'], {k: round(v,1) for k,v in d['roofline']['kernel_ms'].items()})" >> gpurun_out/ab.log
+o = d['roofline'].get('ops', {}); q = max(1, o.get('point_queries', 1))
+print('$lib', d['value'], {k: round(v,1) for k,v in d['roofline']['kernel_ms'].items()},
+      {k: round(o.get(k, 0) / q, 2) for k in ('plane_tests', 'triangle_tests', 'grid_part_queries', 'scan_part_queries')})" >> gpurun_out/ab.log
 done
