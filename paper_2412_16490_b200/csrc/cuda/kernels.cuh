@@ -557,7 +557,7 @@ __device__ __forceinline__ float group_fmin(unsigned gmask, float v) {
 
 template <int L>
 __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int p0, int p1, int warm_face, int gl, unsigned gmask,
-                                        unsigned* plane_tests, unsigned* tri_tests) {
+                                        unsigned* plane_tests, unsigned* tri_tests, int warm_sep = -1) {
   PointHit best;
   best.d = INFINITY;
   best.pb = mk(0, 0, 0);
@@ -585,8 +585,8 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int p0, int p1
     }
     const int c0 = __ldg(O.part_cbeg + part), c1 = __ldg(O.part_cbeg + part + 1);
     float ubA = INFINITY;
-    int seed_f;
-    {
+    int seed_f = warm_face;
+    if (!(warm_face >= f0 && warm_face < f1)) {  // (the warm face seeds its own part)
       float lb_seed = INFINITY;
       int seed_c = c0;
       for (int c = c0 + gl; c < c1; c += L) {
@@ -615,34 +615,74 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int p0, int p1
       }
       group_lexmin<L>(gmask, lbf, seed_f);
     }
+    // Inside test as in point_to_mesh: the seed, last separating and warm
+    // planes first, then the normal groups whose depth bound does not exceed
+    // a known depth, each group's planes split over the lanes.
     bool inside;
     double min_depth = INFINITY;
-    int min_face = INT_MAX;
+    int min_face = INT_MAX, sep_f = -1;
+    double ub_depth;
     {
       const double4 Q = ld_plane(O, seed_f);
       if (gl == 0) ++planes;
-      inside = !((Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z)) < -1e-12);
+      ub_depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
+      inside = !(ub_depth < -1e-12);
+      sep_f = inside ? -1 : seed_f;
+    }
+    if (inside && warm_sep >= f0 && warm_sep < f1 && warm_sep != seed_f) {
+      const double4 Q = ld_plane(O, warm_sep);
+      if (gl == 0) ++planes;
+      const double depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
+      inside = !(depth < -1e-12);
+      sep_f = inside ? -1 : warm_sep;
+      ub_depth = fmin(ub_depth, depth);
+    }
+    if (inside && warm_face >= f0 && warm_face < f1 && warm_face != seed_f) {
+      const double4 Q = ld_plane(O, warm_face);
+      if (gl == 0) ++planes;
+      const double depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
+      inside = !(depth < -1e-12);
+      sep_f = inside ? -1 : warm_face;
+      ub_depth = fmin(ub_depth, depth);
     }
     if (inside) {
-      // chunks of L planes; the group stops after the first chunk with a
-      // separating plane (whether one exists does not depend on the order)
-      for (int fb = f0; fb < f1; fb += L) {
-        const int f = fb + gl;
-        bool sep = false;
-        if (f < f1) {
-          const double4 Q = ld_plane(O, f);
-          ++planes;
-          const double depth = Q.w - (Q.x * p.x + Q.y * p.y + Q.z * p.z);
-          if (depth < -1e-12) {
-            sep = true;
-          } else if (depth < min_depth) {
-            min_depth = depth;
-            min_face = f;
+      // every lane of the group evaluates the same bounds (same p, same
+      // ub_depth), so the group stays converged through the group loops
+      const float thr = (float)ub_depth + kCullSlack32;
+      auto group_far = [&](const float4* B) {
+        const float4 B0 = __ldg(B), B1 = __ldg(B + 1);
+        const float rx = B1.x - px, ry = B1.y - py, rz = B1.z - pz;
+        const float lb = (B0.w + (B0.x * rx + B0.y * ry + B0.z * rz)) - B1.w * (fabsf(rx) + fabsf(ry) + fabsf(rz));
+        return lb > thr;
+      };
+      const int s1 = __ldg(O.part_gbeg + part + 1);
+      for (int sg = __ldg(O.part_gbeg + part); sg < s1 && inside; ++sg) {
+        if (group_far(O.sup_bound + 2 * sg)) continue;
+        const int q1 = __ldg(O.sup_gbeg + sg + 1);
+        for (int q = __ldg(O.sup_gbeg + sg); q < q1 && inside; ++q) {
+          if (group_far(O.grp_bound + 2 * q)) continue;
+          const int k1 = __ldg(O.grp_beg + q + 1);
+          int my_sep = -1;
+          for (int k = __ldg(O.grp_beg + q) + gl; k < k1; k += L) {
+            const double2* qq = reinterpret_cast<const double2*>(O.grp_plane + k);
+            const double2 qa = __ldg(qq), qb = __ldg(qq + 1);
+            ++planes;
+            const double depth = qb.y - (qa.x * p.x + qa.y * p.y + qb.x * p.z);
+            const int f = __ldg(O.grp_face + k);
+            if (depth < -1e-12) {
+              my_sep = f;
+              break;
+            }
+            if (depth < min_depth || (depth == min_depth && f < min_face)) {
+              min_depth = depth;
+              min_face = f;
+            }
           }
-        }
-        if (__any_sync(gmask, sep)) {
-          inside = false;
-          break;
+          const unsigned sep = __ballot_sync(gmask, my_sep >= 0);
+          if (sep) {
+            inside = false;
+            sep_f = __shfl_sync(gmask, my_sep, __ffs(sep) - 1);
+          }
         }
       }
       if (inside) group_lexmin<L>(gmask, min_depth, min_face);
@@ -660,9 +700,12 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int p0, int p1
     } else {
       float bound;
       {
-        if (gl == 0) ++tris;
-        const double* F = O.faces + (size_t)seed_f * kFaceStride;
-        const double d_seed = nrm(p - closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6)));
+        double d_seed = ub_warm;
+        if (seed_f != warm_face) {
+          if (gl == 0) ++tris;
+          const double* F = O.faces + (size_t)seed_f * kFaceStride;
+          d_seed = nrm(p - closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6)));
+        }
         bound = fminf(fminf(ubA, __double2float_ru(d_seed)), __double2float_ru(ub_warm)) + kCullSlack32;
       }
       sd = INFINITY;
@@ -725,6 +768,7 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int p0, int p1
       best.n = nn;
       best.part = part;
       best.face = sf;
+      best.sep = sep_f;
     }
   }
   if (plane_tests) *plane_tests = planes;
@@ -751,9 +795,10 @@ __global__ void __launch_bounds__(GDEV_PQG_BLOCK) k_point_query_group(DevObject 
   const D3 p = ld3(st.qpts + ((size_t)g * st.NQ + slot) * 3);
   unsigned planes, tris;
   int* qf = st.qface + (size_t)g * st.NQ + slot;
+  int* qs = st.qsep + (size_t)g * st.NQ + slot;
   int p0, p1;
   obj_parts(O, st, g, p0, p1);
-  const PointHit h = point_to_mesh_group<L>(O, p, p0, p1, *qf, gl, gmask, &planes, &tris);
+  const PointHit h = point_to_mesh_group<L>(O, p, p0, p1, *qf, gl, gmask, &planes, &tris, *qs);
   __syncwarp(gmask);
   if (st.ops) {
     op_add(st.ops, kOpPlaneTests, planes);
@@ -762,6 +807,7 @@ __global__ void __launch_bounds__(GDEV_PQG_BLOCK) k_point_query_group(DevObject 
   }
   if (gl != 0) return;
   *qf = h.face;
+  *qs = h.sep;
   double* o = st.qres + ((size_t)g * st.NQ + slot) * 8;
   o[0] = h.d;
   st3(o + 1, h.pb);

@@ -18,6 +18,7 @@ ap.add_argument("--batch", type=int, default=512)
 ap.add_argument("--coarse", type=int, default=300)
 ap.add_argument("--fine", type=int, default=100)
 ap.add_argument("--final", type=int, default=100)
+ap.add_argument("--option", action="append", default=[], help="engine option name=value (repeatable)")
 args = ap.parse_args()
 
 hand = G.HandModel.builtin() if args.hand == "trident" else G.HandModel.from_file(
@@ -32,6 +33,9 @@ x0 = G.init_poses(hand, obj, args.batch, 17)
 eng = G.Engine(0)
 eng.set_hand(hand)
 eng.set_object(obj)
+for o in args.option:
+    k, v = o.split("=")
+    eng.set_option(k, int(v))
 eng.synthesize(cfg, x0[:64])
 t = time.perf_counter()
 out = eng.synthesize(cfg, x0)
