@@ -296,6 +296,10 @@ __global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_RESIDENT_WARPS / G
   // fp64 operations. The first sweep starts from the warm (z, u), which need
   // not be complementary, and is peeled (kFirst).
   double vz[KMAX];
+  // countdown to the next check sweep (iter % check_interval == 0) without
+  // an integer division per sweep
+  const int interval = P.check_interval > 0 ? P.check_interval : 1;
+  int to_check = interval;
   auto sweep = [&]<bool kFirst>(int iter) -> bool {
     // rhs = A'(rho z - y) + sigma x - q = rq + vct (vct: the cap and total
     // rows, common to the lane's edges) ; r' = B^-1 rhs
@@ -304,7 +308,8 @@ __global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_RESIDENT_WARPS / G
 #pragma unroll
     for (int e = 0; e < KMAX; ++e)
       rq[e] = e < k ? rho * (kFirst ? zid[e] - uid[e] : fabs(vz[e])) + (sigma * x[e] + nq[e]) : 0.0;
-    const double bsum = tree_sum<KMAX>(rq) + k * vct;
+    const double rsum = tree_sum<KMAX>(rq);
+    const double bsum = rsum + k * vct;
     const double bb = betap * bsum;
     double tv[7];
     {
@@ -372,7 +377,8 @@ __global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_RESIDENT_WARPS / G
 #pragma unroll
     for (int e = 0; e < KMAX; ++e)
       axt[e] = e < k ? ((a_inv_a * rq[e] + hh) - agb * P.cos_t[e]) - agc * P.sin_t[e] : 0.0;
-    const double aztc = tree_sum<KMAX>(axt);
+    // sum of the lane's axt_e from the sums already formed (no second tree)
+    const double aztc = a_inv_a * rsum + (k * hh - (agb * ccos + agc * csin));
     const double aztt = qp_group_sum<MT>(aztc, base, m);
     // Relaxed updates and projection (z = Pi(zbar + u), u += zbar - z).
 #pragma unroll
@@ -401,7 +407,9 @@ __global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_RESIDENT_WARPS / G
       utot = v - zn;
       ztot = zn;
     }
-    if (iter % P.check_interval == 0 || iter == P.max_iters) {
+    const bool check_now = --to_check == 0;
+    if (check_now) to_check = interval;
+    if (check_now || iter == P.max_iters) {
       double axc = 0.0;
 #pragma unroll
       for (int e = 0; e < KMAX; ++e)
