@@ -841,50 +841,44 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
   out.n_support = 1;
   out.gjk_iters = 0;
   out.epa_iters = 0;
-  // The simplex is only ever indexed by compile-time constants (unrolled
-  // loops with predicates) so it stays in registers.
   out.gjk_skipped = 0;
-  ns = 1;
-  simp[0] = support_pair(A, B, mk(1, 0, 0));
-  simp[1] = simp[2] = simp[3] = simp[0];
+  // The simplex is only ever indexed by compile-time constants (unrolled
+  // loops with predicates) so it stays in registers. One support_pair and
+  // one closest_on_simplex call site (instruction-cache footprint): the
+  // loop enters at the seed support (direction +x, geometry.cpp:107-108),
+  // and the iteration cap (geometry.cpp:151-163: the estimate on the
+  // unreduced simplex, i.e. its support subset, no contact test) leaves
+  // through the common separated exit.
+  ns = 0;
   GjkCycle cyc;
   cycle_init(cyc, A.nv, B.nv);
   bool overlap = false;
   Simplex sx;
-  // One closest_on_simplex call site (code size): call kGjkMaxIters is the
-  // iteration-cap estimate on the unreduced simplex (geometry.cpp:136-149).
-  for (int iter = 0;; ++iter) {
+  D3 dir = mk(1, 0, 0);
+  for (int iter = -1;;) {
+    const SP w = support_pair(A, B, dir);
+    if (iter < 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) simp[i] = w;
+    } else {
+      ++out.n_support;
+      ++out.gjk_iters;
+      const double gap = sx.dist2 - dot(sx.v, w.w);
+      bool repeat = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < ns && nrm(simp[i].w - w.w) < 1e-14 * scale) repeat = true;
+      if (gap <= kGjkRelTol * sx.dist2 + 1e-300 || repeat || ns == 4) break;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i == ns) simp[i] = w;
+    }
+    ++ns;
+    ++iter;
     const int jump = cycle_step(cyc, simp, ns, iter);
     iter += jump;
     out.gjk_skipped += jump;
     sx = closest_on_simplex(simp, ns);
-#ifdef GJK_TRACE
-    printf("iter %d ns %d -> nkeep %d contains %d dist2 %.17g keep %d %d %d %d wts %.3g %.3g %.3g %.3g\n", iter, ns,
-           sx.nkeep, (int)sx.contains, sx.dist2, sx.keep[0], sx.keep[1], sx.keep[2], sx.keep[3], sx.wts[0], sx.wts[1],
-           sx.wts[2], sx.wts[3]);
-    for (int i = 0; i < ns; ++i) printf("   w%d %.17g %.17g %.17g\n", i, simp[i].w.x, simp[i].w.y, simp[i].w.z);
-#endif
-    if (iter == kGjkMaxIters) {
-      D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (i < sx.nkeep) {
-          const int src = sx.keep[i];
-          SP p = simp[0];
-          if (src == 1) p = simp[1];
-          if (src == 2) p = simp[2];
-          if (src == 3) p = simp[3];
-          wa += sx.wts[i] * sp_a(A, p);
-          wb += sx.wts[i] * sp_b(B, p);
-        }
-      }
-      const double d = sqrt(sx.dist2);
-      out.d = d;
-      out.pa = wa;
-      out.pb = wb;
-      out.n = d > 1e-14 ? (wa - wb) / d : mk(0, 0, 1);
-      return false;
-    }
     SP red[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -897,23 +891,12 @@ GDEV_FN bool gjk_phase(const Hull& A, const Hull& B, double scale, PairResult& o
     ns = sx.nkeep;
 #pragma unroll
     for (int i = 0; i < 4; ++i) simp[i] = red[i];
+    if (iter == kGjkMaxIters) break;
     if (sx.contains || sqrt(sx.dist2) < kTouchTol * scale) {
       overlap = true;
       break;
     }
-    const SP w = support_pair(A, B, -sx.v);
-    ++out.n_support;
-    ++out.gjk_iters;
-    const double gap = sx.dist2 - dot(sx.v, w.w);
-    bool repeat = false;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i < ns && nrm(simp[i].w - w.w) < 1e-14 * scale) repeat = true;
-    if (gap <= kGjkRelTol * sx.dist2 + 1e-300 || repeat || ns == 4) break;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i == ns) simp[i] = w;
-    ++ns;
+    dir = -sx.v;
   }
   if (!overlap) {
     D3 wa = mk(0, 0, 0), wb = mk(0, 0, 0);
