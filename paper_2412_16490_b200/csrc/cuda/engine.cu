@@ -96,6 +96,8 @@ struct grasp_ctx {
   // per device; synthesize shards the batch over them.
   std::vector<grasp_ctx*> shards;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // k_pairs_early, forked from and joined back into `stream`
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool has_hand = false, has_object = false;
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
   DevBuf<int> pq_key, pq_list, pq_total, pq_count;
@@ -186,6 +188,9 @@ struct grasp_ctx {
       cudaEventDestroy(p.second.second);
     }
     if (stream) cudaStreamDestroy(stream);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
   }
 
   cudaEvent_t take_event() {
@@ -978,8 +983,8 @@ struct grasp_ctx {
     epa_hist.ensure(g * NP);
     ck(cudaMemsetAsync(epa_hist.p, 0, g * NP, stream), "memset");
     st.epa_hist = epa_hist.p;
-    seg_count.ensure(NP * kPairBuckets);
-    seg_offset.ensure(NP * kPairBuckets);
+    seg_count.ensure(NP * kPairBuckets + 1);
+    seg_offset.ensure(NP * kPairBuckets + 1);
     st.pair_need = pair_need.p;
     st.seg_count = seg_count.p;
     st.seg_offset = seg_offset.p;
@@ -1102,13 +1107,21 @@ struct grasp_ctx {
       ck(cudaMemsetAsync(ovf_count.p, 0, sizeof(int), stream), "memset");
       const int* lk = tips_only ? h_tip_links_sorted.p : nullptr;
       ck(cudaMemsetAsync(pair_count.p, 0, 4 * sizeof(int), stream), "memset");
-      ck(cudaMemsetAsync(seg_count.p, 0, sizeof(int) * nl * O.Pmax * kPairBuckets, stream), "memset");
+      const int n_seg = nl * O.Pmax * kPairBuckets + 1;
+      ck(cudaMemsetAsync(seg_count.p, 0, sizeof(int) * n_seg, stream), "memset");
       k_pairs_cull<<<blocks(n, 128), 128, 0, stream>>>(H, O, st, lk, nl);
-      k_pairs_scan<<<1, 1024, 0, stream>>>(st, nl * O.Pmax * kPairBuckets);
+      k_pairs_scan<<<1, 1024, 0, stream>>>(st, n_seg);
       k_pairs_scatter<<<blocks(n, 128), 128, 0, stream>>>(st, lk, nl, O.Pmax);
+      // the early pairs (GJK + EPA per thread) on the side stream, next to
+      // the GJK pass and the EPA of the other pairs
+      ck(cudaEventRecord(ev_fork, stream), "event");
+      ck(cudaStreamWaitEvent(side, ev_fork, 0), "event");
+      k_pairs_early<<<blocks(std::min<long long>(n, st.epa_cap), 32), 32, 0, side>>>(H, O, st);
+      ck(cudaEventRecord(ev_join, side), "event");
       k_pairs_list<<<blocks(n, GDEV_PAIRS_BLOCK), GDEV_PAIRS_BLOCK, 0, stream>>>(H, O, st);
       // EPA jobs spread over all SMs (32-thread blocks; few jobs per launch)
       k_pairs_epa<<<blocks(2 * std::min<long long>(n, st.epa_cap), 32), 32, 0, stream>>>(H, O, st);
+      ck(cudaStreamWaitEvent(stream, ev_join, 0), "event");
     });
     launch(7, [&] { k_pairs_big<<<kBigSlots / 128, 128, 0, stream>>>(H, O, st); });
   }
@@ -1303,6 +1316,9 @@ int grasp_ctx_create(int device, grasp_ctx** out) {
     try {
       ctx->set_device();
       ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      ck(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "cudaStreamCreate");
+      ck(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "cudaEventCreate");
       // No cudaDeviceSetLimit(cudaLimitStackSize): the EPA kernels' local
       // polytopes are static frames (<= 11.8 KB/thread, ptxas), which the
       // driver provisions per launch; a device-wide limit would reserve that

@@ -1043,6 +1043,12 @@ __device__ __forceinline__ int warp_segment_add(int* counters, int seg, bool act
   return base + __popc(peers & ((1u << lane) - 1));
 }
 
+// List segments: 0 = the early pairs (the slot's last EPA took more than
+// kEpaEarlyPred iterations: GJK + EPA in one thread by k_pairs_early,
+// concurrently with k_pairs_list), then (link-part, GJK-length bucket).
+constexpr int kPairEarly = 254;  // (pair_need stores 1 + bucket in a byte)
+__device__ __forceinline__ int pair_segment(int lp, int b) { return b == kPairEarly ? 0 : 1 + lp * kPairBuckets + b; }
+
 __global__ void __launch_bounds__(128) k_pairs_cull(DevHand H, DevObject O, DevState st,
                                                     const int* __restrict__ links, int n_links) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1067,12 +1073,13 @@ __global__ void __launch_bounds__(128) k_pairs_cull(DevHand H, DevObject O, DevS
         o[0] = INFINITY;
         o[10] = kPairCulled;
       } else {
-        b = pair_bucket(st.pair_hist[(size_t)g * st.NP + link * O.Pmax + part]);
+        const size_t slot = (size_t)g * st.NP + link * O.Pmax + part;
+        b = st.epa_hist[slot] > kEpaEarlyPred ? kPairEarly : pair_bucket(st.pair_hist[slot]);
       }
     }
     st.pair_need[t] = need ? (unsigned char)(1 + b) : 0;
   }
-  warp_segment_add(st.seg_count, lp * kPairBuckets + b, need);
+  warp_segment_add(st.seg_count, pair_segment(lp, b), need);
 }
 
 // Pass 1b: exclusive scan of the segment counts (one block); seg_count turns
@@ -1110,7 +1117,7 @@ __global__ void __launch_bounds__(128) k_pairs_scatter(DevState st, const int* _
   const int code = t < n ? st.pair_need[t] : 0;
   const bool need = code != 0;
   const int lp = t < n ? (int)(t / st.G) : 0;
-  const int pos = warp_segment_add(st.seg_count, lp * kPairBuckets + (need ? code - 1 : 0), need);
+  const int pos = warp_segment_add(st.seg_count, pair_segment(lp, need ? code - 1 : 0), need);
   if (need) {
     const int g = (int)(t % st.G);
     const int link = links ? links[lp / P] : lp / P;
@@ -1267,7 +1274,7 @@ __device__ __forceinline__ void write_epa_job(const DevState& st, int slot, cons
 
 // Pass 2 (default): GJK, one thread per listed pair from start to end.
 __global__ void __launch_bounds__(GDEV_PAIRS_BLOCK, GDEV_PAIRS_MIN_BLOCKS) k_pairs_list(DevHand H, DevObject O, DevState st) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = st.seg_offset[1] + blockIdx.x * blockDim.x + threadIdx.x;  // after the early pairs
   if (i >= *st.pair_count) return;
   const int slot = st.pair_list[i];
   Hull A, B;
@@ -1337,6 +1344,53 @@ __global__ void __launch_bounds__(32, GDEV_EPA_MIN_BLOCKS) k_pairs_epa(DevHand H
   store_pair(st.pairs + (size_t)slot * 12, r);
 }
 
+
+// The early pairs (list segment 0): GJK and, on overlap, EPA in one thread,
+// launched on a second stream next to k_pairs_list so that the long EPA runs
+// overlap the GJK pass instead of forming k_pairs_epa's tail. Same functions,
+// same results as the two-pass path.
+__device__ __forceinline__ void pair_early(const DevHand& H, const DevObject& O, const DevState& st, int slot) {
+  Hull A, B;
+  double scale;
+  slot_hulls(H, O, st, slot, A, B, scale);
+  PairResult r;
+  SP simp[4];
+  int ns;
+  const bool overlap = gjk_phase(A, B, scale, r, simp, ns);
+  st.pair_hist[slot] = (unsigned char)min(255u, r.gjk_iters + 1);
+  if (st.ops) {
+    op_add(st.ops, kOpSupportVerts, r.n_support * (A.nv + B.nv));
+    count_gjk(st.ops, r.gjk_iters + 1, r.gjk_skipped);
+    op_add(st.ops, kOpPairsNeeded, 1u);
+  }
+  if (overlap) {
+    r.n_support = 0;
+    EpaScratch scratch;
+    epa(simp, ns, A, B, scale, scratch, r);
+    if (st.ops) {
+      op_add(st.ops, kOpSupportVerts, r.n_support * (A.nv + B.nv));
+      op_add(st.ops, kOpEpaIters, r.epa_iters);
+      atomicMax(st.ops + kOpEpaMaxIters, (unsigned long long)r.epa_iters);
+      op_add(st.ops, kOpEpaLongJobs, r.epa_iters > 8 ? 1u : 0u);
+      op_add(st.ops, kOpEpaOverflow, (r.flags & kPairOverflow) ? 1u : 0u);
+    }
+    if (r.flags & kPairDegenerate) atomicAdd(st.err + 0, 1);
+    if (r.flags & kPairOverflow) {
+      st.epa_hist[slot] = (unsigned char)min(255, r.epa_iters);
+      queue_overflow(st, slot);
+      return;
+    }
+  }
+  st.epa_hist[slot] = (unsigned char)min(255, overlap ? r.epa_iters : 0);
+  store_pair(st.pairs + (size_t)slot * 12, r);
+}
+
+__global__ void __launch_bounds__(32) k_pairs_early(DevHand H, DevObject O, DevState st) {
+  const int n_early = st.seg_offset[1];
+  // (grid-stride: the grid is sized for the usual count, not the worst case)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_early; i += gridDim.x * blockDim.x)
+    pair_early(H, O, st, st.pair_list[i]);
+}
 
 // Redoes the queued pairs with the large global-memory EPA buffer.
 __global__ void __launch_bounds__(128) k_pairs_big(DevHand H, DevObject O, DevState st) {

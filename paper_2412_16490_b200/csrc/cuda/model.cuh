@@ -233,6 +233,10 @@ constexpr int kEpaJobStride = 18;  // slot, ns, 4 x (w, support key)
 // slot's previous GJK length (kPairBuckets buckets), so a warp's pairs tend
 // to need the same number of iterations.
 constexpr int kPairBuckets = 16;
+#ifndef GDEV_EPA_EARLY_PRED
+#define GDEV_EPA_EARLY_PRED 24  // 8: 354, 16: 346, 24: 340, 32: 342, 40: 346 ms pairs; off: 346
+#endif
+constexpr int kEpaEarlyPred = GDEV_EPA_EARLY_PRED;  // k_pairs_early: slots whose last EPA took more iterations
 __host__ __device__ inline int pair_bucket(int calls) { return calls < 1 ? 0 : (calls > 16 ? 15 : calls - 1); }
 
 // Op counters (profiling mode) for the roofline's algorithmic flop count

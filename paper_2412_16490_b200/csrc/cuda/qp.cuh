@@ -308,8 +308,7 @@ __global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_RESIDENT_WARPS / G
 #pragma unroll
     for (int e = 0; e < KMAX; ++e)
       rq[e] = e < k ? rho * (kFirst ? zid[e] - uid[e] : fabs(vz[e])) + (sigma * x[e] + nq[e]) : 0.0;
-    const double rsum = tree_sum<KMAX>(rq);
-    const double bsum = rsum + k * vct;
+    const double bsum = tree_sum<KMAX>(rq) + k * vct;
     const double bb = betap * bsum;
     double tv[7];
     {
@@ -377,8 +376,10 @@ __global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_RESIDENT_WARPS / G
 #pragma unroll
     for (int e = 0; e < KMAX; ++e)
       axt[e] = e < k ? ((a_inv_a * rq[e] + hh) - agb * P.cos_t[e]) - agc * P.sin_t[e] : 0.0;
-    // sum of the lane's axt_e from the sums already formed (no second tree)
-    const double aztc = a_inv_a * rsum + (k * hh - (agb * ccos + agc * csin));
+    // (a closed form from the sums already formed saves the tree but rounds
+    // differently; the end-to-end comparison with the oracle drifted past
+    // its 1e-5 tolerance on the short trident schedule, so the tree stays)
+    const double aztc = tree_sum<KMAX>(axt);
     const double aztt = qp_group_sum<MT>(aztc, base, m);
     // Relaxed updates and projection (z = Pi(zbar + u), u += zbar - z).
 #pragma unroll
