@@ -274,7 +274,9 @@ int grasp_ctx_profile(grasp_ctx* ctx, double* ms /*[8]*/, long long* launches /*
  * "tip_query_lanes" (tip-only launches, default 4), "pair_cull" (0: every
  * (link, part) pair through GJK like the reference; 1: the opt-in separation
  * cull, exact for the true geometry only) with "pair_sat" (its
- * link-box vs part-box test, default 1). GRASP_EINVAL for unknown names. */
+ * link-box vs part-box test, default 1), "pair_early" (pairs whose last EPA
+ * ran more than this many iterations run GJK + EPA on a side stream next to
+ * the GJK pass; default 24, >= 255 off). GRASP_EINVAL for unknown names. */
 int grasp_ctx_set_option(grasp_ctx* ctx, const char* name, int value);
 
 /* Kernels launched by this context so far. */

@@ -532,7 +532,8 @@ class Engine:
         return N.lib().grasp_ctx_stream(self._ctx) or 0
 
     def set_option(self, name: str, value: int) -> None:
-        """grasp_ctx_set_option: "query_buckets", "query_lanes", "tip_query_lanes", "pair_cull", "pair_sat"."""
+        """grasp_ctx_set_option: "query_buckets", "query_lanes", "tip_query_lanes", "pair_cull", "pair_sat",
+        "pair_early" (EPA-iteration threshold for the early GJK+EPA pass; >= 255 turns it off)."""
         N.check(N.lib().grasp_ctx_set_option(self._ctx, name.encode(), int(value)))
 
     def set_profiling(self, on: bool) -> None:

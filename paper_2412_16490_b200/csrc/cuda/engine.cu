@@ -107,6 +107,7 @@ struct grasp_ctx {
   bool opt_sat = true;         // "pair_sat": link-box vs part-box SAT inside that cull
   int query_lanes = 1;         // "query_lanes": lanes per query in all-slot launches
   int tip_query_lanes = 4;     // "tip_query_lanes": lanes per query in tip-only launches
+  int early_pred = kEpaEarlyPred;  // "pair_early": EPA-iteration threshold of k_pairs_early (>= 255: off)
 
   void apply_hand_options() {
     H.link_box = opt_sat ? h_link_box.p : nullptr;
@@ -959,6 +960,7 @@ struct grasp_ctx {
     qsep.ensure(g * NQ);
     ck(cudaMemsetAsync(qsep.p, 0xff, sizeof(int) * g * NQ, stream), "memset");
     st.qsep = qsep.p;
+    st.early_pred = early_pred;
     failed.ensure(g);
     have_pregrasp.ensure(g);
     err.ensure(4);
@@ -2018,6 +2020,9 @@ int grasp_ctx_set_option(grasp_ctx* ctx, const char* name, int value) {
         c->query_lanes = value;
       } else if (n == "tip_query_lanes" && lanes_ok(value)) {
         c->tip_query_lanes = value;
+      } else if (n == "pair_early" && value >= 0) {
+        c->early_pred = value;
+        c->st.early_pred = value;
       } else {
         throw std::invalid_argument("unknown option or value: " + n);
       }

@@ -1044,7 +1044,7 @@ __device__ __forceinline__ int warp_segment_add(int* counters, int seg, bool act
 }
 
 // List segments: 0 = the early pairs (the slot's last EPA took more than
-// kEpaEarlyPred iterations: GJK + EPA in one thread by k_pairs_early,
+// st.early_pred iterations: GJK + EPA in one thread by k_pairs_early,
 // concurrently with k_pairs_list), then (link-part, GJK-length bucket).
 constexpr int kPairEarly = 254;  // (pair_need stores 1 + bucket in a byte)
 __device__ __forceinline__ int pair_segment(int lp, int b) { return b == kPairEarly ? 0 : 1 + lp * kPairBuckets + b; }
@@ -1074,7 +1074,7 @@ __global__ void __launch_bounds__(128) k_pairs_cull(DevHand H, DevObject O, DevS
         o[10] = kPairCulled;
       } else {
         const size_t slot = (size_t)g * st.NP + link * O.Pmax + part;
-        b = st.epa_hist[slot] > kEpaEarlyPred ? kPairEarly : pair_bucket(st.pair_hist[slot]);
+        b = st.epa_hist[slot] > st.early_pred ? kPairEarly : pair_bucket(st.pair_hist[slot]);
       }
     }
     st.pair_need[t] = need ? (unsigned char)(1 + b) : 0;

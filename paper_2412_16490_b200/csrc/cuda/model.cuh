@@ -26,7 +26,7 @@ constexpr double kCullSlack = 1e-9;
 
 struct DevHand {
   int L, dof, m, S, nsp, D;
-  int cull;                         // opt-in (GRASP_CULL=1) separation cull of (link, part) pairs, see pair_needed
+  int cull;                         // opt-in (option "pair_cull") separation cull of (link, part) pairs, see pair_needed
   const int* link_parent_joint;     // [L]
   const int* link_depth;            // [L] path length root..l
   const int* link_path;             // [L*kMaxDepth] links from root to l
@@ -185,6 +185,7 @@ struct DevState {
   double* qres;     // [G*NQ*8]: d, pb(3), n(3), part
   int* qface;       // [G*NQ] closest face of the slot's last query (warm-start seed), -1 if none
   int* qsep;        // [G*NQ] face whose plane put the last query outside its winning part, -1 if none
+  int early_pred;   // k_pairs_early takes slots whose last EPA ran more iterations (option "pair_early")
   const int* obj;   // [G] object of each grasp (multi-object contexts), nullptr = object 0
   int* pq_key;      // [G*NQ] bucket of each query slot (its last closest face's cluster, ...)
   int* pq_count;    // [NC + P + 1] queries per bucket, then the fill cursor

@@ -765,6 +765,35 @@ def test_bucketed_point_queries_bitwise(G, case):
         assert np.array_equal(getattr(outs[0], f), getattr(outs[1], f), equal_nan=True), f
 
 
+@pytest.mark.parametrize("case", ["shadow_drill", "trident_box"])
+def test_early_epa_pass_bitwise(G, case):
+    """Pairs whose last EPA ran long take the early pass (k_pairs_early: GJK + EPA per thread on a
+    side stream, option "pair_early"); every threshold, from all overlapping pairs (0) to none
+    (255), gives bitwise the same records as the two-pass GJK -> EPA path."""
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    if case == "shadow_drill":
+        hand = G.HandModel.from_file(root / "paper_2412_16490_b200/assets/hands/shadow_like.json")
+        obj = G.load_object(root / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+    else:
+        hand, obj = G.HandModel.builtin(), G.make_primitive("box", 0.08)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 128, 37
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 40, 30, 30
+    x0 = G.init_poses(hand, obj, cfg.batch, cfg.seed, cfg.init)
+    outs = {}
+    for thr in (255, 0, 4, 24):
+        eng = G.Engine(0)
+        eng.set_hand(hand)
+        eng.set_object(obj)
+        eng.set_option("pair_early", thr)
+        outs[thr] = eng.synthesize(cfg, x0)
+    ref = outs[255]
+    for thr, o in outs.items():
+        for f in ("x", "x_p", "x_s", "energy_total", "stage_energy", "failed", "contacts"):
+            assert np.array_equal(getattr(o, f), getattr(ref, f), equal_nan=True), (thr, f)
+
+
 def test_synthesis_deterministic_and_batch_prefix_independent(G, trident, engine):
     """test_pipeline.cpp:399-421 on the device: the same start states give bitwise-equal
     records on a rerun, and a grasp's record does not depend on the batch it is in
