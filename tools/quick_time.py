@@ -19,6 +19,7 @@ ap.add_argument("--coarse", type=int, default=300)
 ap.add_argument("--fine", type=int, default=100)
 ap.add_argument("--final", type=int, default=100)
 ap.add_argument("--option", action="append", default=[], help="engine option name=value (repeatable)")
+ap.add_argument("--shards", type=int, default=1, help="contexts on device 0 splitting the batch")
 args = ap.parse_args()
 
 hand = G.HandModel.builtin() if args.hand == "trident" else G.HandModel.from_file(
@@ -30,7 +31,7 @@ cfg.seed = 17
 cfg.batch = args.batch
 cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = args.coarse, args.fine, args.final
 x0 = G.init_poses(hand, obj, args.batch, 17)
-eng = G.Engine(0)
+eng = G.Engine(0, devices=[0] * args.shards if args.shards > 1 else None)
 eng.set_hand(hand)
 eng.set_object(obj)
 for o in args.option:
