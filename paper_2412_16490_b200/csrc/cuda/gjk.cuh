@@ -217,14 +217,23 @@ GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (
             m[r][S - 1] = t;
           }
         }
-        const double piv = m[k][k];
+        // The pivot is exactly 1 (the KKT ones; see above), and x / 1 = x
+        // exactly, so the column scaling is the identity and is skipped. At
+        // k = 0 the pivot row is the ones row (1, ..., 1, 0): m[r][0] * 1 is
+        // exact, and the last column (all 1) minus m[r][0] * 0 stays 1, so
+        // only the subtractions remain.
+        if (k == 0) {
 #pragma unroll
-        for (int r = k + 1; r < S; ++r) m[r][k] /= piv;
+          for (int c = 1; c < S - 1; ++c)
 #pragma unroll
-        for (int c = k + 1; c < S; ++c) {
-          const double mkc = m[k][c];
+            for (int r = 1; r < S; ++r) m[r][c] -= m[r][0];
+        } else {
 #pragma unroll
-          for (int r = k + 1; r < S; ++r) m[r][c] -= m[r][k] * mkc;
+          for (int c = k + 1; c < S; ++c) {
+            const double mkc = m[k][c];
+#pragma unroll
+            for (int r = k + 1; r < S; ++r) m[r][c] -= m[r][k] * mkc;
+          }
         }
         continue;
       }
@@ -317,7 +326,10 @@ GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (
 #pragma unroll
   for (int i = S - 1; i >= 0; --i) {
     const bool act = i < rank && c[i] != 0.0;
-    const double ci = c[i] / (act ? m[i][i] : 1.0);
+    // u_00 = u_11 = 1 exactly on the KKT fast path (columns 0 and 1 are never
+    // swapped again), so those divisions are identities
+    double ci = c[i];
+    if (!(KKT && i < 2 && fast)) ci = c[i] / (act ? m[i][i] : 1.0);
     c[i] = act ? ci : c[i];
 #pragma unroll
     for (int r = 0; r < i; ++r) c[r] = act ? c[r] - ci * m[r][i] : c[r];
