@@ -990,9 +990,10 @@ struct grasp_ctx {
     st.pair_need = pair_need.p;
     st.seg_count = seg_count.p;
     st.seg_offset = seg_offset.p;
-    // EPA jobs: up to a quarter of all pair slots at once; beyond that the
-    // pair is redone by k_pairs_big (never observed).
-    const size_t epa_cap = std::max<size_t>(1024, g * NP / 4);
+    // EPA jobs: room for every pair slot (beyond the capacity a pair would be
+    // redone by the slow k_pairs_big; a quarter of the slots overflowed on
+    // config 3, where the Leap hand's links sink into the primitives).
+    const size_t epa_cap = std::max<size_t>(1024, g * NP);
     epa_jobs.ensure(2 * epa_cap * kEpaJobStride);
     st.epa_count = pair_count.p + 1;
     st.epa_long_count = pair_count.p + 3;
@@ -1118,11 +1119,13 @@ struct grasp_ctx {
       // the GJK pass and the EPA of the other pairs
       ck(cudaEventRecord(ev_fork, stream), "event");
       ck(cudaStreamWaitEvent(side, ev_fork, 0), "event");
-      k_pairs_early<<<blocks(std::min<long long>(n, st.epa_cap), 32), 32, 0, side>>>(H, O, st);
+      // (both grid-stride: grids sized for the usual counts, n / 8 early pairs
+      // and n / 4 EPA jobs, not for the worst case)
+      k_pairs_early<<<blocks(std::max<long long>(1024, n / 8), 32), 32, 0, side>>>(H, O, st);
       ck(cudaEventRecord(ev_join, side), "event");
       k_pairs_list<<<blocks(n, GDEV_PAIRS_BLOCK), GDEV_PAIRS_BLOCK, 0, stream>>>(H, O, st);
       // EPA jobs spread over all SMs (32-thread blocks; few jobs per launch)
-      k_pairs_epa<<<blocks(2 * std::min<long long>(n, st.epa_cap), 32), 32, 0, stream>>>(H, O, st);
+      k_pairs_epa<<<blocks(std::max<long long>(1024, n / 2), 32), 32, 0, stream>>>(H, O, st);
       ck(cudaStreamWaitEvent(stream, ev_join, 0), "event");
     });
     launch(7, [&] { k_pairs_big<<<kBigSlots / 128, 128, 0, stream>>>(H, O, st); });

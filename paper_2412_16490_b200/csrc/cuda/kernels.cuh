@@ -1259,6 +1259,7 @@ __device__ __forceinline__ void write_epa_job(const DevState& st, int slot, cons
   const bool long_job = st.epa_hist[slot] > kEpaLongPred;
   const int job = atomicAdd(long_job ? st.epa_long_count : st.epa_count, 1);
   if (job >= st.epa_cap) {
+    if (st.ops) atomicAdd(st.ops + kOpEpaOverflow, 1ull);
     queue_overflow(st, slot);
     return;
   }
@@ -1302,14 +1303,17 @@ __global__ void __launch_bounds__(GDEV_PAIRS_BLOCK, GDEV_PAIRS_MIN_BLOCKS) k_pai
 #ifndef GDEV_EPA_MIN_BLOCKS
 #define GDEV_EPA_MIN_BLOCKS 1
 #endif
+__device__ __forceinline__ void epa_job(const DevHand& H, const DevObject& O, const DevState& st, int job);
+
+// (grid-stride over the jobs: the grid is sized for the usual job count)
 __global__ void __launch_bounds__(32, GDEV_EPA_MIN_BLOCKS) k_pairs_epa(DevHand H, DevObject O, DevState st) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int n_long = min(*st.epa_long_count, st.epa_cap);
-  int job = st.epa_cap + i;  // predicted-long jobs first
-  if (i >= n_long) {
-    job = i - n_long;
-    if (job >= min(*st.epa_count, st.epa_cap)) return;
-  }
+  const int n_all = n_long + min(*st.epa_count, st.epa_cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_all; i += gridDim.x * blockDim.x)
+    epa_job(H, O, st, i < n_long ? st.epa_cap + i : i - n_long);  // predicted-long jobs first
+}
+
+__device__ __forceinline__ void epa_job(const DevHand& H, const DevObject& O, const DevState& st, int job) {
   const double* jb = st.epa_jobs + (size_t)job * kEpaJobStride;
   const int slot = (int)jb[0], ns = (int)jb[1];
   SP simp[4];
