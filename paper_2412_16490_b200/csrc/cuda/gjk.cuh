@@ -305,15 +305,27 @@ GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (
   double c[S];
 #pragma unroll
   for (int i = 0; i < S; ++i) c[i] = rhs[i];
+  bool permute = true;
+  if constexpr (KKT) {
+    // rhs = e_{S-1} and the fast path's row transpositions are (0, S-1), none,
+    // then swaps among rows >= 2 (zeros): the permuted rhs is e_0 exactly
+    if (fast) {
 #pragma unroll
-  for (int k = 0; k < S; ++k) {
-    const double old = c[k];
-    double pick = old;
+      for (int i = 0; i < S; ++i) c[i] = i == 0 ? 1.0 : 0.0;
+      permute = false;
+    }
+  }
+  if (permute) {
 #pragma unroll
-    for (int r = k + 1; r < S; ++r) pick = (rowt[k] == r) ? c[r] : pick;
+    for (int k = 0; k < S; ++k) {
+      const double old = c[k];
+      double pick = old;
 #pragma unroll
-    for (int r = k + 1; r < S; ++r) c[r] = (rowt[k] == r) ? old : c[r];
-    c[k] = pick;
+      for (int r = k + 1; r < S; ++r) pick = (rowt[k] == r) ? c[r] : pick;
+#pragma unroll
+      for (int r = k + 1; r < S; ++r) c[r] = (rowt[k] == r) ? old : c[r];
+      c[k] = pick;
+    }
   }
   // Substitutions with the reference's zero skips as selects (same
   // operations on the taken path, no lane-dependent branches).
