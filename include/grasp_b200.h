@@ -60,6 +60,19 @@ int grasp_object_parse(const char* obj_text, double scale, const char* source, g
 int grasp_object_from_points(int n_parts, const int* counts, const double* points, grasp_object** out);
 void grasp_object_free(grasp_object* o);
 double grasp_object_bounding_radius(const grasp_object* o);
+/* geom::make_convex_part for many point clouds on the device (
+ * geometry.cpp:414-466 with the quickhull of hull3d.cpp:291-303), one thread
+ * per part, bit-identical to the host builder (grasp_object_from_points).
+ * Part p's points are points[3 * point_begin[p] .. 3 * point_begin[p + 1]).
+ * Outputs per part p: out_n_verts[p] hull vertices at out_verts[3 *
+ * point_begin[p] ...], out_n_faces[p] faces (local vertex triples) at
+ * out_faces[6 * point_begin[p] ...] (room for 2 faces per point),
+ * out_volume[p], out_centroid[3p..], out_obb[15p..] (center, half extents,
+ * rotation column-major), out_status[p] (0 ok, 1 degenerate: fewer than 4
+ * non-coplanar points or non-positive volume, 2 workspace overflow). */
+int grasp_build_convex_parts(int device, const double* points, const int* point_begin, int n_parts, double merge_tol,
+                             double* out_verts, int* out_n_verts, int* out_faces, int* out_n_faces,
+                             double* out_volume, double* out_centroid, double* out_obb, int* out_status);
 
 /* Packed, read-only views of a model (pointers stay valid while the handle lives). */
 typedef struct grasp_hand_desc {

@@ -98,6 +98,8 @@ SIGNATURES = {
     "grasp_object_primitive": (C.c_int, [C.c_char_p, C.c_double, C.POINTER(C.c_void_p)]),
     "grasp_object_parse": (C.c_int, [C.c_char_p, C.c_double, C.c_char_p, C.POINTER(C.c_void_p)]),
     "grasp_object_from_points": (C.c_int, [C.c_int, _ip, _dp, C.POINTER(C.c_void_p)]),
+    "grasp_build_convex_parts": (C.c_int, [C.c_int, _dp, _ip, C.c_int, C.c_double, _dp, _ip, _ip, _ip, _dp, _dp, _dp,
+                                           _ip]),
     "grasp_object_free": (None, [C.c_void_p]),
     "grasp_object_bounding_radius": (C.c_double, [C.c_void_p]),
     "grasp_hand_describe": (C.c_int, [C.c_void_p, C.POINTER(HandDesc)]),

@@ -325,6 +325,32 @@ load_object = ObjectModel.load
 PRIMITIVE_NAMES = ("sphere", "box", "cylinder", "capsule", "flat_box")
 
 
+def build_convex_parts(parts, merge_tol: float = 1e-9, device: int = 0) -> List[dict]:
+    """make_convex_part (geometry.cpp:414-466) of many point clouds on the device, one thread per
+    part (grasp_build_convex_parts), bit-identical to the host builder (ObjectModel.from_points).
+    Returns per part: vertices (V, 3), faces (F, 3) local indices, volume, centroid (3,),
+    obb (15,) = center, half extents, rotation column-major, status (0 ok, 1 degenerate,
+    2 workspace overflow)."""
+    arrs = [np.asarray(p, dtype=np.float64).reshape(-1, 3) for p in parts]
+    begin = np.zeros(len(arrs) + 1, dtype=np.int32)
+    begin[1:] = np.cumsum([len(a) for a in arrs])
+    n_pts, n = int(begin[-1]), len(arrs)
+    pts = np.ascontiguousarray(np.concatenate(arrs) if n_pts else np.zeros((0, 3)))
+    verts = np.zeros((max(n_pts, 1), 3))
+    faces = np.zeros((max(2 * n_pts, 1), 3), dtype=np.int32)
+    nv, nf, status = (np.zeros(max(n, 1), dtype=np.int32) for _ in range(3))
+    vol, cen, obb = np.zeros(max(n, 1)), np.zeros((max(n, 1), 3)), np.zeros((max(n, 1), 15))
+    N.check(N.lib().grasp_build_convex_parts(int(device), dptr(pts), iptr(begin), n, float(merge_tol), dptr(verts),
+                                             iptr(nv), iptr(faces), iptr(nf), dptr(vol), dptr(cen), dptr(obb),
+                                             iptr(status)))
+    out = []
+    for p in range(n):
+        b = int(begin[p])
+        out.append(dict(vertices=verts[b:b + nv[p]].copy(), faces=faces[2 * b:2 * b + nf[p]].copy(),
+                        volume=float(vol[p]), centroid=cen[p].copy(), obb=obb[p].copy(), status=int(status[p])))
+    return out
+
+
 def init_poses(model: HandModel, obj: ObjectModel, n: int, seed: int, params: InitParams = None) -> np.ndarray:
     """pipeline.cpp:388-424 -> (n, D) array."""
     params = params or InitParams()
