@@ -421,6 +421,10 @@ __global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_RESIDENT_WARPS / G
       for (int e = 0; e < KMAX; ++e)
         if (e < k) rp_ = fmax(rp_, fabs(x[e] - relu_bits(vz[e])));
       rp_ = qp_group_max<MT>(rp_, base, m);
+      // The dual residual only matters for a live column whose primal residual
+      // passed: skipped (warp-uniformly) when there is none (ok is false then).
+      double rd = INFINITY;
+      if (__any_sync(kFull, !frozen && rp_ <= P.eps_primal)) {
       // W x over the column, then (W^T W x)_e = edge_e . (wf + wt x p)
       D3 wf, wt;
       double sx_;
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_RESIDENT_WARPS / G
       const D3 u = wf + cross(wt, fp);
       const D3 fn = ld3(s.frame + 12 * c + 3), fd = ld3(s.frame + 12 * c + 6), fe = ld3(s.frame + 12 * c + 9);
       const double nu = dot(fn, u), du = dot(fd, u), eu = dot(fe, u);
-      double rd = 0.0;
+      rd = 0.0;
 #pragma unroll
       for (int e = 0; e < KMAX; ++e) {
         if (e < k) {
@@ -440,6 +444,7 @@ __global__ void __launch_bounds__(32 * GDEV_QP_WARPS, GDEV_QP_RESIDENT_WARPS / G
         }
       }
       rd = qp_group_max<MT>(rd, base, m);
+      }
       if (!frozen) {
         const bool ok = rp_ <= P.eps_primal && rd <= P.eps_dual;
         if (ok || iter == P.max_iters) {
