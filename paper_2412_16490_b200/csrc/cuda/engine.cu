@@ -950,7 +950,7 @@ struct grasp_ctx {
     pq_key.ensure(g * NQ);
     pq_list.ensure(g * NQ);
     pq_total.ensure(1);
-    pq_count.ensure(static_cast<size_t>(has_object ? O.NC + O.P + 1 : 1));
+    pq_count.ensure(static_cast<size_t>(has_object ? 2 * O.NC + O.P + 1 : 1));
     st.pq_key = pq_key.p;
     st.pq_list = pq_list.p;
     st.pq_total = pq_total.p;
@@ -1083,7 +1083,7 @@ struct grasp_ctx {
     const int* sl = tips_only ? h_tip_slots.p : nullptr;
     if (!tips_only && L == 1 && bucket_queries) {
       launch(0, [&] {
-        const int nb = O.NC + O.P + 1;
+        const int nb = 2 * O.NC + O.P + 1;
         ck(cudaMemsetAsync(pq_count.p, 0, sizeof(int) * nb, stream), "memset");
         k_pq_count<<<blocks(n, 128), 128, 0, stream>>>(O, st);
         k_exclusive_scan<<<1, 1024, 0, stream>>>(pq_count.p, nb, pq_total.p);

@@ -1133,11 +1133,13 @@ __global__ void __launch_bounds__(128) k_pairs_scatter(DevState st, const int* _
 // a query does not change its result, so the order is free.
 __device__ __forceinline__ int pq_bucket(const DevObject& O, const DevState& st, size_t t) {
   const int f = st.qface[t];
-  if (f >= 0 && f < O.F) return __ldg(O.face_cluster + f);
   const double d = st.qres[t * 8];
+  // inside queries (last result negative) apart from outside ones: they take
+  // the plane-group path, the others the face scan
+  if (f >= 0 && f < O.F) return __ldg(O.face_cluster + f) + (d < 0.0 ? O.NC : 0);
   const double pd = st.qres[t * 8 + 7];
-  if (d < 0.0 && pd >= 0.0 && pd < O.P) return O.NC + (int)pd;
-  return O.NC + O.P;
+  if (d < 0.0 && pd >= 0.0 && pd < O.P) return 2 * O.NC + (int)pd;
+  return 2 * O.NC + O.P;
 }
 
 __global__ void __launch_bounds__(128) k_pq_count(DevObject O, DevState st) {
