@@ -34,24 +34,31 @@ def shard_start_states(model, obj, cfg: RunConfig, rank: int, world: int) -> np.
 
 
 def gather_outputs(local: SynthesisOutput, cfg: RunConfig, world: int, device=None) -> SynthesisOutput:
-    """all_gather every record field (padded to the largest shard) and
-    reassemble the global batch in input order on every rank."""
+    """One all_gather of every record field: each rank packs its rows (all fields side by side,
+    as float64 - the integer fields are small and exact in it) into one matrix padded to the
+    largest shard, and every rank unpacks the global batch in input order."""
     import torch
     import torch.distributed as dist
 
     sizes = [shard_range(r, world, cfg.batch)[1] - shard_range(r, world, cfg.batch)[0] for r in range(world)]
     cap = max(sizes)
+    cols = [getattr(local, name).reshape(local.failed.shape[0], -1) for name in FIELDS]
+    widths = [c.shape[1] for c in cols]
+    packed = np.zeros((cap, sum(widths)))
+    packed[: local.failed.shape[0]] = np.concatenate([c.astype(np.float64) for c in cols], axis=1)
+    t = torch.from_numpy(packed)
+    if device is not None:
+        t = t.to(device)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    rows = np.concatenate([p.cpu().numpy()[:n] for p, n in zip(parts, sizes)])
     glob = SynthesisOutput.__new__(SynthesisOutput)
-    for name in FIELDS:
-        arr = getattr(local, name)
-        pad = np.zeros((cap,) + arr.shape[1:], dtype=arr.dtype)
-        pad[: arr.shape[0]] = arr
-        t = torch.from_numpy(pad)
-        if device is not None:
-            t = t.to(device)
-        parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t)
-        setattr(glob, name, np.concatenate([p.cpu().numpy()[:n] for p, n in zip(parts, sizes)]))
+    off = 0
+    for name, w in zip(FIELDS, widths):
+        ref = getattr(local, name)
+        block = rows[:, off:off + w].reshape((rows.shape[0],) + ref.shape[1:])
+        setattr(glob, name, block.astype(ref.dtype))
+        off += w
     return glob
 
 
