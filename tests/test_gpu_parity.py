@@ -877,3 +877,53 @@ def test_diverging_grasps_are_flagged_on_device(G, O, trident, engine):
     assert np.array_equal(gpu.failed, cpu.failed)
     assert np.isfinite(gpu.x).all()
     assert np.isnan(gpu.energy_total).all()
+
+
+def _finger_hand_json(lengths):
+    """A palm box with one chain of revolute box links per finger (lengths[i] links), the last
+    link of each finger carrying a tip proxy."""
+    import json
+    box = [[x, y, z] for x in (-0.005, 0.005) for y in (-0.005, 0.005) for z in (0.0, 0.02)]
+    prox = [{"center": [0, 0, 0.01], "radius": 0.005}]
+    links = [{"name": "palm", "vertices": box, "proxies": prox}]
+    for f, n in enumerate(lengths):
+        parent = "palm"
+        for i in range(n):
+            name = f"f{f}_{i}"
+            origin = [0.012 * (f - len(lengths) / 2), 0, 0.02] if i == 0 else [0, 0, 0.02]
+            link = {"name": name, "joint": {"name": f"j{f}_{i}", "parent": parent, "origin": origin,
+                                            "axis": [1, 0, 0], "lower": -0.5, "upper": 0.5},
+                    "vertices": box, "proxies": prox}
+            if i == n - 1:
+                link["tip_proxy"] = 0
+            links.append(link)
+            parent = name
+    return json.dumps({"format_version": 1, "name": "fingers", "links": links})
+
+
+def test_device_capacity_limits_are_invalid_arguments(G, engine):
+    """The engine's fixed capacities (32 links, 1..5 fingertips, chains up to 12 joints deep,
+    64 parts per object) and an empty batch are reported as invalid arguments (the reference's
+    std::invalid_argument), never truncated; a hand at the limits runs."""
+    ok = G.HandModel.from_json(_finger_hand_json([7, 6, 6, 6, 6]))  # 32 links, 31 joints, 5 tips
+    obj = G.make_primitive("sphere", 0.1)
+    engine.set_hand(ok)
+    engine.set_object(obj)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 4, 3
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 3, 2, 2
+    out = engine.synthesize(cfg, G.init_poses(ok, obj, cfg.batch, cfg.seed, cfg.init))
+    assert out.x.shape[0] == 4
+    for lengths in ([7, 7, 6, 6, 6], [2] * 6, [13]):  # 33 links; 6 tips; a chain deeper than 12
+        h = G.HandModel.from_json(_finger_hand_json(lengths))
+        with pytest.raises(G.InvalidArgument):
+            engine.set_hand(h)
+    engine.set_hand(ok)
+    many = G.ObjectModel.from_points([np.random.default_rng(i).normal(size=(8, 3)) * 0.01 + [0.05 * i, 0, 0]
+                                      for i in range(65)])
+    with pytest.raises(G.InvalidArgument):
+        engine.set_object(many)
+    engine.set_object(obj)
+    cfg.batch = 0
+    with pytest.raises(G.InvalidArgument):
+        engine.synthesize(cfg, np.zeros((0, ok.dims())))
