@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -131,7 +132,8 @@ struct grasp_ctx {
   DevBuf<double> o_faces, o_verts, o_centroid, o_half, o_obb, o_part_sphere, o_face_sphere, o_part_box;
   DevBuf<float4> o_face_sphere32, o_cluster_sphere32, o_face_box32, o_cluster_box32;
   DevBuf<double4> o_face_plane;
-  DevBuf<int> o_part_cbeg, o_cluster_fbeg, o_face_cluster, o_obj_pbeg, obj_ids;
+  DevBuf<int> o_part_cbeg, o_cluster_fbeg, o_face_cluster, o_obj_pbeg, obj_ids, o_pq_fid;
+  DevBuf<double> o_pq_faces;
   DevBuf<int> o_part_gbeg, o_grp_beg, o_grp_face, o_sup_gbeg;
   DevBuf<float4> o_grp_bound, o_sup_bound;
   DevBuf<double4> o_grp_plane;
@@ -582,11 +584,52 @@ struct grasp_ctx {
     o_part_sphere.upload(part_sphere, s);
     o_part_box.upload(containing_boxes(d->part_obb, d->verts, d->part_vert_begin, P), s);
     o_face_sphere.upload(face_sphere, s);
+    // Point-query face order: within each part the faces are reordered into
+    // spatially compact runs (recursive median splits of the centroids along
+    // the widest axis, runs of kFaceCluster), so the clusters' bounds are
+    // tight. The scans then compare (distance, original index) pairs, the
+    // lexicographic minimum the reference's index-order strict '<' picks, so
+    // the order is free. faces_q / face_sphere_q are the permuted copies,
+    // pq_fid maps a position back to the face index.
+    std::vector<int> perm(d->n_faces);
+    {
+      std::function<void(int*, int*)> split = [&](int* b, int* e) {
+        const long n = e - b;
+        if (n <= kFaceCluster) return;
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int* q = b; q < e; ++q)
+          for (int k = 0; k < 3; ++k) {
+            lo[k] = std::min(lo[k], face_sphere[4 * *q + k]);
+            hi[k] = std::max(hi[k], face_sphere[4 * *q + k]);
+          }
+        int ax = 0;
+        for (int k = 1; k < 3; ++k)
+          if (hi[k] - lo[k] > hi[ax] - lo[ax]) ax = k;
+        std::stable_sort(b, e, [&](int x, int y) { return face_sphere[4 * x + ax] < face_sphere[4 * y + ax]; });
+        const long h = ((n + 2 * kFaceCluster - 1) / (2 * kFaceCluster)) * kFaceCluster;
+        split(b, b + h);
+        split(b + h, e);
+      };
+      for (int p = 0; p < P; ++p) {
+        for (int f = fbeg[p]; f < fbeg[p + 1]; ++f) perm[f] = f;
+        split(perm.data() + fbeg[p], perm.data() + fbeg[p + 1]);
+      }
+    }
+    std::vector<double> faces_q(faces.size()), face_sphere_q(face_sphere.size());
+    for (int k = 0; k < d->n_faces; ++k) {
+      std::copy_n(faces.data() + static_cast<size_t>(perm[k]) * kFaceStride, kFaceStride,
+                  faces_q.data() + static_cast<size_t>(k) * kFaceStride);
+      std::copy_n(face_sphere.data() + 4 * static_cast<size_t>(perm[k]), 4, face_sphere_q.data() + 4 * static_cast<size_t>(k));
+    }
+    o_pq_faces.upload(faces_q, s);
+    o_pq_fid.upload(perm, s);
+    O.pq_faces = o_pq_faces.p;
+    O.pq_fid = o_pq_fid.p;
     std::vector<float4> face32(d->n_faces);
     for (int f = 0; f < d->n_faces; ++f) {
-      const float r = static_cast<float>(face_sphere[4 * f + 3]);
-      face32[f] = make_float4(static_cast<float>(face_sphere[4 * f]), static_cast<float>(face_sphere[4 * f + 1]),
-                              static_cast<float>(face_sphere[4 * f + 2]),
+      const float r = static_cast<float>(face_sphere_q[4 * f + 3]);
+      face32[f] = make_float4(static_cast<float>(face_sphere_q[4 * f]), static_cast<float>(face_sphere_q[4 * f + 1]),
+                              static_cast<float>(face_sphere_q[4 * f + 2]),
                               std::nextafter(std::nextafter(r, 1e30f), 1e30f) * (1.0f + 1e-6f));
     }
     o_face_sphere32.upload(face32, s);
@@ -595,8 +638,8 @@ struct grasp_ctx {
     // rounded axes (+ relative and absolute pad), so the box contains the
     // triangle exactly in the rounded frame.
     std::vector<float4> box32(4 * static_cast<size_t>(d->n_faces));
-    for (int f = 0; f < d->n_faces; ++f) {
-      const double* F = faces.data() + static_cast<size_t>(f) * kFaceStride;
+    for (int f = 0; f < d->n_faces; ++f) {  // (point-query order)
+      const double* F = faces_q.data() + static_cast<size_t>(f) * kFaceStride;
       const double* V[3] = {F, F + 3, F + 6};
       int e0 = 0;
       double best = -1.0;
@@ -661,7 +704,7 @@ struct grasp_ctx {
       planes[f] = F[13] != 0.0 ? make_double4(F[9], F[10], F[11], F[12]) : make_double4(0.0, 0.0, 0.0, INFINITY);
     }
     o_face_plane.upload(planes, s);
-    // Face clusters: runs of kFaceCluster consecutive faces inside a part,
+    // Face clusters: runs of kFaceCluster consecutive faces (point-query order) inside a part,
     // each with a sphere containing its faces' spheres (fp32 centre, radius
     // from the rounded centre in fp64, rounded up).
     std::vector<int> part_cbeg(P + 1, 0), cluster_fbeg;
@@ -672,12 +715,12 @@ struct grasp_ctx {
         const int b = std::min(fbeg[p + 1], a + kFaceCluster);
         double c[3] = {0, 0, 0};
         for (int f = a; f < b; ++f)
-          for (int k = 0; k < 3; ++k) c[k] += face_sphere[4 * f + k] / (b - a);
+          for (int k = 0; k < 3; ++k) c[k] += face_sphere_q[4 * f + k] / (b - a);
         const float cx = static_cast<float>(c[0]), cy = static_cast<float>(c[1]), cz = static_cast<float>(c[2]);
         double r = 0.0;
         for (int f = a; f < b; ++f) {
-          const double dx = face_sphere[4 * f] - cx, dy = face_sphere[4 * f + 1] - cy, dz = face_sphere[4 * f + 2] - cz;
-          r = std::max(r, std::sqrt(dx * dx + dy * dy + dz * dz) + face_sphere[4 * f + 3]);
+          const double dx = face_sphere_q[4 * f] - cx, dy = face_sphere_q[4 * f + 1] - cy, dz = face_sphere_q[4 * f + 2] - cz;
+          r = std::max(r, std::sqrt(dx * dx + dy * dy + dz * dz) + face_sphere_q[4 * f + 3]);
         }
         const float r32 = std::nextafter(std::nextafter(static_cast<float>(r * (1.0 + 1e-12)), 1e30f), 1e30f);
         cluster32.push_back(make_float4(cx, cy, cz, r32 * (1.0f + 1e-6f)));
@@ -692,10 +735,10 @@ struct grasp_ctx {
           const int nv = 3 * (b - a);
           for (int f = a; f < b; ++f)
             for (int q = 0; q < 3; ++q)
-              for (int k = 0; k < 3; ++k) mean[k] += faces[static_cast<size_t>(f) * kFaceStride + 3 * q + k] / nv;
+              for (int k = 0; k < 3; ++k) mean[k] += faces_q[static_cast<size_t>(f) * kFaceStride + 3 * q + k] / nv;
           for (int f = a; f < b; ++f)
             for (int q = 0; q < 3; ++q) {
-              const double* X = faces.data() + static_cast<size_t>(f) * kFaceStride + 3 * q;
+              const double* X = faces_q.data() + static_cast<size_t>(f) * kFaceStride + 3 * q;
               for (int r = 0; r < 3; ++r)
                 for (int k = 0; k < 3; ++k) C[r][k] += (X[r] - mean[r]) * (X[k] - mean[k]);
             }
@@ -732,7 +775,7 @@ struct grasp_ctx {
           double h[3] = {0, 0, 0};
           for (int f = a; f < b; ++f)
             for (int q = 0; q < 3; ++q) {
-              const double* X = faces.data() + static_cast<size_t>(f) * kFaceStride + 3 * q;
+              const double* X = faces_q.data() + static_cast<size_t>(f) * kFaceStride + 3 * q;
               const double r3[3] = {X[0] - of[0], X[1] - of[1], X[2] - of[2]};
               for (int r = 0; r < 3; ++r)
                 h[r] = std::max(h[r], std::fabs(r3[0] * ax[r][0] + r3[1] * ax[r][1] + r3[2] * ax[r][2]));
@@ -753,9 +796,9 @@ struct grasp_ctx {
     o_cluster_sphere32.upload(cluster32, s);
     o_cluster_box32.upload(cbox32, s);
     {
-      std::vector<int> fc(d->n_faces, 0);
+      std::vector<int> fc(d->n_faces, 0);  // indexed by face, the cluster of its position
       for (size_t c = 0; c + 1 < cluster_fbeg.size(); ++c)
-        for (int f = cluster_fbeg[c]; f < cluster_fbeg[c + 1]; ++f) fc[f] = static_cast<int>(c);
+        for (int k = cluster_fbeg[c]; k < cluster_fbeg[c + 1]; ++k) fc[perm[k]] = static_cast<int>(c);
       o_face_cluster.upload(fc, s);
     }
     // Plane groups for the inside test: per part, the non-degenerate faces

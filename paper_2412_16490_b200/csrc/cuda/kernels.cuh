@@ -332,18 +332,19 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p
           seed_c = c;
         }
       }
-      seed_f = __ldg(O.cluster_fbeg + seed_c);
+      int seed_k = __ldg(O.cluster_fbeg + seed_c);
       const int e = __ldg(O.cluster_fbeg + seed_c + 1);
       float lbf = INFINITY;
-      for (int f = seed_f; f < e; ++f) {
-        const float4 S = __ldg(O.face_sphere32 + f);
+      for (int k = seed_k; k < e; ++k) {
+        const float4 S = __ldg(O.face_sphere32 + k);
         const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
         const float lb = sqrt_approx(dx * dx + dy * dy + dz * dz) - S.w;
         if (lb < lbf) {
           lbf = lb;
-          seed_f = f;
+          seed_k = k;
         }
       }
+      seed_f = __ldg(O.pq_fid + seed_k);
     }
     // Inside test (query_part, geometry.cpp:369-383): inside iff no face
     // plane has depth < -1e-12; then the shallowest face in index order
@@ -464,10 +465,10 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p
         }
         if (cluster_box_far(O, c, px, py, pz, fminf(bound, sd32) + kCullSlack32)) continue;
         const int e = __ldg(O.cluster_fbeg + c + 1);
-        for (int f = __ldg(O.cluster_fbeg + c); f < e; ++f) {
+        for (int k = __ldg(O.cluster_fbeg + c); k < e; ++k) {
           const float cut = fminf(bound, sd32);
           {
-            const float4 S = __ldg(O.face_sphere32 + f);
+            const float4 S = __ldg(O.face_sphere32 + k);
             const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
             const float reach = cut + S.w + kCullSlack32;
             if (dx * dx + dy * dy + dz * dz > reach * reach) continue;
@@ -479,8 +480,8 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p
           // covered by the slack). Tight for the long thin faces that
           // sphere bounds cannot separate.
           {
-            const float4 B0 = __ldg(O.face_box32 + 4 * f), B1 = __ldg(O.face_box32 + 4 * f + 1);
-            const float4 B2 = __ldg(O.face_box32 + 4 * f + 2), B3 = __ldg(O.face_box32 + 4 * f + 3);
+            const float4 B0 = __ldg(O.face_box32 + 4 * k), B1 = __ldg(O.face_box32 + 4 * k + 1);
+            const float4 B2 = __ldg(O.face_box32 + 4 * k + 2), B3 = __ldg(O.face_box32 + 4 * k + 3);
             const float rx = px - B0.x, ry = py - B0.y, rz = pz - B0.z;
             const float eu = fmaxf(fabsf(rx * B1.x + ry * B1.y + rz * B1.z) - B0.w, 0.0f);
             const float ev = fmaxf(fabsf(rx * B2.x + ry * B2.y + rz * B2.z) - B1.w, 0.0f);
@@ -489,10 +490,11 @@ __device__ inline PointHit point_to_mesh(const DevObject& O, D3 p, int p0, int p
             if (eu * eu + ev * ev + en * en > reach * reach) continue;
           }
           ++tris;
-          const double* F = O.faces + (size_t)f * kFaceStride;
+          const double* F = O.pq_faces + (size_t)k * kFaceStride;
           const D3 cp = closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6));
           const double d = nrm(p - cp);
-          if (d < sd) {
+          const int f = __ldg(O.pq_fid + k);
+          if (d < sd || (d == sd && f < sf)) {  // lexicographic (distance, face) minimum
             sd = d;
             sd32 = __double2float_ru(d) + kCullSlack32;
             pt = cp;
@@ -614,6 +616,7 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int p0, int p1
         }
       }
       group_lexmin<L>(gmask, lbf, seed_f);
+      seed_f = __ldg(O.pq_fid + seed_f);  // position -> face
     }
     // Inside test as in point_to_mesh: the seed, last separating and warm
     // planes first, then the normal groups whose depth bound does not exceed
@@ -721,17 +724,17 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int p0, int p1
         }
         if (cluster_box_far(O, c, px, py, pz, fminf(bound, sd32) + kCullSlack32)) continue;
         const int e = __ldg(O.cluster_fbeg + c + 1);
-        for (int f = __ldg(O.cluster_fbeg + c) + gl; f < e; f += L) {
+        for (int k = __ldg(O.cluster_fbeg + c) + gl; k < e; k += L) {
           const float cut = fminf(bound, sd32);
           {
-            const float4 S = __ldg(O.face_sphere32 + f);
+            const float4 S = __ldg(O.face_sphere32 + k);
             const float dx = px - S.x, dy = py - S.y, dz = pz - S.z;
             const float reach = cut + S.w + kCullSlack32;
             if (dx * dx + dy * dy + dz * dz > reach * reach) continue;
           }
           {
-            const float4 B0 = __ldg(O.face_box32 + 4 * f), B1 = __ldg(O.face_box32 + 4 * f + 1);
-            const float4 B2 = __ldg(O.face_box32 + 4 * f + 2), B3 = __ldg(O.face_box32 + 4 * f + 3);
+            const float4 B0 = __ldg(O.face_box32 + 4 * k), B1 = __ldg(O.face_box32 + 4 * k + 1);
+            const float4 B2 = __ldg(O.face_box32 + 4 * k + 2), B3 = __ldg(O.face_box32 + 4 * k + 3);
             const float rx = px - B0.x, ry = py - B0.y, rz = pz - B0.z;
             const float eu = fmaxf(fabsf(rx * B1.x + ry * B1.y + rz * B1.z) - B0.w, 0.0f);
             const float ev = fmaxf(fabsf(rx * B2.x + ry * B2.y + rz * B2.z) - B1.w, 0.0f);
@@ -740,10 +743,11 @@ __device__ PointHit point_to_mesh_group(const DevObject& O, D3 p, int p0, int p1
             if (eu * eu + ev * ev + en * en > reach * reach) continue;
           }
           ++tris;
-          const double* F = O.faces + (size_t)f * kFaceStride;
+          const double* F = O.pq_faces + (size_t)k * kFaceStride;
           const D3 cp = closest_on_triangle(p, ldg3(F), ldg3(F + 3), ldg3(F + 6));
           const double d = nrm(p - cp);
-          if (d < sd) {
+          const int f = __ldg(O.pq_fid + k);
+          if (d < sd || (d == sd && f < lf)) {  // lexicographic (distance, face) minimum
             sd = d;
             sd32 = __double2float_ru(d) + kCullSlack32;
             pt = cp;

@@ -72,11 +72,17 @@ struct DevObject {
   const double* part_sphere;    // [P*4] bounding sphere of the part: center, radius
   const double* part_box;       // [P*15] box containing the part hull: center, half, axes (col-major)
   const double* face_sphere;    // [F*4] bounding sphere of each triangle: center, radius
-  const float4* face_sphere32;  // [F] same in fp32, radius rounded up (culling bounds only)
+  // Point-query order: within each part the faces are permuted into spatially
+  // compact runs (engine.cu set_object); face_sphere32, face_box32, the
+  // clusters and pq_faces are indexed by position, pq_fid maps a position to
+  // the face index (the scans compare (distance, face index) pairs).
+  const double* pq_faces;       // [F*kFaceStride] face records in point-query order
+  const int* pq_fid;            // [F] face index of each position
+  const float4* face_sphere32;  // [F] (point-query order) face spheres in fp32, radius rounded up (culling bounds only)
   const double4* face_plane;    // [F] (n, n.a) in fp64; degenerate faces (0, 0, 0, +inf)
-  const float4* face_box32;     // [4F] thin box per face: (o, hu), (u, hv), (v, hn), (n, 0); fp32, bounds only
+  const float4* face_box32;     // [4F] (point-query order) thin box per face: (o, hu), (u, hv), (v, hn), (n, 0); fp32, bounds only
   const int* part_cbeg;         // [P+1] face clusters of each part
-  const int* cluster_fbeg;      // [NC+1] first face of each cluster (consecutive indices)
+  const int* cluster_fbeg;      // [NC+1] first position of each cluster (point-query order)
   const float4* cluster_sphere32;  // [NC] fp32 sphere bounding the cluster's face spheres
   const float4* cluster_box32;     // [NC*4] fp32 oriented box of the cluster's vertices (face-box layout)
   const int* part_cm;              // [P] base of the part hull's support map in cm_off, -1 = full scan
