@@ -104,6 +104,7 @@ struct grasp_ctx {
   DevBuf<int> pq_key, pq_list, pq_total, pq_count;
   // Engine options (grasp_ctx_set_option; defaults = the product settings).
   bool bucket_queries = true;  // "query_buckets": coarse queries listed by spatial bucket
+  long long pq_age = 0;        // launches since the bucketed list was rebuilt (0: rebuild)
   bool opt_cull = false;       // "pair_cull": opt-in separation cull of (link, part) pairs
   bool opt_sat = true;         // "pair_sat": link-box vs part-box SAT inside that cull
   int query_lanes = 1;         // "query_lanes": lanes per query in all-slot launches
@@ -1125,12 +1126,18 @@ struct grasp_ctx {
     const int L = tips_only ? tip_query_lanes : query_lanes;
     const int* sl = tips_only ? h_tip_slots.p : nullptr;
     if (!tips_only && L == 1 && bucket_queries) {
+      // The bucketed list is a permutation of the live slots and only
+      // affects speed; it is rebuilt every kPqRebucket calls (and at the
+      // start of a run): points move little per iteration.
+      const bool rebuild = pq_age++ % kPqRebucket == 0;
       launch(0, [&] {
-        const int nb = 2 * O.NC + O.P + 1;
-        ck(cudaMemsetAsync(pq_count.p, 0, sizeof(int) * nb, stream), "memset");
-        k_pq_count<<<blocks(n, 128), 128, 0, stream>>>(O, st);
-        k_exclusive_scan<<<1, 1024, 0, stream>>>(pq_count.p, nb, pq_total.p);
-        k_pq_scatter<<<blocks(n, 128), 128, 0, stream>>>(st);
+        if (rebuild) {
+          const int nb = 2 * O.NC + O.P + 1;
+          ck(cudaMemsetAsync(pq_count.p, 0, sizeof(int) * nb, stream), "memset");
+          k_pq_count<<<blocks(n, 128), 128, 0, stream>>>(O, st);
+          k_exclusive_scan<<<1, 1024, 0, stream>>>(pq_count.p, nb, pq_total.p);
+          k_pq_scatter<<<blocks(n, 128), 128, 0, stream>>>(st);
+        }
         k_point_query_list<<<blocks(n, GDEV_PQ_BLOCK), GDEV_PQ_BLOCK, 0, stream>>>(O, st);
       });
       return;
@@ -1207,6 +1214,7 @@ struct grasp_ctx {
 
   // The whole synthesis for G grasps whose start states are in x (device).
   void run(const grasp_run_params* p) {
+    pq_age = 0;
     const DevParams P = make_params(p, H.m);
     const grasp_stage_params* scheds[3] = {&p->coarse, &p->fine, &p->final_stage};
     const double offsets[3] = {p->contact_offset, p->contact_offset, 0.0};
@@ -1750,6 +1758,7 @@ int grasp_total_energy(grasp_ctx* ctx, const grasp_run_params* p, int stage, int
         std::vector<int> ready(n, 1);
         ck(cudaMemcpyAsync(ctx->qp_ready.p, ready.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s), "ready");
       }
+      ctx->pq_age = 0;  // rebuild the bucketed list for this state
       ctx->launch_queries(false);
       ctx->launch_qp(P, m, 0, 1);
       ctx->launch_step(P, A, true);

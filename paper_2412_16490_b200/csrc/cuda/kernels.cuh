@@ -1199,6 +1199,7 @@ __global__ void __launch_bounds__(GDEV_PQ_BLOCK, GDEV_PQ_THREADS_PER_SM / GDEV_P
   if (i >= *st.pq_total) return;
   const int t = st.pq_list[i];
   const int g = t / st.NQ;
+  if (st.failed[g]) return;  // (the list may predate the grasp's failure)
   const D3 p = ld3(st.qpts + (size_t)t * 3);
   unsigned planes, tris;
   int* qf = st.qface + t;

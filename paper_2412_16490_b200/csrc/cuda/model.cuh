@@ -117,6 +117,10 @@ struct DevObject {
 #define GDEV_SUPPORT_MAP_MIN_VERTS 24
 #endif
 constexpr int kSupportMapN = GDEV_SUPPORT_MAP_N;
+#ifndef GDEV_PQ_REBUCKET
+#define GDEV_PQ_REBUCKET 4
+#endif
+constexpr int kPqRebucket = GDEV_PQ_REBUCKET;  // coarse point-query list rebuilt every this many iterations
 constexpr int kSupportCells = 6 * kSupportMapN * kSupportMapN;
 constexpr int kSupportMapMinVerts = GDEV_SUPPORT_MAP_MIN_VERTS;
 
