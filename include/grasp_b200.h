@@ -292,7 +292,8 @@ int grasp_ctx_profile(grasp_ctx* ctx, double* ms /*[8]*/, long long* launches /*
  * the GJK pass; default 24, >= 255 off). GRASP_EINVAL for unknown names. */
 int grasp_ctx_set_option(grasp_ctx* ctx, const char* name, int value);
 
-/* Kernels launched by this context so far. */
+/* Kernels launched by synthesis on this context so far (every kernel, all of
+ * a launch group: the pair pass counts its six kernels). */
 long long grasp_ctx_launch_count(grasp_ctx* ctx);
 
 /* Per-iteration trace of the next grasp_synthesize* calls (teacher-forced parity:

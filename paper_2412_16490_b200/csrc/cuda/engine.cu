@@ -177,6 +177,7 @@ struct grasp_ctx {
   // algorithmic op counters only while profiling.
   // point_query, qp, step_coarse, pairs, step_mesh, fk, finalize, pairs_big
   static constexpr int kClasses = 8;
+  long long kernels = 0;  // kernels launched (grasp_ctx_launch_count)
   long long launches[kClasses] = {};
   bool profiling = false;
   double prof_ms[kClasses] = {};
@@ -209,8 +210,9 @@ struct grasp_ctx {
   }
 
   template <class F>
-  void launch(int cls, F&& f) {
+  void launch(int cls, F&& f, int n_kernels = 1) {
     ++launches[cls];
+    kernels += n_kernels;
     if (!profiling) {
       f();
       return;
@@ -1139,7 +1141,7 @@ struct grasp_ctx {
           k_pq_scatter<<<blocks(n, 128), 128, 0, stream>>>(st);
         }
         k_point_query_list<<<blocks(n, GDEV_PQ_BLOCK), GDEV_PQ_BLOCK, 0, stream>>>(O, st);
-      });
+      }, rebuild ? 4 : 1);
       return;
     }
     launch(0, [&] {
@@ -1177,7 +1179,7 @@ struct grasp_ctx {
       // EPA jobs spread over all SMs (32-thread blocks; few jobs per launch)
       k_pairs_epa<<<blocks(std::max<long long>(1024, n / 2), 32), 32, 0, stream>>>(H, O, st);
       ck(cudaStreamWaitEvent(stream, ev_join, 0), "event");
-    });
+    }, 6);
     launch(7, [&] { k_pairs_big<<<kBigSlots / 128, 128, 0, stream>>>(H, O, st); });
   }
   void launch_qp(const DevParams& P, int m, int mode, int with_grad) {
@@ -2087,8 +2089,7 @@ int grasp_ctx_set_option(grasp_ctx* ctx, const char* name, int value) {
 
 long long grasp_ctx_launch_count(grasp_ctx* ctx) {
   long long n = 0;
-  if (ctx)
-    for (long long v : ctx->launches) n += v;
+  if (ctx) n += ctx->kernels;
   if (ctx)
     for (grasp_ctx* sh : ctx->shards) n += grasp_ctx_launch_count(sh);
   return n;

@@ -18,5 +18,6 @@ cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.ite
 eng = G.Engine(0)
 eng.set_hand(hand)
 eng.set_object(obj)
+k0 = eng.launch_count()
 out = eng.synthesize(cfg, G.init_poses(hand, obj, batch, 17))
-print("ok failed", int((out.failed != 0).sum()))
+print("ok failed", int((out.failed != 0).sum()), "kernels", eng.launch_count() - k0)
