@@ -192,6 +192,7 @@ struct grasp_ctx {
       cudaEventDestroy(p.second.first);
       cudaEventDestroy(p.second.second);
     }
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (stream) cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -1215,6 +1216,66 @@ struct grasp_ctx {
   }
 
   // The whole synthesis for G grasps whose start states are in x (device).
+  // run() through a CUDA graph (option "graphs"): the whole synthesis - some
+  // 3000 kernels, memsets and the side-stream fork/join - is captured once per
+  // (hand, object, state buffers, run parameters), keyed by the bytes of the
+  // device descriptors and the parameters (every pointer and size the kernels
+  // see), and replayed with one launch. Profiling and tracing run eagerly.
+  bool use_graphs = true;
+  cudaGraphExec_t graph_exec = nullptr;
+  std::string graph_key;
+  long long graph_kernels = 0, graph_launches[kClasses] = {};
+  void run_graph(const grasp_run_params* p) {
+    if (!use_graphs || profiling || tracing) {
+      run(p);
+      return;
+    }
+    std::string key;
+    key.append(reinterpret_cast<const char*>(&H), sizeof(H));
+    key.append(reinterpret_cast<const char*>(&O), sizeof(O));
+    key.append(reinterpret_cast<const char*>(&st), sizeof(st));
+    key.append(reinterpret_cast<const char*>(p), sizeof(*p));
+    // buffers run() passes directly (not through the descriptors)
+    const void* direct[] = {pq_count.p, pq_total.p, h_tip_slots.p, h_tip_links_sorted.p, ovf_count.p,
+                            pair_count.p, seg_count.p, x_s.p};
+    key.append(reinterpret_cast<const char*>(direct), sizeof(direct));
+    key.append(reinterpret_cast<const char*>(&query_lanes), sizeof(query_lanes));
+    key.append(reinterpret_cast<const char*>(&tip_query_lanes), sizeof(tip_query_lanes));
+    key.append(reinterpret_cast<const char*>(&bucket_queries), sizeof(bucket_queries));
+    if (!graph_exec || key != graph_key) {
+      if (graph_exec) {
+        cudaGraphExecDestroy(graph_exec);
+        graph_exec = nullptr;
+      }
+      const long long k0 = kernels;
+      long long l0[kClasses];
+      std::copy(launches, launches + kClasses, l0);
+      cudaGraph_t g = nullptr;
+      ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "graph capture");
+      try {
+        run(p);
+      } catch (...) {
+        cudaStreamEndCapture(stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      ck(cudaStreamEndCapture(stream, &g), "graph capture");
+      const cudaError_t e = cudaGraphInstantiate(&graph_exec, g, 0);
+      cudaGraphDestroy(g);
+      ck(e, "graph instantiate");
+      graph_key = key;
+      graph_kernels = kernels - k0;
+      for (int c = 0; c < kClasses; ++c) {
+        graph_launches[c] = launches[c] - l0[c];
+        launches[c] = l0[c];
+      }
+      kernels = k0;
+    }
+    ck(cudaGraphLaunch(graph_exec, stream), "graph launch");
+    kernels += graph_kernels;
+    for (int c = 0; c < kClasses; ++c) launches[c] += graph_launches[c];
+  }
+
   void run(const grasp_run_params* p) {
     pq_age = 0;
     const DevParams P = make_params(p, H.m);
@@ -1348,7 +1409,7 @@ int synthesize_impl(grasp_ctx* ctx, const grasp_run_params* p, int batch, const 
                        device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream),
        "x0 copy");
     try {
-      ctx->run(p);
+      ctx->run_graph(p);
       ctx->check_errors();
     } catch (...) {
       ctx->st.obj = nullptr;
@@ -2077,6 +2138,8 @@ int grasp_ctx_set_option(grasp_ctx* ctx, const char* name, int value) {
         c->query_lanes = value;
       } else if (n == "tip_query_lanes" && lanes_ok(value)) {
         c->tip_query_lanes = value;
+      } else if (n == "graphs") {
+        c->use_graphs = value != 0;
       } else if (n == "pair_early" && value >= 0) {
         c->early_pred = value;
         c->st.early_pred = value;

@@ -794,6 +794,42 @@ def test_early_epa_pass_bitwise(G, case):
             assert np.array_equal(getattr(o, f), getattr(ref, f), equal_nan=True), (thr, f)
 
 
+def test_graph_replay_bitwise_equals_eager(G):
+    """Synthesis through a captured CUDA graph (option "graphs", default on: captured once per
+    hand/object/buffers/parameters, then replayed) gives bitwise the eager launches' records,
+    on a replay and after a recapture for new parameters; the kernel count is the same."""
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    hand = G.HandModel.from_file(root / "paper_2412_16490_b200/assets/hands/shadow_like.json")
+    obj = G.load_object(root / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+    cfg = G.RunConfig()
+    cfg.batch, cfg.seed = 96, 41
+    cfg.pipeline.coarse.iters, cfg.pipeline.fine.iters, cfg.pipeline.final_stage.iters = 24, 12, 12
+    fields = ("x", "x_p", "x_s", "energy_total", "stage_energy", "failed", "contacts", "contact_forces")
+
+    def runs(flag, seeds):
+        eng = G.Engine(0)
+        eng.set_hand(hand)
+        eng.set_object(obj)
+        eng.set_option("graphs", flag)
+        outs, counts = [], []
+        for sd in seeds:
+            c = G.RunConfig.from_params(cfg.to_params())
+            c.seed = sd
+            k0 = eng.launch_count()
+            outs.append(eng.synthesize(c, G.init_poses(hand, obj, c.batch, sd, c.init)))
+            counts.append(eng.launch_count() - k0)
+        return outs, counts
+
+    seeds = (41, 41, 7)
+    eager, k_eager = runs(0, seeds)
+    graph, k_graph = runs(1, seeds)
+    assert k_eager == k_graph
+    for e, g in zip(eager, graph):
+        for f in fields:
+            assert np.array_equal(getattr(e, f), getattr(g, f), equal_nan=True), f
+
+
 def test_synthesis_deterministic_and_batch_prefix_independent(G, trident, engine):
     """test_pipeline.cpp:399-421 on the device: the same start states give bitwise-equal
     records on a rerun, and a grasp's record does not depend on the batch it is in
