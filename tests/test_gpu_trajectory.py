@@ -149,6 +149,16 @@ def test_trajectory_parity_config1_allegro(G, O, engine, shape):
     run_trajectory_parity(G, O, engine, hand, obj, 64, 17, f"config1_allegro_{shape}")
 
 
+@pytest.mark.parametrize("shape,scale", [("cylinder", 0.10), ("capsule", 0.06)])
+def test_trajectory_parity_config3_leap(G, O, engine, shape, scale):
+    """BASELINE config 3's hand (Leap-like) on two of its 16 primitives; config 3 runs them all
+    in one multi-object batch, which equals per-object runs bitwise
+    (test_synthesize_objects_equals_per_object_runs)."""
+    hand = G.HandModel.from_file(ROOT / "paper_2412_16490_b200/assets/hands/leap_like.json")
+    obj = G.make_primitive(shape, scale)
+    run_trajectory_parity(G, O, engine, hand, obj, 64, 3, f"config3_leap_{shape}")
+
+
 def test_config2_end_to_end_matches_oracle(G, O, engine):
     """End-to-end on the benchmarked config: GPU synthesize vs the oracle's run_grasp on the same
     x0 (64 grasps, full schedule). Failure flags identical; final energy, stage energies and
