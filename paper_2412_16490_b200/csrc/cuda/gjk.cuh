@@ -361,11 +361,30 @@ GDEV_FN void fullpiv_solve_t(double (&m)[S][S], const double (&rhs)[S], double (
   }
 #pragma unroll
   for (int j = 0; j < S; ++j) sol[j] = 0.0;
+  bool general = true;
+  if constexpr (KKT && S > 2) {
+    // fast path: column transpositions (none, (1, S-1), then among >= 2), so
+    // perm[0] = 0 and perm[1] = S - 1, and rank >= 2 (two unit pivots); the
+    // rest of perm permutes 1 .. S-2
+    if (fast) {
+      general = false;
+      sol[0] = c[0];
+      sol[S - 1] = c[1];
 #pragma unroll
-  for (int i = 0; i < S; ++i) {
-    const double v = i < rank ? c[i] : 0.0;
+      for (int i = 2; i < S; ++i) {
+        const double v = i < rank ? c[i] : 0.0;
 #pragma unroll
-    for (int j = 0; j < S; ++j) sol[j] = (perm[i] == j) ? v : sol[j];
+        for (int j = 1; j < S - 1; ++j) sol[j] = (perm[i] == j) ? v : sol[j];
+      }
+    }
+  }
+  if (general) {
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const double v = i < rank ? c[i] : 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j) sol[j] = (perm[i] == j) ? v : sol[j];
+    }
   }
 }
 
