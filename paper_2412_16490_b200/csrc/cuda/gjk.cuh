@@ -432,94 +432,6 @@ struct Simplex {
   bool contains;
 };
 
-// Cheap classification of one subset (closest_fast's first pass). Solves
-// the same least-norm problem in edge form (w0 + sum s_i e_i, normal
-// equations by Cramer) and bounds its error against the reference's
-// FullPivLU solve of the KKT system: E grows with the conditioning of both
-// (poorly conditioned subsets are never classified). Returns
-//   0  certainly rejected (some weight < -1e-12 by more than E),
-//   1  certainly accepted, with d2 and an error bound err on it,
-//   2  ambiguous.
-template <int K>
-GDEV_FN int cheap_subset(const SP* simp, const int (&idx)[K], double& d2, double& err) {
-  if constexpr (K == 1) {
-    d2 = sqn(simp[idx[0]].w);
-    err = 1e-9 * d2;
-    return 1;
-  } else {
-    constexpr int E_ = K - 1;
-    const D3 w0 = simp[idx[0]].w;
-    D3 e[E_];
-    double A[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, b[3] = {0, 0, 0};
-    double w2max = sqn(w0), emin = INFINITY;
-#pragma unroll
-    for (int i = 0; i < E_; ++i) {
-      e[i] = simp[idx[i + 1]].w - w0;
-      w2max = fmax(w2max, sqn(simp[idx[i + 1]].w));
-    }
-#pragma unroll
-    for (int i = 0; i < E_; ++i) {
-#pragma unroll
-      for (int j = 0; j < E_; ++j) A[i][j] = dot(e[i], e[j]);
-      b[i] = -dot(w0, e[i]);
-      emin = fmin(emin, A[i][i]);
-    }
-    if (!(emin > 0.0)) return 2;
-    double s[3] = {0, 0, 0}, kappa;
-    if constexpr (E_ == 1) {
-      s[0] = b[0] / A[0][0];
-      kappa = 1.0;
-    } else if constexpr (E_ == 2) {
-      const double det = A[0][0] * A[1][1] - A[0][1] * A[1][0];
-      if (!(det > 1e-6 * A[0][0] * A[1][1])) return 2;
-      const double inv = 1.0 / det;
-      s[0] = (b[0] * A[1][1] - b[1] * A[0][1]) * inv;
-      s[1] = (A[0][0] * b[1] - A[1][0] * b[0]) * inv;
-      kappa = (A[0][0] + A[1][1]) * (A[0][0] + A[1][1]) * inv;
-    } else {
-      const double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1];
-      const double c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2];
-      const double c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
-      const double det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
-      if (!(det > 1e-6 * A[0][0] * A[1][1] * A[2][2])) return 2;
-      const double c11 = A[0][0] * A[2][2] - A[0][2] * A[2][0];
-      const double c12 = A[0][1] * A[2][0] - A[0][0] * A[2][1];
-      const double c22 = A[0][0] * A[1][1] - A[0][1] * A[1][0];
-      const double c10 = A[0][2] * A[2][1] - A[0][1] * A[2][2];
-      const double c20 = A[0][1] * A[1][2] - A[0][2] * A[1][1];
-      const double c21 = A[0][2] * A[1][0] - A[0][0] * A[1][2];
-      const double inv = 1.0 / det;
-      s[0] = (c00 * b[0] + c10 * b[1] + c20 * b[2]) * inv;
-      s[1] = (c01 * b[0] + c11 * b[1] + c21 * b[2]) * inv;
-      s[2] = (c02 * b[0] + c12 * b[1] + c22 * b[2]) * inv;
-      const double tr = A[0][0] + A[1][1] + A[2][2];
-      kappa = tr * tr * tr * inv;
-    }
-    double l0 = 1.0, lmax = 0.0, lmin = INFINITY;
-#pragma unroll
-    for (int i = 0; i < E_; ++i) {
-      l0 -= s[i];
-      lmax = fmax(lmax, fabs(s[i]));
-      lmin = fmin(lmin, s[i]);
-    }
-    lmax = fmax(lmax, fabs(l0));
-    lmin = fmin(lmin, l0);
-    // Error bound on |lam_cheap - lam_LU|: both solves carry ~eps * cond; the
-    // KKT form used by FullPivLU degrades with |w|^2 / |e|^2.
-    const double cond = kappa * fmax(1.0, w2max / emin);
-    if (!(cond < 1e6)) return 2;
-    const double E = 1e-9 * (1.0 + lmax) * fmax(1.0, cond * 1e-3);
-    if (lmin < -1e-12 - E) return 0;
-    if (!(lmin >= -1e-12 + E)) return 2;
-    D3 v = w0;
-#pragma unroll
-    for (int i = 0; i < E_; ++i) v += s[i] * e[i];
-    d2 = sqn(v);
-    err = 1e-9 * w2max * (1.0 + lmax) * fmax(1.0, cond * 1e-3);
-    return 1;
-  }
-}
-
 // One subset of closest_on_simplex (geometry.cpp:61-93): solve the
 // (K+1)x(K+1) affine least-norm KKT system for the gathered points P[0..K)
 // (original simplex indices id[0..K)) and apply the acceptance and tie rules
@@ -640,7 +552,6 @@ GDEV_FN Simplex closest_on_simplex(const SP* simp, int n) {
   return best;
 }
 
-GDEV_FN Simplex closest_on_simplex_var(const SP* simp, int n) { return closest_on_simplex(simp, n); }
 
 struct PairResult {
   double d;
