@@ -9,5 +9,5 @@ for lib in default "$@"; do
 import json,sys; d=json.loads(open('gpurun_out/ab_$lib.json').read().strip().splitlines()[-1])
 o = d['roofline'].get('ops', {}); q = max(1, o.get('point_queries', 1))
 print('$lib', d['value'], {k: round(v,1) for k,v in d['roofline']['kernel_ms'].items()},
-      {k: round(o.get(k, 0) / q, 2) for k in ('plane_tests', 'triangle_tests', 'grid_part_queries', 'scan_part_queries')})" >> gpurun_out/ab.log
+      {k: round(o.get(k, 0) / q, 2) for k in ('plane_tests', 'triangle_tests')})" >> gpurun_out/ab.log
 done
