@@ -122,6 +122,27 @@ def test_point_queries_multipart(G, O, trident, engine):
     np.testing.assert_allclose(got[:, :7], ref[:, :7], atol=1e-9, rtol=0)
 
 
+def test_point_queries_drill_match_oracle(G, O, trident):
+    """The drill mesh (6 parts, long strip faces) through the spatial point-query face order and
+    the normal plane groups: points on shells from inside to 0.3 m out, plus a cloud near the
+    surface; part index and values agree with the oracle's index-order scan."""
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    obj = G.load_object(root / "paper_2412_16490_b200/assets/objects/drill_like.obj", 0.10)
+    eng = G.Engine(0)
+    eng.set_hand(trident)
+    eng.set_object(obj)
+    rng = np.random.default_rng(12)
+    d = rng.normal(size=(8000, 3))
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    pts = np.concatenate([d * rng.uniform(0.0, 0.3, 8000)[:, None], rng.normal(size=(4000, 3)) * 0.03])
+    ref = O.point_to_mesh(obj, pts)
+    got = gpu_points(eng, pts)
+    assert (got[:, 7] == ref[:, 7]).all()
+    assert np.array_equal(got[:, 0] < 0, ref[:, 0] < 0)
+    np.testing.assert_allclose(got[:, :7], ref[:, :7], atol=1e-9, rtol=0)
+
+
 WARM_START_SCRIPT = r'''
 import ctypes as C, sys
 import numpy as np
