@@ -101,7 +101,7 @@ struct grasp_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool has_hand = false, has_object = false;
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
-  DevBuf<int> pq_key, pq_list, pq_total, pq_count;
+  DevBuf<int> pq_key, pq_list, pq_total, pq_count, pq_split;
   // Engine options (grasp_ctx_set_option; defaults = the product settings).
   bool bucket_queries = true;  // "query_buckets": coarse queries listed by spatial bucket
   long long pq_age = 0;        // launches since the bucketed list was rebuilt (0: rebuild)
@@ -997,7 +997,8 @@ struct grasp_ctx {
     pq_key.ensure(g * NQ);
     pq_list.ensure(g * NQ);
     pq_total.ensure(1);
-    pq_count.ensure(static_cast<size_t>(has_object ? 2 * O.NC + O.P + 1 : 1));
+    pq_count.ensure(static_cast<size_t>(has_object ? 2 * (2 * O.NC + O.P + 1) : 1));
+    pq_split.ensure(1);
     st.pq_key = pq_key.p;
     st.pq_list = pq_list.p;
     st.pq_total = pq_total.p;
@@ -1134,15 +1135,22 @@ struct grasp_ctx {
       // start of a run): points move little per iteration.
       const bool rebuild = pq_age++ % kPqRebucket == 0;
       launch(0, [&] {
+        const int nb1 = 2 * O.NC + O.P + 1;
         if (rebuild) {
-          const int nb = 2 * O.NC + O.P + 1;
-          ck(cudaMemsetAsync(pq_count.p, 0, sizeof(int) * nb, stream), "memset");
-          k_pq_count<<<blocks(n, 128), 128, 0, stream>>>(O, st);
-          k_exclusive_scan<<<1, 1024, 0, stream>>>(pq_count.p, nb, pq_total.p);
+          ck(cudaMemsetAsync(pq_count.p, 0, sizeof(int) * 2 * nb1, stream), "memset");
+          k_pq_count<<<blocks(n, 128), 128, 0, stream>>>(H, O, st);
+          k_exclusive_scan<<<1, 1024, 0, stream>>>(pq_count.p, 2 * nb1, pq_total.p, nb1, pq_split.p);
           k_pq_scatter<<<blocks(n, 128), 128, 0, stream>>>(st);
         }
-        k_point_query_list<<<blocks(n, GDEV_PQ_BLOCK), GDEV_PQ_BLOCK, 0, stream>>>(O, st);
-      }, rebuild ? 4 : 1);
+        // the other proxies (read by the step kernel only) on the side
+        // stream next to the QP; the step joins (launch_step)
+        ck(cudaEventRecord(ev_fork, stream), "event");
+        ck(cudaStreamWaitEvent(side, ev_fork, 0), "event");
+        k_point_query_list<<<blocks(n, GDEV_PQ_BLOCK), GDEV_PQ_BLOCK, 0, side>>>(O, st, pq_split.p, pq_total.p);
+        ck(cudaEventRecord(ev_join, side), "event");
+        k_point_query_list<<<blocks(n, GDEV_PQ_BLOCK), GDEV_PQ_BLOCK, 0, stream>>>(O, st, nullptr, pq_split.p);
+      }, rebuild ? 5 : 2);
+      queries_forked = true;
       return;
     }
     launch(0, [&] {
@@ -1189,7 +1197,14 @@ struct grasp_ctx {
   void launch_fk(const DevParams& P) {
     launch(5, [&] { k_fk<<<blocks(st.G, 2), 64, 0, stream>>>(H, P, st); });
   }
+  bool queries_forked = false;  // side-stream point queries not joined yet
+  void join_queries() {
+    if (!queries_forked) return;
+    ck(cudaStreamWaitEvent(stream, ev_join, 0), "event");
+    queries_forked = false;
+  }
   void launch_step(const DevParams& P, const StageArgs& A, bool coarse) {
+    join_queries();
     if (coarse)
       launch(2, [&] { k_step_coarse<<<blocks(st.G, 2), 64, 0, stream>>>(H, P, A, st); });
     else
@@ -1236,7 +1251,7 @@ struct grasp_ctx {
     key.append(reinterpret_cast<const char*>(&st), sizeof(st));
     key.append(reinterpret_cast<const char*>(p), sizeof(*p));
     // buffers run() passes directly (not through the descriptors)
-    const void* direct[] = {pq_count.p, pq_total.p, h_tip_slots.p, h_tip_links_sorted.p, ovf_count.p,
+    const void* direct[] = {pq_count.p, pq_total.p, pq_split.p, h_tip_slots.p, h_tip_links_sorted.p, ovf_count.p,
                             pair_count.p, seg_count.p, x_s.p};
     key.append(reinterpret_cast<const char*>(direct), sizeof(direct));
     key.append(reinterpret_cast<const char*>(&query_lanes), sizeof(query_lanes));
@@ -1326,6 +1341,7 @@ struct grasp_ctx {
     launch_qp(P, H.m, 1, 0);
     launch(6, [&] { k_squeeze<<<blocks(st.G, 128), 128, 0, stream>>>(H, st, x_s.p); });
     launch(6, [&] { k_mask_failed<<<blocks(st.G, 128), 128, 0, stream>>>(H, st, p->n_edges); });
+    join_queries();
     ck(cudaGetLastError(), "kernel launch");
     collect_profile();
     if (tracing) trace_flush(nv, Mq);

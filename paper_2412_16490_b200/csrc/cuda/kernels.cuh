@@ -1135,6 +1135,17 @@ __global__ void __launch_bounds__(128) k_pairs_scatter(DevState st, const int* _
 // queries with the same path through point_to_mesh (same parts culled, same
 // clusters scanned, same inside test) into the same warps. Which thread runs
 // a query does not change its result, so the order is free.
+// Query class: 0 = what the QP reads (tip proxies and their FD stencils),
+// 1 = the other proxies (read by the step kernel only), listed after class 0
+// so the two can run as separate launches (class 1 next to the QP).
+__device__ __forceinline__ int pq_class(const DevHand& H, const DevState& st, size_t t) {
+  const int slot = (int)(t % st.NQ);
+  if (slot >= H.S) return 0;
+  for (int f = 0; f < H.m; ++f)
+    if (__ldg(H.tip_proxy + f) == slot) return 0;
+  return 1;
+}
+
 __device__ __forceinline__ int pq_bucket(const DevObject& O, const DevState& st, size_t t) {
   const int f = st.qface[t];
   const double d = st.qres[t * 8];
@@ -1146,21 +1157,23 @@ __device__ __forceinline__ int pq_bucket(const DevObject& O, const DevState& st,
   return 2 * O.NC + O.P;
 }
 
-__global__ void __launch_bounds__(128) k_pq_count(DevObject O, DevState st) {
+__global__ void __launch_bounds__(128) k_pq_count(DevHand H, DevObject O, DevState st) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long n = (long long)st.G * st.NQ;
   bool active = false;
   int key = 0;
   if (t < n) {
     active = !st.failed[t / st.NQ];
-    if (active) key = pq_bucket(O, st, (size_t)t);
+    if (active) key = pq_bucket(O, st, (size_t)t) + pq_class(H, st, (size_t)t) * (2 * O.NC + O.P + 1);
     st.pq_key[t] = active ? key : -1;
   }
   warp_segment_add(st.pq_count, key, active);
 }
 
 // Exclusive scan of n counts in place (one block); *total = their sum.
-__global__ void __launch_bounds__(1024) k_exclusive_scan(int* counts, int n, int* total) {
+// split_out (optional): the exclusive prefix at index split_at (0 <= split_at <= n).
+__global__ void __launch_bounds__(1024) k_exclusive_scan(int* counts, int n, int* total, int split_at = -1,
+                                                         int* split_out = nullptr) {
   __shared__ int part_sum[1024];
   const int tid = threadIdx.x;
   const int per = (n + 1023) / 1024;
@@ -1178,10 +1191,14 @@ __global__ void __launch_bounds__(1024) k_exclusive_scan(int* counts, int n, int
   int run = part_sum[tid] - s;
   for (int i = b; i < e; ++i) {
     const int c = counts[i];
+    if (split_out && i == split_at) *split_out = run;
     counts[i] = run;
     run += c;
   }
-  if (tid == 1023) *total = part_sum[1023];
+  if (tid == 1023) {
+    *total = part_sum[1023];
+    if (split_out && split_at == n) *split_out = part_sum[1023];
+  }
 }
 
 __global__ void __launch_bounds__(128) k_pq_scatter(DevState st) {
@@ -1194,9 +1211,11 @@ __global__ void __launch_bounds__(128) k_pq_scatter(DevState st) {
 }
 
 // k_point_query over the bucketed list.
-__global__ void __launch_bounds__(GDEV_PQ_BLOCK, GDEV_PQ_THREADS_PER_SM / GDEV_PQ_BLOCK) k_point_query_list(DevObject O, DevState st) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= *st.pq_total) return;
+// Entries [*begin, *end) of the bucketed list (begin == nullptr: 0).
+__global__ void __launch_bounds__(GDEV_PQ_BLOCK, GDEV_PQ_THREADS_PER_SM / GDEV_PQ_BLOCK) k_point_query_list(
+    DevObject O, DevState st, const int* begin, const int* end) {
+  const int i = (begin ? *begin : 0) + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *end) return;
   const int t = st.pq_list[i];
   const int g = t / st.NQ;
   if (st.failed[g]) return;  // (the list may predate the grasp's failure)
