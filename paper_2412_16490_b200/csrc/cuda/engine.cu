@@ -98,7 +98,7 @@ struct grasp_ctx {
   std::vector<grasp_ctx*> shards;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // k_pairs_early, forked from and joined back into `stream`
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_qfork = nullptr;
   bool has_hand = false, has_object = false;
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
   DevBuf<int> pq_key, pq_list, pq_total, pq_count, pq_split;
@@ -197,6 +197,7 @@ struct grasp_ctx {
     if (side) cudaStreamDestroy(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_qfork) cudaEventDestroy(ev_qfork);
   }
 
   cudaEvent_t take_event() {
@@ -1153,16 +1154,28 @@ struct grasp_ctx {
       queries_forked = true;
       return;
     }
+    // Tip-centre queries with the pair cull off (the default): the pair pass
+    // does not read them (pair_needed), only the step kernel and the final
+    // frames do, so they run on the side stream next to the pair pass (ahead
+    // of k_pairs_early there; launch_pairs joins the side stream).
+    const bool fork = tips_only && !H.cull;
+    cudaStream_t qs = fork ? side : stream;
     launch(0, [&] {
-      switch (L) {
-        case 2: k_point_query_group<2><<<blocks(n * 2, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, stream>>>(O, st, sl, per); break;
-        case 4: k_point_query_group<4><<<blocks(n * 4, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, stream>>>(O, st, sl, per); break;
-        case 8: k_point_query_group<8><<<blocks(n * 8, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, stream>>>(O, st, sl, per); break;
-        case 16: k_point_query_group<16><<<blocks(n * 16, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, stream>>>(O, st, sl, per); break;
-        case 32: k_point_query_group<32><<<blocks(n * 32, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, stream>>>(O, st, sl, per); break;
-        default: k_point_query<<<blocks(n, GDEV_PQ_BLOCK), GDEV_PQ_BLOCK, 0, stream>>>(O, st, sl, per);
+      if (fork) {
+        ck(cudaEventRecord(ev_qfork, stream), "event");
+        ck(cudaStreamWaitEvent(side, ev_qfork, 0), "event");
       }
+      switch (L) {
+        case 2: k_point_query_group<2><<<blocks(n * 2, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, qs>>>(O, st, sl, per); break;
+        case 4: k_point_query_group<4><<<blocks(n * 4, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, qs>>>(O, st, sl, per); break;
+        case 8: k_point_query_group<8><<<blocks(n * 8, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, qs>>>(O, st, sl, per); break;
+        case 16: k_point_query_group<16><<<blocks(n * 16, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, qs>>>(O, st, sl, per); break;
+        case 32: k_point_query_group<32><<<blocks(n * 32, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, qs>>>(O, st, sl, per); break;
+        default: k_point_query<<<blocks(n, GDEV_PQ_BLOCK), GDEV_PQ_BLOCK, 0, qs>>>(O, st, sl, per);
+      }
+      if (fork) ck(cudaEventRecord(ev_join, side), "event");
     });
+    if (fork) queries_forked = true;
   }
   void launch_pairs(bool tips_only) {
     const int nl = tips_only ? H.m : H.L;
@@ -1293,6 +1306,7 @@ struct grasp_ctx {
 
   void run(const grasp_run_params* p) {
     pq_age = 0;
+    queries_forked = false;  // (earlier forks were joined by their pair pass or step)
     const DevParams P = make_params(p, H.m);
     const grasp_stage_params* scheds[3] = {&p->coarse, &p->fine, &p->final_stage};
     const double offsets[3] = {p->contact_offset, p->contact_offset, 0.0};
@@ -1454,6 +1468,7 @@ int grasp_ctx_create(int device, grasp_ctx** out) {
       ck(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "cudaStreamCreate");
       ck(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
       ck(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventCreateWithFlags(&ctx->ev_qfork, cudaEventDisableTiming), "cudaEventCreate");
       // No cudaDeviceSetLimit(cudaLimitStackSize): the EPA kernels' local
       // polytopes are static frames (<= 11.8 KB/thread, ptxas), which the
       // driver provisions per launch; a device-wide limit would reserve that
