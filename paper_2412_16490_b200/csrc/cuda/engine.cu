@@ -98,7 +98,9 @@ struct grasp_ctx {
   std::vector<grasp_ctx*> shards;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // k_pairs_early, forked from and joined back into `stream`
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_qfork = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_qfork = nullptr, ev_qjoin = nullptr;
+  cudaStream_t side_q = nullptr;  // the mesh stages' tip queries (next to the pair pass)
+  bool tips_forked = false;
   bool has_hand = false, has_object = false;
   DevBuf<int> pair_count, pair_list, seg_count, seg_offset;
   DevBuf<int> pq_key, pq_list, pq_total, pq_count, pq_split;
@@ -198,6 +200,8 @@ struct grasp_ctx {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_qfork) cudaEventDestroy(ev_qfork);
+    if (ev_qjoin) cudaEventDestroy(ev_qjoin);
+    if (side_q) cudaStreamDestroy(side_q);
   }
 
   cudaEvent_t take_event() {
@@ -1159,11 +1163,11 @@ struct grasp_ctx {
     // frames do, so they run on the side stream next to the pair pass (ahead
     // of k_pairs_early there; launch_pairs joins the side stream).
     const bool fork = tips_only && !H.cull;
-    cudaStream_t qs = fork ? side : stream;
+    cudaStream_t qs = fork ? side_q : stream;
     launch(0, [&] {
       if (fork) {
         ck(cudaEventRecord(ev_qfork, stream), "event");
-        ck(cudaStreamWaitEvent(side, ev_qfork, 0), "event");
+        ck(cudaStreamWaitEvent(side_q, ev_qfork, 0), "event");
       }
       switch (L) {
         case 2: k_point_query_group<2><<<blocks(n * 2, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, qs>>>(O, st, sl, per); break;
@@ -1173,9 +1177,9 @@ struct grasp_ctx {
         case 32: k_point_query_group<32><<<blocks(n * 32, GDEV_PQG_BLOCK), GDEV_PQG_BLOCK, 0, qs>>>(O, st, sl, per); break;
         default: k_point_query<<<blocks(n, GDEV_PQ_BLOCK), GDEV_PQ_BLOCK, 0, qs>>>(O, st, sl, per);
       }
-      if (fork) ck(cudaEventRecord(ev_join, side), "event");
+      if (fork) ck(cudaEventRecord(ev_qjoin, side_q), "event");
     });
-    if (fork) queries_forked = true;
+    if (fork) tips_forked = true;
   }
   void launch_pairs(bool tips_only) {
     const int nl = tips_only ? H.m : H.L;
@@ -1212,9 +1216,9 @@ struct grasp_ctx {
   }
   bool queries_forked = false;  // side-stream point queries not joined yet
   void join_queries() {
-    if (!queries_forked) return;
-    ck(cudaStreamWaitEvent(stream, ev_join, 0), "event");
-    queries_forked = false;
+    if (queries_forked) ck(cudaStreamWaitEvent(stream, ev_join, 0), "event");
+    if (tips_forked) ck(cudaStreamWaitEvent(stream, ev_qjoin, 0), "event");
+    queries_forked = tips_forked = false;
   }
   void launch_step(const DevParams& P, const StageArgs& A, bool coarse) {
     join_queries();
@@ -1306,7 +1310,7 @@ struct grasp_ctx {
 
   void run(const grasp_run_params* p) {
     pq_age = 0;
-    queries_forked = false;  // (earlier forks were joined by their pair pass or step)
+    queries_forked = tips_forked = false;  // (earlier forks were joined by their step or eval)
     const DevParams P = make_params(p, H.m);
     const grasp_stage_params* scheds[3] = {&p->coarse, &p->fine, &p->final_stage};
     const double offsets[3] = {p->contact_offset, p->contact_offset, 0.0};
@@ -1349,6 +1353,7 @@ struct grasp_ctx {
     launch_fk(P);
     launch_queries(true);
     launch_pairs(true);
+    join_queries();
     launch(6, [&] {
       k_final_frames<<<blocks(static_cast<long long>(st.G) * H.m, 128), 128, 0, stream>>>(H, O, st, nullptr);
     });
@@ -1469,6 +1474,8 @@ int grasp_ctx_create(int device, grasp_ctx** out) {
       ck(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
       ck(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "cudaEventCreate");
       ck(cudaEventCreateWithFlags(&ctx->ev_qfork, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventCreateWithFlags(&ctx->ev_qjoin, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaStreamCreateWithFlags(&ctx->side_q, cudaStreamNonBlocking), "cudaStreamCreate");
       // No cudaDeviceSetLimit(cudaLimitStackSize): the EPA kernels' local
       // polytopes are static frames (<= 11.8 KB/thread, ptxas), which the
       // driver provisions per launch; a device-wide limit would reserve that
@@ -1633,6 +1640,7 @@ int grasp_eval(grasp_ctx* ctx, const grasp_run_params* p, const grasp_eval_param
     k_eval_depths<<<grasp_ctx::blocks(n, 128), 128, 0, s>>>(ctx->H, ctx->O, ctx->st, self_d.p, pd.p, spd.p);
     ctx->launch_queries(true);
     ctx->launch_pairs(true);
+    ctx->join_queries();  // (tip queries may run on their own stream)
     k_final_frames<<<grasp_ctx::blocks(static_cast<long long>(n) * m, 128), 128, 0, s>>>(ctx->H, ctx->O, ctx->st,
                                                                                       ctx->witness.p);
     ck(cudaGetLastError(), "launch");
@@ -1646,6 +1654,7 @@ int grasp_eval(grasp_ctx* ctx, const grasp_run_params* p, const grasp_eval_param
     ctx->launch_fk(P);
     ctx->launch_queries(true);
     ctx->launch_pairs(true);
+    ctx->join_queries();  // (tip queries may run on their own stream)
     k_final_frames<<<grasp_ctx::blocks(static_cast<long long>(n) * m, 128), 128, 0, s>>>(ctx->H, ctx->O, ctx->st,
                                                                                       ctx->witness.p);
     ck(cudaGetLastError(), "launch");
@@ -1925,6 +1934,7 @@ int grasp_fine_contact_query_world(grasp_ctx* ctx, int n, const double* world, d
     k_tip_points<<<grasp_ctx::blocks(static_cast<long long>(n) * ctx->H.m, 128), 128, 0, s>>>(ctx->H, ctx->st);
     ctx->launch_queries(true);
     ctx->launch_pairs(true);
+    ctx->join_queries();  // (tip queries may run on their own stream)
     k_final_frames<<<grasp_ctx::blocks(static_cast<long long>(n) * ctx->H.m, 128), 128, 0, s>>>(ctx->H, ctx->O, ctx->st,
                                                                                               ctx->witness.p);
     ck(cudaGetLastError(), "launch");
@@ -1949,6 +1959,7 @@ int grasp_fine_contact_query(grasp_ctx* ctx, int n, const double* x, double* out
     ctx->launch_fk(P);
     ctx->launch_queries(true);
     ctx->launch_pairs(true);
+    ctx->join_queries();  // (tip queries may run on their own stream)
     k_final_frames<<<grasp_ctx::blocks(static_cast<long long>(n) * ctx->H.m, 128), 128, 0, s>>>(ctx->H, ctx->O, ctx->st,
                                                                                               ctx->witness.p);
     ck(cudaGetLastError(), "launch");
