@@ -274,6 +274,7 @@ def run_ours(args):
     shard_cfg = dataclasses.replace(cfg, batch=B)
 
     eng = G.Engine(local)
+    eng.set_option("graphs", 1)  # one context per GPU: the synthesis replays as one CUDA graph
     eng.set_hand(hand)
     eng.set_object(obj)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)

@@ -58,6 +58,7 @@ def run(steps=2, warmup=2, grasps=1024, mode="single", rank=0, world=1, local=0,
     failed = [0]
     if mode == "single":
         eng = G.Engine(local)
+        eng.set_option("graphs", 1)  # one context: the synthesis replays as one CUDA graph
         eng.set_hand(hand)
         eng.set_objects([o[3] for o in mine])
         x0 = np.concatenate([G.init_poses(hand, o[3], B, o[0], cfg.init) for o in mine])

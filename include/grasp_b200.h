@@ -290,8 +290,9 @@ int grasp_ctx_profile(grasp_ctx* ctx, double* ms /*[8]*/, long long* launches /*
  * link-box vs part-box test, default 1), "pair_early" (pairs whose last EPA
  * ran more than this many iterations run GJK + EPA on a side stream next to
  * the GJK pass; default 24, >= 255 off), "graphs" (1: a synthesis runs as a
- * captured CUDA graph, recaptured when the models, buffers or parameters
- * change; 0: eager launches). GRASP_EINVAL for unknown names. */
+ * captured CUDA graph, cached per models, buffers and parameters; 0, the
+ * default: eager launches, better when several contexts share a device).
+ * GRASP_EINVAL for unknown names. */
 int grasp_ctx_set_option(grasp_ctx* ctx, const char* name, int value);
 
 /* Kernels launched by synthesis on this context so far (every kernel, all of

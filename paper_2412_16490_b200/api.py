@@ -560,7 +560,7 @@ class Engine:
     def set_option(self, name: str, value: int) -> None:
         """grasp_ctx_set_option: "query_buckets", "query_lanes", "tip_query_lanes", "pair_cull", "pair_sat",
         "pair_early" (EPA-iteration threshold for the early GJK+EPA pass; >= 255 turns it off),
-        "graphs" (1: synthesis as a captured CUDA graph, the default; 0: eager launches)."""
+        "graphs" (1: synthesis as a captured CUDA graph; 0, the default: eager launches)."""
         N.check(N.lib().grasp_ctx_set_option(self._ctx, name.encode(), int(value)))
 
     def set_profiling(self, on: bool) -> None:
