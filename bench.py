@@ -129,6 +129,8 @@ NCU_CAPTURES = {
     "pairs": "profiles/r02_ncu_pairs_list_full.json",
     "qp": "profiles/r02_ncu_qp_full.json",
     "point_query": "profiles/r02_ncu_point_query_full.json",
+    "step_coarse": "profiles/r02_ncu_step_coarse_full.json",
+    "step_mesh": "profiles/r02_ncu_step_mesh_full.json",
 }
 
 
