@@ -1549,11 +1549,13 @@ struct LinkAcc {
 };
 
 // Adds one chunk of up to 32 items (item lane t owns itL/itF/itT[t]) to the
-// per-link accumulator held by lane == link. Fixed item order.
+// per-link accumulator held by lane == link. Fixed item order; only the lanes
+// holding an item (itL >= 0, each lane wrote its own slot) are visited.
 __device__ __forceinline__ void flush_items(WarpScratch& s, int lane, LinkAcc& acc, bool any) {
   __syncwarp();
   if (any) {
-    for (int i = 0; i < 32; ++i) {
+    for (unsigned m = __ballot_sync(kFull, s.itL[lane] >= 0); m; m &= m - 1) {
+      const int i = __ffs(m) - 1;
       if (s.itL[i] == lane) {
         acc.F += ld3(s.itF + 3 * i);
         acc.T += ld3(s.itT + 3 * i);
@@ -1561,6 +1563,18 @@ __device__ __forceinline__ void flush_items(WarpScratch& s, int lane, LinkAcc& a
     }
   }
   __syncwarp();
+}
+
+// Adds a chunk of per-lane energy terms to lane 0's running total in lane
+// order (the reference's sequential sum). Zero terms are skipped: the total
+// starts at +0 and x + 0 == x for every x other than -0, which a sum from +0
+// never reaches, so the result is bitwise the full sequential sum.
+__device__ __forceinline__ void add_terms(WarpScratch& s, int lane, double term, double& total) {
+  const unsigned nz = __ballot_sync(kFull, term != 0.0);
+  s.red[lane] = term;
+  __syncwarp();
+  if (lane == 0)
+    for (unsigned m = nz; m; m &= m - 1) total += s.red[__ffs(m) - 1];
 }
 
 __device__ __forceinline__ void put_item(WarpScratch& s, int lane, int link, D3 pw, D3 fw) {
@@ -1755,10 +1769,7 @@ __global__ void __launch_bounds__(64) k_step_coarse(DevHand H, DevParams P, Stag
       s.itL[lane] = -1;
     }
     // Energy in reference order: sequential over proxies.
-    s.red[lane] = term;
-    __syncwarp();
-    if (lane == 0)
-      for (int i = 0; i < 32 && base + i < H.S; ++i) total += s.red[i];
+    add_terms(s, lane, term, total);
     if (with_grad) flush_items(s, lane, acc, __any_sync(kFull, active));
     __syncwarp();
   }
@@ -1866,10 +1877,7 @@ __global__ void __launch_bounds__(64) k_step_mesh(DevHand H, DevObject O, DevPar
         if (with_grad) put_item(s, lane, t / O.Pmax, ld3(pr + (size_t)t * 12 + 1), (P.w_pen * 2.0 * d) * ld3(pr + (size_t)t * 12 + 7));
       }
     }
-    s.red[lane] = term;
-    __syncwarp();
-    if (lane == 0)
-      for (int i = 0; i < 32 && base + i < npairs; ++i) total += s.red[i];
+    add_terms(s, lane, term, total);
     if (with_grad) flush_items(s, lane, acc, __any_sync(kFull, active));
     __syncwarp();
   }
