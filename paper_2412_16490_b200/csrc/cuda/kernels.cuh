@@ -1589,10 +1589,15 @@ __device__ __forceinline__ void put_item(WarpScratch& s, int lane, int link, D3 
 // Expands per-link accumulators into the state gradient s.grad (adds to the
 // limit gradient already there).
 __device__ inline void expand_gradient(const DevHand& H, WarpScratch& s, int lane, const LinkAcc& acc) {
-  // Totals and per-joint subtree sums, fixed link order.
+  // Totals and per-joint subtree sums, fixed link order. Links whose
+  // accumulator is all zeros are skipped: the sums start at +0 and adding an
+  // exact zero changes no value other than -0, which they never reach.
   D3 Ftot = mk(0, 0, 0), Ttot = mk(0, 0, 0), Fsub = mk(0, 0, 0), Tsub = mk(0, 0, 0);
   const unsigned sub = lane < H.dof ? H.joint_subtree[lane] : 0u;
-  for (int l = 0; l < H.L; ++l) {
+  const bool nz = lane < H.L && (acc.F.x != 0.0 || acc.F.y != 0.0 || acc.F.z != 0.0 || acc.T.x != 0.0 ||
+                                 acc.T.y != 0.0 || acc.T.z != 0.0);
+  for (unsigned m = __ballot_sync(kFull, nz); m; m &= m - 1) {
+    const int l = __ffs(m) - 1;
     const D3 F = mk(__shfl_sync(kFull, acc.F.x, l), __shfl_sync(kFull, acc.F.y, l), __shfl_sync(kFull, acc.F.z, l));
     const D3 T = mk(__shfl_sync(kFull, acc.T.x, l), __shfl_sync(kFull, acc.T.y, l), __shfl_sync(kFull, acc.T.z, l));
     Ftot += F;
